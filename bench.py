@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 M-step solver (BASELINE.json metric: solver
+voxel-iterations/s at 512^3, time-to-tolerance, % HBM roofline per iteration).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+A step = one m_step solve of --iters ISTA iterations (the reference's default
+semantics: lipschitz step, per-inner reweighting, monotone audit every
+iteration) over the resident 512^3 synthetic problem (synth.py).
+value = N^3 * iters * steps / device time (CUDA events), inputs resident in HBM.
+e2e   = the same through the C ABI call cm_m_step with pinned HOST buffers
+        (full-grid fp64 accumulator + volume H2D, result D2H inside the timing).
+Under torchrun each rank solves its own replica (weak scaling, no data-path
+collective: SURVEY §8(e) config 5 "replicas only").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--iters", type=int, default=100, help="ISTA iterations per step")
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--cpu-n", type=int, default=256, help="CPU-baseline sample side")
+    ap.add_argument("--cpu-iters", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ttt", type=int, default=1, help="measure time-to-tolerance (0/1)")
+    ap.add_argument("--ttt-max-iters", type=int, default=6000)
+    ap.add_argument("--tol", type=float, default=1e-6)
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", HBM_FALLBACK_GBS)), "measured"
+    return HBM_FALLBACK_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [q.strip() for q in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_problem(n: int, rank: int, world: int):
+    """Rank 0 generates (synth.py); other ranks memory-map the same bytes."""
+    from paper_1905_13408_b200 import synth
+
+    if world == 1:
+        return synth.synthetic_problem(n)
+    cache = Path(f"/tmp/cm_bench_problem_{n}")
+    if rank == 0:
+        p = synth.synthetic_problem(n)
+        cache.mkdir(exist_ok=True)
+        for k in ("truth", "weight", "numerator", "x0"):
+            np.save(cache / f"{k}.npy", getattr(p, k))
+        (cache / "meta.json").write_text(json.dumps({"eps": p.eps, "eps_prime": p.eps_prime}))
+    barrier(world)
+    if rank != 0:
+        meta = json.loads((cache / "meta.json").read_text())
+        arr = {k: np.load(cache / f"{k}.npy") for k in ("truth", "weight", "numerator", "x0")}
+        p = synth.Problem(n, arr["truth"], arr["weight"], arr["numerator"], arr["x0"],
+                          meta["eps"], meta["eps_prime"])
+    return p
+
+
+# ---- algorithmic bytes per launch ------------------------------
+def kernel_bytes(n: int, rsize: int, audit_prev: bool):
+    """Algorithmic HBM bytes per launch of each per-iteration kernel, packed
+    half spectrum (H' = n^2 * n/2 complex) and real volumes of L = n^3."""
+    L = n ** 3
+    c = 2 * rsize            # complex element
+    Hp = n * n * (n // 2)
+    nyq = n * n
+    return {
+        "K3_zpass": Hp * c * 2 + (Hp + nyq) * rsize + (Hp + nyq) * c,  # S rw, W, Yh
+        "K4_yinv": Hp * c * 2,
+        "K1_xline": Hp * c * 2 + L * rsize * (4 if audit_prev else 3),  # S rw, x, anchor, x_next (+x_prev)
+        "FIN": 0,
+        "K2_yfwd": Hp * c * 2,
+    }
+
+
+def ncu_traffic(n: int):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return {}
+    d = json.loads(p.read_text())
+    return d.get(str(n), {})
+
+
+# ---------------------------------------------------------------------------------
+def cpu_baseline(args, prefer_reference=True):
+    """Reference solver on the host cores (oracle/_ref), bounded sample."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import REF_DIR, Oracle, Reference, make_cfg
+    from paper_1905_13408_b200 import synth
+
+    kind = "reference" if (prefer_reference and (REF_DIR / "libcryomap_ref.so").exists()) else "port"
+    lib = Reference() if kind == "reference" else Oracle()
+    n = args.cpu_n
+    p = synth.synthetic_problem(n)
+    rc, sy, sn = lib.scale_data(p.weight, p.numerator)
+    rc, cfg = lib.derive_config(sy, sn, p.eps, p.eps_prime)
+    cfg.inner_iters = args.cpu_iters
+    t0 = time.perf_counter()
+    rc, x, tr = lib.m_step(p.weight, p.numerator, p.x0, p.x0, cfg, trace=False)
+    secs = time.perf_counter() - t0
+    if kind == "reference":
+        secs = lib.last_seconds  # the m_step call alone (std::chrono inside the C shim)
+    assert rc == 0
+    v = n ** 3 * args.cpu_iters / secs
+    src = "unmodified reference sources + FFTW3-API shim (oracle/fftc.c)" if kind == "reference" \
+        else "oracle C restatement"
+    return {
+        "value": v, "unit": "voxel-iterations/s", "cores": 1, "kind": kind,
+        "sample": f"{src}; m_step {n}^3, {args.cpu_iters} iteration(s), lipschitz step with "
+                  f"audit, per_inner reweighting, 1 thread (m_step is single-threaded as "
+                  f"written); {secs:.2f} s; host nproc={os.cpu_count()}",
+        "seconds": secs,
+    }
+
+
+def run_reference(args):
+    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 3))
+    warm = min(args.warmup, 1)
+    vals = []
+    cb = None
+    for s in range(warm + steps):
+        cb = cpu_baseline(args)
+        if s >= warm:
+            vals.append(cb["seconds"])
+    secs = sum(vals)
+    v = args.cpu_n ** 3 * args.cpu_iters * steps / secs
+    line = {
+        "metric": "solver voxel-iterations/s (512^3 m_step, ISTA, per-inner reweighting, audit)",
+        "value": v, "unit": "voxel-iterations/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": 1e3 * secs / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"m_step {args.n}^3 (bounded CPU sample at {args.cpu_n}^3)",
+                   "side": args.cpu_n, "iters_per_step": args.cpu_iters},
+        "cpu_baseline": {k: cb[k] for k in ("kind", "cores", "sample")} | {"value": v,
+                                                                           "unit": cb["unit"]},
+        "e2e": {"value": v, "unit": "voxel-iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    import paper_1905_13408_b200 as cm
+
+    n, iters = args.n, args.iters
+    t0 = time.time()
+    p = load_problem(n, rank, world)
+    gen_s = time.time() - t0
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    ctx = cm.Context(n, args.precision, device=local)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = iters  # reference semantics: lipschitz + per_inner + audit
+    ctx.set_volumes(p.x0, p.x0)
+
+    for _ in range(args.warmup):
+        ctx.solve(cfg)
+    barrier(world)
+    torch.cuda.synchronize()
+    launches = 0
+    dev_ms = 0.0
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            st = ctx.solve(cfg)
+            launches += st.kernel_launches
+            dev_ms += st.solve_ms
+        e1.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    t_ms = e0.elapsed_time(e1)
+    t_ms = allreduce_max(t_ms, world)
+    clocks = clk.summary()
+    total_vox_iters = float(n) ** 3 * iters * args.steps * world
+    value = total_vox_iters / (t_ms / 1e3)
+
+    # ---- per-kernel profile pass (events around every launch, same stream) --------
+    ctx.set_profiling(True)
+    prof_iters = min(iters, 30)
+    pcfg = cm.RegConfig(**{**cfg.__dict__, "inner_iters": prof_iters})
+    ctx.solve(pcfg)
+    ms5, it = ctx.get_profile()
+    ctx.set_profiling(False)
+    names = ["K3_zpass", "K4_yinv", "K1_xline", "FIN", "K2_yfwd"]
+    avg = {k: ms5[q] / it for q, k in enumerate(names)}
+    rsize = 4 if args.precision == 32 else 8
+    kb = kernel_bytes(n, rsize, audit_prev=True)
+    hbm, peak_kind = peaks()
+    dom = max(names, key=lambda k: avg[k])
+    achieved = kb[dom] / (avg[dom] / 1e3) / 1e9
+    traffic = ncu_traffic(n).get(dom)
+    iter_bytes = sum(kb.values())
+    ms_iter = t_ms / (args.steps * iters)
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+        "algorithmic_bytes_per_launch": kb[dom], "avg_launch_ms": avg[dom],
+        "per_kernel_ms": avg,
+        "per_kernel_frac": {k: (kb[k] / (avg[k] / 1e3) / 1e9 / hbm if kb[k] else None)
+                            for k in names},
+        "iteration": {"bytes": iter_bytes, "ms": ms_iter,
+                      "achieved": iter_bytes / (ms_iter / 1e3) / 1e9,
+                      "frac": iter_bytes / (ms_iter / 1e3) / 1e9 / hbm},
+    }
+
+    # ---- end to end through the C ABI with pinned host buffers -----------------------
+    e2e = None
+    if not args.no_e2e:
+        L = n ** 3
+        pin_w = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
+        pin_y = torch.empty(2 * L, dtype=torch.float64, pin_memory=True).numpy()
+        pin_x = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
+        pin_o = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
+        pin_w[...] = p.weight
+        pin_y[...] = p.numerator.view(np.float64).reshape(-1)
+        pin_x[...] = p.x0
+        pacc = cm.AccumulatorPair(n, pin_y.view(np.complex128).reshape(n, n, n), pin_w, True)
+        ctx.m_step_host(pacc, pin_x, pin_x, cfg, pin_o)  # warm
+        barrier(world)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            ctx.m_step_host(pacc, pin_x, pin_x, cfg, pin_o)
+        f1.record()
+        torch.cuda.synchronize()
+        e_ms = allreduce_max(f0.elapsed_time(f1), world)
+        e2e = {"value": float(n) ** 3 * iters * args.e2e_steps * world / (e_ms / 1e3),
+               "unit": "voxel-iterations/s", "h2d_bytes_per_step": 32 * L,
+               "d2h_bytes_per_step": 8 * L, "steps": args.e2e_steps,
+               "ms_per_step": e_ms / args.e2e_steps}
+
+    # ---- time to tolerance (ISTA reference semantics, then FISTA) -----------------------
+    ttt = None
+    if args.ttt:
+        ttt = {}
+        for name, extra in (("ista", dict(momentum=0, tol_kind=1)),
+                            ("fista", dict(momentum=1, tol_kind=2))):
+            tc = cm.RegConfig(**{**cfg.__dict__, "inner_iters": args.ttt_max_iters,
+                                 "refresh": cm.Refresh.per_m_step, "tol": args.tol, **extra})
+            torch.cuda.synchronize()
+            st = ctx.solve(tc)
+            ttt[name] = {"iterations": st.iterations, "seconds": st.solve_ms / 1e3,
+                         "stop_reason": st.stop_reason, "last_rel": st.last_rel,
+                         "criterion": ("frozen-weight surrogate relative decrease" if name == "ista"
+                                       else "relative step ||x+ - x||/||x+||"),
+                         "tol": args.tol, "refresh": "per_m_step"}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(args)
+            cb.pop("seconds", None)
+        except Exception as e:  # noqa: BLE001
+            cb = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": "solver voxel-iterations/s (512^3 m_step, ISTA, per-inner reweighting, audit)",
+            "value": value, "unit": "voxel-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
+            "config": {"workload": f"m_step {n}^3 synthetic blob phantom (BASELINE config 3), "
+                                   f"{iters} ISTA iterations per step" +
+                                   (f", {world} independent replicas" if world > 1 else ""),
+                       "side": n, "iters_per_step": iters, "step_rule": "lipschitz",
+                       "refresh": "per_inner", "audit": True,
+                       "l2": "working set (>2 GB) larger than the 126 MB L2; no flush needed",
+                       "parallelism": f"replicas{world}"},
+            "device_ms_solver_stream": dev_ms, "gen_seconds": gen_s,
+            "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches, "time_to_tolerance": ttt,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

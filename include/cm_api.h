@@ -1,0 +1,153 @@
+/* cm_api.h — C ABI of the B200-native M-step solver (libcm.so).
+ *
+ * This is the drop-in boundary for the reference's hot path,
+ * cryomap::m_step (/root/reference/proj/include/cryomap/regularizer.hpp:98-100,
+ * src/regularizer.cpp:164-220) and the component entry points of the same
+ * header (regularizer.hpp:45-85), fourier.hpp:11-31 and params.hpp:22,39-41.
+ * Plain pointers and sizes only; no exceptions cross it. Every function
+ * returns a cm_status; cm_last_error() holds a thread-local message.
+ *
+ * Data layout (identical to the reference, volume.hpp:13-27,
+ * backproject.hpp:15-25):
+ *   real volume        double[n*n*n], x fastest: flat (k*n + j)*n + i
+ *   accumulator weight double[n*n*n], full Fourier grid, storage indices
+ *   numerator          double[2*n*n*n], interleaved (re, im), same order
+ * Status codes map 1:1 to the reference exception types (errors.hpp:7-30);
+ * the C++ adapter (paper_1905_13408_b200/adapter/) rethrows them.
+ *
+ * Threading: one context per host thread; a context is not thread-safe.
+ * Calls are stream-ordered and synchronous on return. A context keeps the
+ * accumulator and volumes resident in HBM between calls (em_refine calls
+ * m_step once per half-map per EM iteration, refine.cpp:181,249).
+ */
+#ifndef CM_API_H
+#define CM_API_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CM_API_VERSION 1
+
+typedef enum {
+    CM_OK = 0,
+    CM_ERR_INVALID_ARGUMENT = 1,   /* cryomap::InvalidArgument   (regularizer.cpp:33-42) */
+    CM_ERR_GRID_MISMATCH = 2,      /* cryomap::GridMismatch      (regularizer.cpp:88,169-170) */
+    CM_ERR_NON_HERMITIAN = 3,      /* cryomap::NonHermitianAccumulator (regularizer.cpp:26-29) */
+    CM_ERR_STEP_DIVERGED = 4,      /* cryomap::StepDiverged      (regularizer.cpp:210-213) */
+    CM_ERR_CUDA = 5,               /* device / runtime failure */
+    CM_ERR_NCCL = 6,               /* collective failure (multi-GPU) */
+    CM_ERR_NON_POSITIVE_SCALE = 7, /* cryomap::NonPositiveScale  (params.cpp:48-50) */
+    CM_ERR_NON_HERMITIAN_INPUT = 8,/* cryomap::NonHermitianInput (fourier.cpp:80-82) */
+    CM_ERR_UNSUPPORTED = 9,        /* side length without a compiled radix plan */
+    CM_ERR_STATE = 10              /* call order (e.g. solve before set_accumulator) */
+} cm_status;
+
+typedef struct cm_ctx cm_ctx;
+
+/* RegConfig (regularizer.hpp:21-35) field for field, then opt-in extensions.
+ * All-zero extensions reproduce the reference exactly (ISTA, exactly
+ * inner_iters iterations, 1e-9 relative audit slack). */
+typedef struct {
+    double alpha, beta, gamma;   /* L1 / TV / restraint weights */
+    double eps, eps_prime, mu;   /* reweighting offsets, TV smoothing */
+    int inner_iters;
+    int step_rule;               /* 0 lipschitz, 1 fixed */
+    double fixed_step;
+    int refresh;                 /* 0 per_inner, 1 per_m_step */
+    int convex_mode;
+    /* ---- extensions ---- */
+    int momentum;                /* 0 ISTA (reference), 1 FISTA (no monotone audit) */
+    int tol_kind;                /* 0 none, 1 frozen-weight surrogate relative decrease,
+                                    2 relative step ||x+ - x|| / ||x+|| */
+    double tol;                  /* stop when the measure drops below tol */
+    double audit_slack;          /* <= 0: 1e-9 in fp64 (reference), 1e-6 in fp32 */
+} cm_reg_config;
+
+/* ObjectiveValue (regularizer.hpp:67-79) order:
+ * fit, l1, tv_smooth, tv_linear, restraint, lognorm_l1, lognorm_tv */
+typedef struct {
+    double before[7];
+    double after[7];
+    double step;
+} cm_trace_row; /* MStepTraceRow (regularizer.hpp:88-92) */
+
+typedef struct {
+    int iterations;     /* iterations behind the returned volume */
+    int trace_rows;     /* rows written to trace */
+    int stop_reason;    /* 1 inner_iters reached, 2 tolerance, 3 diverged */
+    int diverged_iter;  /* -1 unless stop_reason == 3 */
+    double last_rel;    /* last tolerance measure */
+    double step;        /* l_r used */
+    double solve_ms;    /* device time of the iteration loop (CUDA events) */
+    int kernel_launches;/* kernels launched by the solve */
+} cm_solve_stats;
+
+int cm_version(void);
+const char* cm_last_error(void);
+
+/* Side lengths with a compiled plan: 4 6 8 12 16 24 32 48 64 96 128 192 256 384
+ * 512 768 1024 (radix 2/3). precision: 32 (fp32 product mode) or 64 (fp64
+ * parity mode). devices/ndev: ndev must be 1 (one process per GPU). */
+int cm_supported_side(int n);
+int cm_ctx_create(int n, const int* devices, int ndev, int precision, cm_ctx** out);
+int cm_ctx_destroy(cm_ctx* ctx);
+int cm_ctx_info(const cm_ctx* ctx, int* n, int* precision, long long* device_bytes);
+
+/* AccumulatorPair upload (backproject.hpp:15-25): symmetry residue
+ * (backproject.cpp:103-118), Hermitian projection to the packed half
+ * spectrum, (-1)^(a+b+c) phase sign, max weight, data scales. */
+int cm_set_accumulator(cm_ctx* ctx, const double* weight, const double* numerator,
+                       int finalized);
+int cm_accumulator_info(const cm_ctx* ctx, double* residue, double* max_weight);
+/* scale_data (params.cpp:9-26): s_y = RMS(Re ifft3(num/sqrt(weight))), s_n = mean weight */
+int cm_scale_data(cm_ctx* ctx, double* s_y, double* s_n);
+/* derive_config (params.cpp:40-64); out gets RegConfig defaults elsewhere */
+int cm_derive_config(double s_y, double s_n, double eps, double eps_prime, double a, double b,
+                     double g, cm_reg_config* out);
+
+/* x_init / x_anchor upload; passing the same pointer marks them as one object
+ * (em_refine passes x for both, refine.cpp:181). */
+int cm_set_volumes(cm_ctx* ctx, const double* x_init, const double* x_anchor);
+/* Run the solver on the resident accumulator and volumes. trace may be null;
+ * otherwise it receives up to trace_cap rows. */
+int cm_solve(cm_ctx* ctx, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
+             cm_solve_stats* stats);
+int cm_get_volume(cm_ctx* ctx, double* x_out);
+
+/* Diagnostics: when on, cm_solve launches every kernel individually between
+ * CUDA events on the context stream (no graph) and accumulates per-kernel
+ * device time: ms5 = {K3 z-pass, K4 y-inverse, K1 x-line sweep, FIN, K2 y-forward}. */
+int cm_set_profiling(cm_ctx* ctx, int on);
+int cm_get_profile(const cm_ctx* ctx, double* ms5, int* iters);
+
+/* m_step (regularizer.hpp:98-100) in one call: upload, solve, download. */
+int cm_m_step(cm_ctx* ctx, const double* weight, const double* numerator, int finalized,
+              const double* x_init, const double* x_anchor, const cm_reg_config* cfg,
+              double* x_out, cm_trace_row* trace, int trace_cap, cm_solve_stats* stats);
+
+/* ---- component entry points (regularizer.hpp:45-85, fourier.hpp) ---- */
+/* data_gradient (regularizer.hpp:62) against the resident accumulator */
+int cm_data_gradient(cm_ctx* ctx, const double* x, double* out);
+/* compute_weights (regularizer.hpp:45-46) */
+int cm_compute_weights(cm_ctx* ctx, const double* x, double eps, double eps_prime, int convex,
+                       double* w_l1, double* w_tv);
+/* smoothed_tv_value / smoothed_tv_gradient (regularizer.hpp:51-57); w_tv may be null */
+int cm_smoothed_tv_value(cm_ctx* ctx, const double* x, double mu, const double* w_tv,
+                         double* out);
+int cm_smoothed_tv_gradient(cm_ctx* ctx, const double* x, double mu, const double* w_tv,
+                            double* out);
+/* prox_l1 (regularizer.hpp:65) */
+int cm_prox_l1(cm_ctx* ctx, const double* x, const double* thresholds, double* out);
+/* penalized_objective (regularizer.hpp:83-85) against the resident accumulator;
+ * out7 in ObjectiveValue order */
+int cm_penalized_objective(cm_ctx* ctx, const double* x, const cm_reg_config* cfg,
+                           const double* x_anchor, const double* x_weights_source,
+                           double* out7);
+/* fft3 (fourier.hpp:11): unnormalised forward transform, full complex grid */
+int cm_fft3(cm_ctx* ctx, const double* x, double* out_interleaved);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

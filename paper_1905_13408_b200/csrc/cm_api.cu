@@ -1,0 +1,242 @@
+// C ABI (include/cm_api.h) of the B200 M-step solver.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/cm_api.h"
+#include "impl.cuh"
+
+namespace cm {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CM_SIDES(X) X(4) X(6) X(8) X(12) X(16) X(24) X(32) X(48) X(64) X(96) X(128) X(192) \
+    X(256) X(384) X(512) X(768) X(1024)
+#define CM_DECL(NN) ImplBase* make_impl_##NN(int precision);
+CM_SIDES(CM_DECL)
+
+static ImplBase* make_impl(int n, int precision) {
+    switch (n) {
+#define CM_CASE(NN) \
+    case NN: return make_impl_##NN(precision);
+        CM_SIDES(CM_CASE)
+#undef CM_CASE
+        default: return nullptr;
+    }
+}
+
+} // namespace cm
+
+using namespace cm;
+
+struct cm_ctx {
+    std::unique_ptr<ImplBase> impl;
+    int n = 0;
+    int precision = 32;
+    int device = 0;
+};
+
+#define CTX_GUARD(ctx)                                                         \
+    do {                                                                       \
+        if (!(ctx) || !(ctx)->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context"); \
+        if (cudaSetDevice((ctx)->device) != cudaSuccess)                       \
+            return fail(CM_ERR_CUDA, "cudaSetDevice failed");                  \
+    } while (0)
+
+extern "C" {
+
+int cm_version(void) { return CM_API_VERSION; }
+const char* cm_last_error(void) { return g_err.c_str(); }
+
+int cm_supported_side(int n) {
+    switch (n) {
+#define CM_ONE(NN) case NN:
+        CM_SIDES(CM_ONE)
+#undef CM_ONE
+        return 1;
+        default:
+            return 0;
+    }
+}
+
+int cm_ctx_create(int n, const int* devices, int ndev, int precision, cm_ctx** out) {
+    if (!out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    if (n < 4 || n % 2 != 0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "side_n must be even and >= 4, got " + std::to_string(n));
+    if (!cm_supported_side(n))
+        return fail(CM_ERR_UNSUPPORTED, "no compiled radix plan for side " + std::to_string(n));
+    if (precision != 32 && precision != 64)
+        return fail(CM_ERR_INVALID_ARGUMENT, "precision must be 32 or 64");
+    if (ndev > 1) return fail(CM_ERR_INVALID_ARGUMENT, "one device per context (one process per GPU)");
+    const int dev = (devices && ndev == 1) ? devices[0] : 0;
+    CK(cudaSetDevice(dev));
+    auto ctx = std::make_unique<cm_ctx>();
+    ctx->n = n;
+    ctx->precision = precision;
+    ctx->device = dev;
+    ctx->impl.reset(make_impl(n, precision));
+    if (!ctx->impl) return fail(CM_ERR_UNSUPPORTED, "unsupported side");
+    const int rc = ctx->impl->init();
+    if (rc != CM_OK) return rc;
+    *out = ctx.release();
+    return CM_OK;
+}
+
+int cm_ctx_destroy(cm_ctx* ctx) {
+    if (!ctx) return CM_OK;
+    cudaSetDevice(ctx->device);
+    delete ctx;
+    return CM_OK;
+}
+
+int cm_ctx_info(const cm_ctx* ctx, int* n, int* precision, long long* device_bytes) {
+    if (!ctx || !ctx->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
+    if (n) *n = ctx->n;
+    if (precision) *precision = ctx->precision;
+    if (device_bytes) *device_bytes = ctx->impl->bytes();
+    return CM_OK;
+}
+
+int cm_set_accumulator(cm_ctx* ctx, const double* weight, const double* numerator, int finalized) {
+    CTX_GUARD(ctx);
+    if (!weight || !numerator) return fail(CM_ERR_INVALID_ARGUMENT, "null accumulator");
+    return ctx->impl->set_accumulator(weight, numerator, finalized);
+}
+
+int cm_accumulator_info(const cm_ctx* ctx, double* residue, double* max_weight) {
+    if (!ctx || !ctx->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
+    if (!ctx->impl->acc_set) return fail(CM_ERR_STATE, "accumulator not set");
+    if (residue) *residue = ctx->impl->residue;
+    if (max_weight) *max_weight = ctx->impl->max_weight;
+    return CM_OK;
+}
+
+int cm_scale_data(cm_ctx* ctx, double* s_y, double* s_n) {
+    CTX_GUARD(ctx);
+    ImplBase* im = ctx->impl.get();
+    if (!im->acc_set) return fail(CM_ERR_STATE, "accumulator not set");
+    // params.cpp:10-11 checks the flag only; the Hermitian guard of ifft3
+    // (fourier.cpp:80) is the symmetry residue here
+    if (!im->acc_finalized)
+        return fail(CM_ERR_NON_HERMITIAN, "scale_data: accumulator is not finalized");
+    if (im->residue > 1e-8)
+        return fail(CM_ERR_NON_HERMITIAN_INPUT, "ifft3: whitened accumulator is not Hermitian");
+    if (s_y) *s_y = im->s_y;
+    if (s_n) *s_n = im->s_n;
+    return CM_OK;
+}
+
+int cm_derive_config(double s_y, double s_n, double eps, double eps_prime, double a, double b,
+                     double g, cm_reg_config* out) {
+    if (!out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    if (s_y < 0.0 || s_n < 0.0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "derive_config: data scales must be >= 0");
+    if (!(eps > 0.0) || !(eps_prime > 0.0))
+        return fail(CM_ERR_INVALID_ARGUMENT, "derive_config: eps and eps_prime must be > 0");
+    if (a < 0.0 || b < 0.0 || g < 0.0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "derive_config: multipliers must be >= 0");
+    if (s_y == 0.0 && (a > 0.0 || b > 0.0))
+        return fail(CM_ERR_NON_POSITIVE_SCALE,
+                    "derive_config: s_y is zero but the L1/TV multipliers are nonzero");
+    std::memset(out, 0, sizeof(*out));
+    out->alpha = a * s_y * eps;
+    out->beta = b * s_y * eps_prime;
+    out->gamma = g * s_n;
+    out->eps = eps;
+    out->eps_prime = eps_prime;
+    out->mu = 0.01 * eps_prime;
+    out->inner_iters = 24;
+    return validate(out);
+}
+
+int cm_set_volumes(cm_ctx* ctx, const double* x_init, const double* x_anchor) {
+    CTX_GUARD(ctx);
+    if (!x_init || !x_anchor) return fail(CM_ERR_INVALID_ARGUMENT, "null volume");
+    return ctx->impl->set_volumes(x_init, x_anchor);
+}
+
+int cm_solve(cm_ctx* ctx, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
+             cm_solve_stats* stats) {
+    CTX_GUARD(ctx);
+    return ctx->impl->solve(cfg, trace, trace_cap, stats);
+}
+
+int cm_set_profiling(cm_ctx* ctx, int on) {
+    CTX_GUARD(ctx);
+    ctx->impl->profiling = on;
+    return CM_OK;
+}
+
+int cm_get_profile(const cm_ctx* ctx, double* ms5, int* iters) {
+    if (!ctx || !ctx->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
+    for (int q = 0; q < 5; ++q) ms5[q] = ctx->impl->prof_ms[q];
+    if (iters) *iters = ctx->impl->prof_iters;
+    return CM_OK;
+}
+
+int cm_get_volume(cm_ctx* ctx, double* x_out) {
+    CTX_GUARD(ctx);
+    if (!x_out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    return ctx->impl->get_volume(x_out);
+}
+
+int cm_m_step(cm_ctx* ctx, const double* weight, const double* numerator, int finalized,
+              const double* x_init, const double* x_anchor, const cm_reg_config* cfg,
+              double* x_out, cm_trace_row* trace, int trace_cap, cm_solve_stats* stats) {
+    CTX_GUARD(ctx);
+    // reference order: validate config, then the accumulator guard (regularizer.cpp:167-168)
+    CKS(validate(cfg));
+    CKS(cm_set_accumulator(ctx, weight, numerator, finalized));
+    CKS(cm_set_volumes(ctx, x_init, x_anchor));
+    const int rc = cm_solve(ctx, cfg, trace, trace_cap, stats);
+    if (rc != CM_OK) return rc;
+    return cm_get_volume(ctx, x_out);
+}
+
+int cm_data_gradient(cm_ctx* ctx, const double* x, double* out) {
+    CTX_GUARD(ctx);
+    return ctx->impl->data_gradient(x, out);
+}
+
+int cm_compute_weights(cm_ctx* ctx, const double* x, double eps, double eps_prime, int convex,
+                       double* w_l1, double* w_tv) {
+    CTX_GUARD(ctx);
+    return ctx->impl->weights(x, eps, eps_prime, convex, w_l1, w_tv);
+}
+
+int cm_smoothed_tv_value(cm_ctx* ctx, const double* x, double mu, const double* w_tv, double* out) {
+    CTX_GUARD(ctx);
+    return ctx->impl->tv(x, mu, w_tv, out, nullptr);
+}
+
+int cm_smoothed_tv_gradient(cm_ctx* ctx, const double* x, double mu, const double* w_tv,
+                            double* out) {
+    CTX_GUARD(ctx);
+    return ctx->impl->tv(x, mu, w_tv, nullptr, out);
+}
+
+int cm_prox_l1(cm_ctx* ctx, const double* x, const double* thresholds, double* out) {
+    CTX_GUARD(ctx);
+    return ctx->impl->prox(x, thresholds, out);
+}
+
+int cm_penalized_objective(cm_ctx* ctx, const double* x, const cm_reg_config* cfg,
+                           const double* x_anchor, const double* x_weights_source, double* out7) {
+    CTX_GUARD(ctx);
+    return ctx->impl->objective(x, cfg, x_anchor, x_weights_source, out7);
+}
+
+int cm_fft3(cm_ctx* ctx, const double* x, double* out_interleaved) {
+    CTX_GUARD(ctx);
+    return ctx->impl->fft3(x, out_interleaved);
+}
+
+} // extern "C"

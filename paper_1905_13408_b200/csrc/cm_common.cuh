@@ -1,0 +1,95 @@
+// Shared device helpers for the B200 M-step solver (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cm {
+
+// ---- real / complex traits (fp32 product mode, fp64 parity mode) ----------
+template <typename R> struct CxT;
+template <> struct CxT<float> { using type = float2; };
+template <> struct CxT<double> { using type = double2; };
+template <typename R> using Cx = typename CxT<R>::type;
+
+template <typename C> __device__ __forceinline__ C cx(decltype(C::x) re, decltype(C::x) im) {
+    C c;
+    c.x = re;
+    c.y = im;
+    return c;
+}
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return cx<C>(a.x + b.x, a.y + b.y); }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return cx<C>(a.x - b.x, a.y - b.y); }
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+    return cx<C>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
+    return cx<C>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename C> __device__ __forceinline__ C cconj(C a) { return cx<C>(a.x, -a.y); }
+template <typename C, typename R> __device__ __forceinline__ C cscale(C a, R s) {
+    return cx<C>(a.x * s, a.y * s);
+}
+// multiply by -i (fwd=true) or +i
+template <bool FWD, typename C> __device__ __forceinline__ C cmul_mi(C a) {
+    return FWD ? cx<C>(a.y, -a.x) : cx<C>(-a.y, a.x);
+}
+
+// ---- solver device state (one per context, in device memory) --------------
+// Written by the per-iteration finalize kernel; read by every kernel of the
+// iteration so that a captured CUDA graph can stop early on the device.
+struct DevState {
+    int iter;          // iterations completed (index of the next iteration)
+    int max_iters;     // inner_iters
+    int done;          // 1: stop — every kernel of later iterations returns at entry
+    int stop_reason;   // 0 running, 1 max_iters, 2 tolerance, 3 diverged
+    int diverged_iter; // first iteration whose audit failed, -1 if none
+    int rows;          // trace rows written
+    int audit;         // objective audit / trace active
+    int check_diverge; // lipschitz step rule: monotone surrogate check
+    int tol_kind;      // 0 none, 1 surrogate relative decrease, 2 relative step
+    int fista;         // momentum on
+    int refresh_inner; // per_inner weights (needs the previous iterate for after_{i-1})
+    int pad0;
+    double tol;
+    double audit_slack; // relative slack of the monotone check (1e-9 in the reference)
+    double step;        // l_r (constant within one m_step)
+    double before[7];   // before_i of the iteration being audited (saved by finalize)
+    double last_rel;    // last tolerance measure
+};
+
+__device__ __forceinline__ int ld_done(const DevState* st) {
+    return *((volatile const int*)&st->done);
+}
+
+// ---- reductions -------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum of NV doubles per thread; result valid in thread 0. scratch
+// must hold 32*NV doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) scratch[wid * NV + q] = v[q];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double s = lane < nw ? scratch[lane * NV + q] : 0.0;
+            v[q] = warp_sum(s);
+        }
+    }
+}
+
+} // namespace cm

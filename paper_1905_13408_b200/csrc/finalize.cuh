@@ -1,0 +1,107 @@
+// Per-iteration finalize: fixed-order reduction of the block partials of the
+// z pass (fit) and the x-line sweep (penalties), trace row, monotone audit and
+// tolerance test. One 256-thread block; deterministic.
+#pragma once
+
+#include "cm_common.cuh"
+#include "kernels.cuh"
+
+namespace cm {
+
+struct FinParams {
+    DevState* st;
+    const double* part1; int nb1;   // xline partials [nb1][NP1]
+    const double* part3; int nb3;   // zpass partials [nb3][NP3]
+    double* trace;                  // [max_iters][15] or null
+    double alpha, beta, gamma, invL;
+    int epilogue;                   // 1: close the last row after the loop
+};
+
+static __device__ __forceinline__ double surrogate7(const double* o) { return o[0] + o[1] + o[2] + o[4]; }
+
+static __global__ void __launch_bounds__(256) finalize_kernel(FinParams p) {
+    __shared__ double red[32 * (NP1 + NP3)];
+    DevState* st = p.st;
+    if (!p.epilogue && ld_done(st)) return;
+    if (p.epilogue && !(st->stop_reason == 1 && st->audit)) return;
+
+    double s[NP1 + NP3];
+#pragma unroll
+    for (int q = 0; q < NP1 + NP3; ++q) s[q] = 0.0;
+    // fixed assignment of blocks to threads + fixed tree => deterministic
+    if (p.part1)
+        for (int b = threadIdx.x; b < p.nb1; b += blockDim.x)
+#pragma unroll
+            for (int q = 0; q < NP1; ++q) s[q] += p.part1[(size_t)b * NP1 + q];
+    if (p.part3)
+        for (int b = threadIdx.x; b < p.nb3; b += blockDim.x)
+#pragma unroll
+            for (int q = 0; q < NP3; ++q) s[NP1 + q] += p.part3[(size_t)b * NP3 + q];
+    block_sum<NP1 + NP3>(s, red);
+    if (threadIdx.x != 0) return;
+
+    const double fit = (s[NP1 + 0] - 2.0 * s[NP1 + 1]) * p.invL;
+    const int i = p.epilogue ? st->max_iters : st->iter;
+    double cur[7] = {fit,
+                     p.alpha * s[0],
+                     p.beta * s[1],
+                     p.beta * s[2],
+                     p.gamma * s[5],
+                     p.alpha * s[3],
+                     p.beta * s[4]};
+    if (st->audit && i > 0) {
+        double after[7];
+        for (int q = 0; q < 7; ++q) after[q] = cur[q];
+        if (st->refresh_inner) { // weights of x_{i-1} at x_i
+            after[1] = p.alpha * s[6];
+            after[2] = p.beta * s[7];
+            after[3] = p.beta * s[8];
+        }
+        const double sb = surrogate7(st->before);
+        const double sa = surrogate7(after);
+        const double slack = st->audit_slack * fmax(1.0, fabs(sb));
+        if (st->check_diverge && sa > sb + slack) {
+            st->diverged_iter = i - 1;
+            st->stop_reason = 3;
+            st->done = 1;
+            st->rows = i - 1;
+            return;
+        }
+        if (p.trace) {
+            double* row = p.trace + (size_t)(i - 1) * 15;
+            for (int q = 0; q < 7; ++q) row[q] = st->before[q];
+            for (int q = 0; q < 7; ++q) row[7 + q] = after[q];
+            row[14] = st->step;
+        }
+        st->rows = i;
+        if (st->tol_kind == 1) {
+            const double rel = fabs(sb - sa) / fmax(fabs(sb), 1e-300);
+            st->last_rel = rel;
+            if (!p.epilogue && rel < st->tol) {
+                // stop with x_i as the result
+                st->stop_reason = 2;
+                st->done = 1;
+                st->iter = i;
+                return;
+            }
+        }
+    }
+    if (p.epilogue) return;
+    for (int q = 0; q < 7; ++q) st->before[q] = cur[q];
+    st->iter = i + 1;
+    if (st->tol_kind == 2) {
+        const double rel = sqrt(s[9] / fmax(s[10], 1e-300));
+        st->last_rel = rel;
+        if (rel < st->tol) {
+            st->stop_reason = 2;
+            st->done = 1;
+            return;
+        }
+    }
+    if (st->iter >= st->max_iters) {
+        st->stop_reason = 1;
+        st->done = 1;
+    }
+}
+
+} // namespace cm

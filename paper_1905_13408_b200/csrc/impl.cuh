@@ -1,0 +1,868 @@
+// Host runtime of the B200 M-step solver: one Impl<R, N> per (precision, side).
+//
+// One context = one GPU, one stream, the accumulator and volumes resident in
+// HBM. The iteration loop is captured once per solve as a CUDA graph of six
+// iterations (K3 K4 K1 FIN K2 x 6; six = lcm of the 3-buffer ISTA and the
+// 2-buffer FISTA rotations) and relaunched; kernels read a device-side stop
+// flag so a graph that overshoots the stopping iteration costs only empty
+// launches. The host polls that flag with a bounded look-ahead.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/cm_api.h"
+#include "finalize.cuh"
+#include "kernels.cuh"
+
+namespace cm {
+
+// thread-local last error (defined in cm_api.cu)
+int fail(int code, const std::string& msg);
+
+#define CK(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(CM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKS(call)                                                                        \
+    do {                                                                                 \
+        int s_ = (call);                                                                 \
+        if (s_ != CM_OK) return s_;                                                      \
+    } while (0)
+
+// ---------------------------------------------------------------------------------
+// upload / conversion kernels (run once per call, not per iteration)
+// ---------------------------------------------------------------------------------
+static __device__ __forceinline__ void atomic_max_pos(unsigned long long* a, double v) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(a, (unsigned long long)__double_as_longlong(v));
+}
+
+// Full-grid fp64 accumulator -> packed half spectrum (Hermitian projection,
+// (-1)^(a+b+c) sign), symmetry residue (backproject.cpp:103-118), max weight,
+// sum weight and the Parseval form of scale_data's whitened RMS.
+template <typename R>
+__global__ void convert_acc_kernel(int n, const double* __restrict__ W,
+                                   const double* __restrict__ Y, R* Wm, R* Wn, Cx<R>* Ym,
+                                   Cx<R>* Yn, double* part, unsigned long long* maxes) {
+    using C = Cx<R>;
+    const int nh = n / 2;
+    const size_t total = (size_t)n * n * (nh + 1);
+    double sw = 0.0, sz = 0.0, worst = 0.0, scale = 0.0, wmax = 0.0;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(q % (nh + 1));
+        const size_t bc = q / (nh + 1);
+        const int b = (int)(bc % n), c = (int)(bc / n);
+        const int am = a ? n - a : 0, bm = b ? n - b : 0, cm_ = c ? n - c : 0;
+        const size_t i = ((size_t)c * n + b) * n + a;
+        const size_t m = ((size_t)cm_ * n + bm) * n + am;
+        const double w = W[i], wmt = W[m];
+        const double yr = Y[2 * i], yi = Y[2 * i + 1];
+        const double mr = Y[2 * m], mi = Y[2 * m + 1];
+        // residue: |Y(n) - conj Y(-n)|, |W(n) - W(-n)|; scale: max |Y|, W
+        worst = fmax(worst, hypot(yr - mr, yi + mi));
+        worst = fmax(worst, fabs(w - wmt));
+        scale = fmax(scale, fmax(hypot(yr, yi), w));
+        scale = fmax(scale, fmax(hypot(mr, mi), wmt));
+        wmax = fmax(wmax, fmax(w, wmt));
+        const bool inner = (a != 0 && a != nh);
+        sw += inner ? (w + wmt) : w;
+        // whitened Hermitian part Z_H = (Y/sqrtW + conj(Ym/sqrtWm)) / 2
+        double zr = 0.0, zi = 0.0;
+        if (w > 0.0) {
+            const double s = 1.0 / sqrt(w);
+            zr += yr * s;
+            zi += yi * s;
+        }
+        if (wmt > 0.0) {
+            const double s = 1.0 / sqrt(wmt);
+            zr += mr * s;
+            zi -= mi * s;
+        }
+        zr *= 0.5;
+        zi *= 0.5;
+        sz += (inner ? 2.0 : 1.0) * (zr * zr + zi * zi);
+        // projected, sign-folded solver inputs
+        const double wp = 0.5 * (w + wmt);
+        const double sg = ((a + b + c) & 1) ? -1.0 : 1.0;
+        const double pr = sg * 0.5 * (yr + mr), pi = sg * 0.5 * (yi - mi);
+        if (a < nh) {
+            const size_t o = ((size_t)c * n + b) * nh + a;
+            Wm[o] = R(wp);
+            Ym[o] = cx<C>(R(pr), R(pi));
+        } else {
+            const size_t o = (size_t)c * n + b;
+            Wn[o] = R(wp);
+            Yn[o] = cx<C>(R(pr), R(pi));
+        }
+    }
+    __shared__ double red[32 * 2];
+    double v[2] = {sw, sz};
+    block_sum<2>(v, red);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x * 2 + 0] = v[0];
+        part[blockIdx.x * 2 + 1] = v[1];
+    }
+    // maxima: warp-reduce then one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) {
+        worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+        scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+        wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_pos(maxes + 0, worst);
+        atomic_max_pos(maxes + 1, scale);
+        atomic_max_pos(maxes + 2, wmax);
+    }
+}
+
+template <typename R>
+__global__ void to_real_kernel(const double* __restrict__ in, R* __restrict__ out, size_t L) {
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < L;
+         q += (size_t)gridDim.x * blockDim.x)
+        out[q] = R(in[q]);
+}
+
+template <typename R>
+__global__ void to_double_kernel(const R* __restrict__ in, double* __restrict__ out, size_t L) {
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < L;
+         q += (size_t)gridDim.x * blockDim.x)
+        out[q] = double(in[q]);
+}
+
+// prox_l1 (regularizer.cpp:103-110), elementwise in fp64
+static __global__ void prox_kernel(const double* __restrict__ x, const double* __restrict__ t,
+                            double* __restrict__ out, size_t L) {
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < L;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const double v = x[q], th = t[q];
+        out[q] = fabs(v) <= th ? 0.0 : v - copysign(th, v);
+    }
+}
+
+inline int grid_for(size_t work, int block) {
+    size_t g = (work + block - 1) / block;
+    return (int)std::min<size_t>(g, 148 * 32);
+}
+
+// ---------------------------------------------------------------------------------
+// validation mirrors validate_reg_config (regularizer.cpp:33-42)
+// ---------------------------------------------------------------------------------
+inline int validate(const cm_reg_config* c) {
+    if (!c) return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: null config");
+    if (c->alpha < 0.0 || c->beta < 0.0 || c->gamma < 0.0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: alpha/beta/gamma must be >= 0");
+    if (c->eps <= 0.0 || c->eps_prime <= 0.0 || c->mu <= 0.0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: eps/eps_prime/mu must be > 0");
+    if (c->inner_iters < 1)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: inner_iters must be >= 1");
+    if (c->step_rule == 1 && c->fixed_step <= 0.0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: fixed step must be > 0");
+    if (c->step_rule != 0 && c->step_rule != 1)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown step rule");
+    if (c->refresh != 0 && c->refresh != 1)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown refresh mode");
+    if (c->momentum != 0 && c->momentum != 1)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown momentum mode");
+    if (c->tol_kind < 0 || c->tol_kind > 2)
+        return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown tolerance kind");
+    return CM_OK;
+}
+
+// ---------------------------------------------------------------------------------
+struct ImplBase {
+    virtual ~ImplBase() = default;
+    virtual int init() = 0;
+    virtual int set_accumulator(const double* w, const double* y, int finalized) = 0;
+    virtual int set_volumes(const double* xi, const double* xa) = 0;
+    virtual int solve(const cm_reg_config* c, cm_trace_row* tr, int cap, cm_solve_stats* st) = 0;
+    virtual int get_volume(double* out) = 0;
+    virtual int data_gradient(const double* x, double* out) = 0;
+    virtual int weights(const double* x, double eps, double epsp, int convex, double* wl1,
+                        double* wtv) = 0;
+    virtual int tv(const double* x, double mu, const double* wtv, double* value,
+                   double* grad) = 0;
+    virtual int prox(const double* x, const double* t, double* out) = 0;
+    virtual int objective(const double* x, const cm_reg_config* c, const double* anchor,
+                          const double* wsrc, double* out7) = 0;
+    virtual int fft3(const double* x, double* out) = 0;
+    virtual long long bytes() const = 0;
+
+    cudaStream_t stream = nullptr;
+    int n = 0;
+    bool acc_set = false, acc_finalized = false, vol_set = false, anchor_is_init = false;
+    double residue = 0.0, max_weight = 0.0, s_y = 0.0, s_n = 0.0;
+    int profiling = 0;      // per-kernel CUDA-event timing (no graph)
+    double prof_ms[5] = {}; // K3 K4 K1 FIN K2 accumulated device ms
+    int prof_iters = 0;
+    int last_iter = 0;      // iterations behind the resident result
+    int last_fista = 0;
+    bool result_valid = false;
+};
+
+template <typename R, int N>
+struct Impl final : ImplBase {
+    using C = Cx<R>;
+    using G = Geo<R, N>;
+    static constexpr size_t L = (size_t)N * N * N;
+    static constexpr int Nh = N / 2;
+    static constexpr size_t H = (size_t)N * N * Nh;
+    static constexpr size_t NN = (size_t)N * N;
+    static constexpr int NB1 = (int)((NN + G::LPC - 1) / G::LPC);
+    static constexpr int NB3 = (Nh / G::TW3) * (N / 2 + 1);
+    static constexpr int LOOK = 8;
+
+    R* X[3] = {};
+    R* XF[2] = {};
+    R* YF[2] = {};
+    R* x0keep = nullptr;
+    R* anchor = nullptr;
+    R* winit = nullptr;
+    C* S = nullptr;
+    R* W = nullptr;
+    R* Wn = nullptr;
+    C* Yh = nullptr;
+    C* Yn = nullptr;
+    C* twN = nullptr;
+    double* stage = nullptr;   // fp64 staging (3L doubles)
+    double* part1 = nullptr;
+    double* part3 = nullptr;
+    double* part_acc = nullptr;
+    unsigned long long* maxes = nullptr;
+    DevState* st = nullptr;
+    double* trace_d = nullptr;
+    int trace_rows_cap = 0;
+    double* theta_d = nullptr;
+    int theta_cap = 0;
+    int* flags_h = nullptr;
+    long long alloc_bytes = 0;
+
+    template <typename T>
+    int dalloc(T** p, size_t count) {
+        const size_t b = sizeof(T) * std::max<size_t>(count, 1);
+        CK(cudaMalloc((void**)p, b));
+        alloc_bytes += (long long)b;
+        return CM_OK;
+    }
+
+    ~Impl() override {
+        void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, S, W,
+                      Wn, Yh, Yn, twN, stage, part1, part3, part_acc, maxes, st, trace_d,
+                      theta_d};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        if (flags_h) cudaFreeHost(flags_h);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    long long bytes() const override { return alloc_bytes; }
+
+    int init() override {
+        n = N;
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        for (auto& p : X) CKS(dalloc(&p, L));
+        CKS(dalloc(&x0keep, L));
+        CKS(dalloc(&anchor, L));
+        CKS(dalloc(&S, H));
+        CKS(dalloc(&W, H));
+        CKS(dalloc(&Wn, NN));
+        CKS(dalloc(&Yh, H));
+        CKS(dalloc(&Yn, NN));
+        CKS(dalloc(&twN, N));
+        CKS(dalloc(&stage, 3 * L));
+        CKS(dalloc(&part1, (size_t)NB1 * NP1));
+        CKS(dalloc(&part3, (size_t)NB3 * NP3));
+        CKS(dalloc(&part_acc, 2 * 148 * 32));
+        CKS(dalloc(&maxes, 4));
+        CKS(dalloc(&st, 1));
+        CK(cudaHostAlloc((void**)&flags_h, sizeof(int) * LOOK, cudaHostAllocDefault));
+        for (auto& p : X) CK(cudaMemsetAsync(p, 0, sizeof(R) * L, stream));
+        // twiddles exp(-2 pi i q / N) computed in fp64 on the host, rounded once
+        std::vector<C> tw(N);
+        for (int q = 0; q < N; ++q) {
+            const double a = -2.0 * M_PI * (double)q / (double)N;
+            tw[q].x = R(std::cos(a));
+            tw[q].y = R(std::sin(a));
+        }
+        CK(cudaMemcpyAsync(twN, tw.data(), sizeof(C) * N, cudaMemcpyHostToDevice, stream));
+        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_INIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_SWEEP>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_OBJ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_DGRAD>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_TVGRAD>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_WEIGHTS>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(ypass_kernel<R, N, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(ypass_kernel<R, N, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(zpass_kernel<R, N, ZM_FULL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(zpass_kernel<R, N, ZM_FIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(zpass_kernel<R, N, ZM_FWD>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSmem<R, N>::bytes));
+        CK(cudaStreamSynchronize(stream));
+        return CM_OK;
+    }
+
+    // ---- launch helpers ----------------------------------------------------------
+    XParams<R> xp() const {
+        XParams<R> p{};
+        p.S = S;
+        p.twN = twN;
+        p.invL = 1.0 / (double)L;
+        return p;
+    }
+    template <int MODE>
+    int launch_x(const XParams<R>& p) {
+        xline_kernel<R, N, MODE><<<NB1, G::LPC * G::TX, XSmem<R, N>::bytes, stream>>>(p);
+        CK(cudaGetLastError());
+        return CM_OK;
+    }
+    int launch_y(bool fwd, DevState* s) {
+        YParams<R> p{S, twN, s};
+        dim3 grid(Nh / G::TWY, N);
+        if (fwd)
+            ypass_kernel<R, N, true><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
+        else
+            ypass_kernel<R, N, false><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
+        CK(cudaGetLastError());
+        return CM_OK;
+    }
+    template <int MODE>
+    int launch_z(double* part, DevState* s) {
+        ZParams<R> p{S, W, Wn, Yh, Yn, twN, part, s};
+        dim3 grid(Nh / G::TW3, N / 2 + 1);
+        zpass_kernel<R, N, MODE><<<grid, 2 * G::TW3 * G::TY, ZSmem<R, N>::bytes, stream>>>(p);
+        CK(cudaGetLastError());
+        return CM_OK;
+    }
+    int upload_real(const double* host, R* dst) {
+        CK(cudaMemcpyAsync(stage, host, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
+        to_real_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(stage, dst, L);
+        CK(cudaGetLastError());
+        return CM_OK;
+    }
+    int download_real(const R* src, double* host) {
+        to_double_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(src, stage, L);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(host, stage, sizeof(double) * L, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return CM_OK;
+    }
+
+    // ---- accumulator ---------------------------------------------------------------
+    int set_accumulator(const double* w, const double* y, int finalized) override {
+        CK(cudaMemcpyAsync(stage, w, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(stage + L, y, sizeof(double) * 2 * L, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemsetAsync(maxes, 0, sizeof(unsigned long long) * 4, stream));
+        const int blocks = grid_for(NN * (Nh + 1), 256);
+        convert_acc_kernel<R><<<blocks, 256, 0, stream>>>(N, stage, stage + L, W, Wn, Yh, Yn,
+                                                          part_acc, maxes);
+        CK(cudaGetLastError());
+        std::vector<double> parts(2 * (size_t)blocks);
+        unsigned long long mx[4];
+        CK(cudaMemcpyAsync(parts.data(), part_acc, sizeof(double) * parts.size(),
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(mx, maxes, sizeof(mx), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        double sw = 0.0, sz = 0.0;
+        for (int b = 0; b < blocks; ++b) {
+            sw += parts[2 * b];
+            sz += parts[2 * b + 1];
+        }
+        double worst, scale, wmax;
+        std::memcpy(&worst, &mx[0], 8);
+        std::memcpy(&scale, &mx[1], 8);
+        std::memcpy(&wmax, &mx[2], 8);
+        residue = scale > 0.0 ? worst / scale : 0.0;
+        max_weight = wmax;
+        s_n = sw / (double)L;
+        s_y = std::sqrt(sz) / (double)L; // Parseval: RMS = sqrt(sum |Z_H|^2 / L) / sqrt(L)
+        acc_set = true;
+        acc_finalized = finalized != 0;
+        return CM_OK;
+    }
+
+    int set_volumes(const double* xi, const double* xa) override {
+        CKS(upload_real(xi, x0keep));
+        anchor_is_init = (xa == xi);
+        if (anchor_is_init) {
+            CK(cudaMemcpyAsync(anchor, x0keep, sizeof(R) * L, cudaMemcpyDeviceToDevice, stream));
+        } else {
+            CKS(upload_real(xa, anchor));
+        }
+        CK(cudaStreamSynchronize(stream));
+        vol_set = true;
+        return CM_OK;
+    }
+
+    int require_acc() {
+        if (!acc_set) return fail(CM_ERR_STATE, "accumulator not set");
+        if (!acc_finalized || residue > 1e-9)
+            return fail(CM_ERR_NON_HERMITIAN, "accumulator is not Friedel-finalized");
+        return CM_OK;
+    }
+
+    // ---- the solver ------------------------------------------------------------------
+    int solve(const cm_reg_config* c, cm_trace_row* trace, int cap, cm_solve_stats* stats) override {
+        CKS(validate(c));
+        CKS(require_acc());
+        if (!vol_set) return fail(CM_ERR_STATE, "volumes not set");
+        const int K = c->inner_iters;
+        const bool lipschitz = c->step_rule == 0;
+        const bool fista = c->momentum == 1;
+        const bool convex = c->convex_mode != 0;
+        const bool want_trace = trace != nullptr && cap > 0;
+        const bool audit = !fista && (lipschitz || want_trace || c->tol_kind == 1);
+        const bool refresh_inner = (c->refresh == 0) && !convex;
+        // max w_tv is attained at voxel (0,0,0), where Dx = 0 under the
+        // replicate rule, so max w_tv = 1/eps' exactly (1 in convex mode)
+        const double max_wtv = convex ? 1.0 : 1.0 / c->eps_prime;
+        const double lr = lipschitz ? 1.0 / (2.0 * max_weight + 2.0 * c->gamma +
+                                             12.0 * c->beta * max_wtv / c->mu)
+                                    : c->fixed_step;
+        double slack = c->audit_slack;
+        if (!(slack > 0.0)) slack = sizeof(R) == 8 ? 1e-9 : 1e-6;
+
+        if (fista) {
+            for (auto& p : XF)
+                if (!p) CKS(dalloc(&p, L));
+            for (auto& p : YF)
+                if (!p) CKS(dalloc(&p, L));
+        }
+        const bool need_winit = (c->refresh == 1) && !convex && !anchor_is_init;
+        if (need_winit && !winit) CKS(dalloc(&winit, L));
+        if (want_trace && trace_rows_cap < K) {
+            if (trace_d) cudaFree(trace_d);
+            trace_d = nullptr;
+            CKS(dalloc(&trace_d, (size_t)K * 15));
+            trace_rows_cap = K;
+        }
+        if (fista && theta_cap < K + 1) {
+            if (theta_d) cudaFree(theta_d);
+            theta_d = nullptr;
+            CKS(dalloc(&theta_d, (size_t)K + 1));
+            theta_cap = K + 1;
+        }
+        if (fista) {
+            std::vector<double> th(K + 1);
+            double tk = 1.0;
+            for (int q = 0; q <= K; ++q) {
+                const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
+                th[q] = (tk - 1.0) / tn;
+                tk = tn;
+            }
+            CK(cudaMemcpyAsync(theta_d, th.data(), sizeof(double) * (K + 1),
+                               cudaMemcpyHostToDevice, stream));
+        }
+
+        // starting point and weight source
+        R* const x0buf = fista ? XF[0] : X[0];
+        CK(cudaMemcpyAsync(x0buf, x0keep, sizeof(R) * L, cudaMemcpyDeviceToDevice, stream));
+        if (fista)
+            CK(cudaMemcpyAsync(YF[0], x0keep, sizeof(R) * L, cudaMemcpyDeviceToDevice, stream));
+        if (need_winit)
+            CK(cudaMemcpyAsync(winit, x0keep, sizeof(R) * L, cudaMemcpyDeviceToDevice, stream));
+        const R* wfixed = (c->refresh == 1 && !convex) ? (anchor_is_init ? anchor : winit) : nullptr;
+
+        DevState hs{};
+        hs.iter = 0;
+        hs.max_iters = K;
+        hs.diverged_iter = -1;
+        hs.audit = audit;
+        hs.check_diverge = audit && lipschitz;
+        hs.tol_kind = c->tol_kind;
+        if (fista && hs.tol_kind == 1) hs.tol_kind = 2; // no surrogate audit under momentum
+        hs.fista = fista;
+        hs.refresh_inner = refresh_inner;
+        hs.tol = c->tol;
+        hs.audit_slack = slack;
+        hs.step = lr;
+        CK(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, stream));
+
+        const bool need_part1 = audit || hs.tol_kind == 2;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, stream));
+        int launches = 0;
+
+        // spectrum of the starting point: x R2C, y forward
+        {
+            XParams<R> p = xp();
+            p.xcur = fista ? YF[0] : X[0];
+            CKS(launch_x<XM_INIT>(p));
+            CKS(launch_y(true, nullptr));
+            launches += 2;
+        }
+
+        auto sweep_and_finalize = [&](int g, cudaEvent_t mid) -> int {
+            // K1
+            XParams<R> p = xp();
+            p.st = st;
+            p.lr = lr;
+            p.alpha = c->alpha;
+            p.beta = c->beta;
+            p.gamma = c->gamma;
+            p.eps = c->eps;
+            p.eps_prime = c->eps_prime;
+            p.mu = c->mu;
+            p.convex = convex;
+            p.audit = audit;
+            p.fista = fista;
+            p.anchor = anchor;
+            p.part = need_part1 ? part1 : nullptr;
+            if (fista) {
+                p.xcur = YF[g % 2];
+                p.xold = XF[g % 2];
+                p.xnext = XF[(g + 1) % 2];
+                p.ynext = YF[(g + 1) % 2];
+                p.theta = theta_d;
+            } else {
+                p.xcur = X[g % 3];
+                p.xnext = X[(g + 1) % 3];
+                p.xprev = (audit && refresh_inner) ? X[(g + 2) % 3] : nullptr;
+            }
+            p.wsrc = wfixed ? wfixed : p.xcur;
+            CKS(launch_x<XM_SWEEP>(p));
+            if (mid) CK(cudaEventRecord(mid, stream));
+            // FIN
+            FinParams f{};
+            f.st = st;
+            f.part1 = need_part1 ? part1 : nullptr;
+            f.nb1 = NB1;
+            f.part3 = audit ? part3 : nullptr;
+            f.nb3 = NB3;
+            f.trace = want_trace ? trace_d : nullptr;
+            f.alpha = c->alpha;
+            f.beta = c->beta;
+            f.gamma = c->gamma;
+            f.invL = 1.0 / (double)L;
+            f.epilogue = 0;
+            finalize_kernel<<<1, 256, 0, stream>>>(f);
+            CK(cudaGetLastError());
+            return CM_OK;
+        };
+        auto iteration = [&](int g) -> int {
+            CKS(launch_z<ZM_FULL>(audit ? part3 : nullptr, st));  // K3
+            CKS(launch_y(false, st));                              // K4
+            CKS(sweep_and_finalize(g, nullptr));                   // K1 + FIN
+            CKS(launch_y(true, st));                               // K2
+            return CM_OK;
+        };
+
+        const bool use_graph = std::getenv("CM_NO_GRAPH") == nullptr && !profiling;
+        const int chunk = 6;
+        const int nchunks = (K + chunk - 1) / chunk;
+        if (profiling) {
+            // per-kernel timing: same kernels, launched one by one between events
+            cudaEvent_t pe[6];
+            for (auto& e : pe) CK(cudaEventCreate(&e));
+            for (int q = 0; q < 5; ++q) prof_ms[q] = 0.0;
+            prof_iters = 0;
+            for (int g = 0; g < K; ++g) {
+                CK(cudaEventRecord(pe[0], stream));
+                CKS(launch_z<ZM_FULL>(audit ? part3 : nullptr, st));
+                CK(cudaEventRecord(pe[1], stream));
+                CKS(launch_y(false, st));
+                CK(cudaEventRecord(pe[2], stream));
+                CKS(sweep_and_finalize(g, pe[3]));
+                CK(cudaEventRecord(pe[4], stream));
+                CKS(launch_y(true, st));
+                CK(cudaEventRecord(pe[5], stream));
+                CK(cudaEventSynchronize(pe[5]));
+                for (int q = 0; q < 5; ++q) {
+                    float m = 0.f;
+                    CK(cudaEventElapsedTime(&m, pe[q], pe[q + 1]));
+                    prof_ms[q] += m;
+                }
+                ++prof_iters;
+                launches += 5;
+            }
+            for (auto& e : pe) cudaEventDestroy(e);
+        } else if (use_graph) {
+            cudaGraph_t graph;
+            cudaGraphExec_t exec;
+            CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            int rc = CM_OK;
+            for (int g = 0; g < chunk && rc == CM_OK; ++g) rc = iteration(g);
+            cudaError_t ce = cudaStreamEndCapture(stream, &graph);
+            if (rc != CM_OK) return rc;
+            CK(ce);
+            CK(cudaGraphInstantiate(&exec, graph, 0));
+            std::vector<cudaEvent_t> ev(LOOK);
+            for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (int q = 0; q < nchunks; ++q) {
+                if (q >= LOOK) {
+                    CK(cudaEventSynchronize(ev[q % LOOK]));
+                    if (flags_h[q % LOOK]) break;
+                }
+                CK(cudaGraphLaunch(exec, stream));
+                launches += 5 * chunk;
+                CK(cudaMemcpyAsync(&flags_h[q % LOOK], &st->done, sizeof(int),
+                                   cudaMemcpyDeviceToHost, stream));
+                CK(cudaEventRecord(ev[q % LOOK], stream));
+            }
+            CK(cudaStreamSynchronize(stream));
+            for (auto& e : ev) cudaEventDestroy(e);
+            cudaGraphExecDestroy(exec);
+            cudaGraphDestroy(graph);
+        } else {
+            for (int g = 0; g < K; ++g) {
+                CKS(iteration(g % 6));
+                launches += 5;
+            }
+        }
+
+        DevState rs;
+        CK(cudaMemcpyAsync(&rs, st, sizeof(rs), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (audit && rs.stop_reason == 1) {
+            // close the last trace row: fit(x_K) and the penalties of x_K under the
+            // weights of iteration K-1 (regularizer.cpp:208)
+            CKS(launch_z<ZM_FIT>(part3, nullptr));
+            XParams<R> p = xp();
+            p.eps = c->eps;
+            p.eps_prime = c->eps_prime;
+            p.mu = c->mu;
+            p.convex = convex;
+            p.audit = 1;
+            p.anchor = anchor;
+            p.part = part1;
+            p.xcur = X[K % 3];
+            p.xprev = refresh_inner ? X[(K + 2) % 3] : nullptr;
+            p.wsrc = wfixed ? wfixed : p.xcur;
+            CKS(launch_x<XM_OBJ>(p));
+            FinParams f{};
+            f.st = st;
+            f.part1 = part1;
+            f.nb1 = NB1;
+            f.part3 = part3;
+            f.nb3 = NB3;
+            f.trace = want_trace ? trace_d : nullptr;
+            f.alpha = c->alpha;
+            f.beta = c->beta;
+            f.gamma = c->gamma;
+            f.invL = 1.0 / (double)L;
+            f.epilogue = 1;
+            finalize_kernel<<<1, 256, 0, stream>>>(f);
+            CK(cudaGetLastError());
+            launches += 3;
+            CK(cudaMemcpyAsync(&rs, st, sizeof(rs), cudaMemcpyDeviceToHost, stream));
+        }
+        CK(cudaEventRecord(e1, stream));
+        CK(cudaStreamSynchronize(stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+
+        const int rows = std::min(rs.rows, want_trace ? cap : 0);
+        if (want_trace && rows > 0) {
+            std::vector<double> tr((size_t)rows * 15);
+            CK(cudaMemcpy(tr.data(), trace_d, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost));
+            for (int r = 0; r < rows; ++r) {
+                std::memcpy(trace[r].before, &tr[15 * r], 7 * sizeof(double));
+                std::memcpy(trace[r].after, &tr[15 * r + 7], 7 * sizeof(double));
+                trace[r].step = tr[15 * r + 14];
+            }
+        }
+        last_iter = rs.iter;
+        last_fista = fista;
+        result_valid = rs.stop_reason != 3;
+        if (stats) {
+            stats->iterations = rs.iter;
+            stats->trace_rows = rows;
+            stats->stop_reason = rs.stop_reason;
+            stats->diverged_iter = rs.diverged_iter;
+            stats->last_rel = rs.last_rel;
+            stats->step = lr;
+            stats->solve_ms = ms;
+            stats->kernel_launches = launches;
+        }
+        if (rs.stop_reason == 3)
+            return fail(CM_ERR_STEP_DIVERGED, "m_step: frozen-weight objective increased");
+        return CM_OK;
+    }
+
+    int get_volume(double* out) override {
+        if (!vol_set || !result_valid) return fail(CM_ERR_STATE, "no solver result resident");
+        const R* src = last_fista ? XF[last_iter % 2] : X[last_iter % 3];
+        return download_real(src, out);
+    }
+
+    // ---- component entry points ---------------------------------------------------------
+    int spectrum_of(const R* x) { // S <- x R2C, y forward, z forward (packed full spectrum)
+        XParams<R> p = xp();
+        p.xcur = x;
+        CKS(launch_x<XM_INIT>(p));
+        CKS(launch_y(true, nullptr));
+        return CM_OK;
+    }
+
+    int data_gradient(const double* x, double* out) override {
+        CKS(require_acc());
+        CKS(upload_real(x, X[0]));
+        CKS(spectrum_of(X[0]));
+        CKS(launch_z<ZM_FULL>(nullptr, nullptr));
+        CKS(launch_y(false, nullptr));
+        XParams<R> p = xp();
+        p.xnext = X[1];
+        CKS(launch_x<XM_DGRAD>(p));
+        result_valid = false; // X[] reused as scratch; x0keep / anchor untouched
+        return download_real(X[1], out);
+    }
+
+    int weights(const double* x, double eps, double epsp, int convex, double* wl1,
+                double* wtv) override {
+        result_valid = false;
+        CKS(upload_real(x, X[0]));
+        XParams<R> p = xp();
+        p.xcur = X[0];
+        p.wsrc = X[0];
+        p.eps = eps;
+        p.eps_prime = epsp;
+        p.convex = convex;
+        p.xnext = X[1];
+        p.ynext = X[2];
+        CKS(launch_x<XM_WEIGHTS>(p));
+        CKS(download_real(X[1], wl1));
+        return download_real(X[2], wtv);
+    }
+
+    int tv(const double* x, double mu, const double* wtv, double* value, double* grad) override {
+        result_valid = false;
+        CKS(upload_real(x, X[0]));
+        if (wtv) CKS(upload_real(wtv, X[2]));
+        XParams<R> p = xp();
+        p.xcur = X[0];
+        p.wsrc = X[0];
+        p.mu = mu;
+        p.eps = 1.0;
+        p.eps_prime = 1.0;
+        p.convex = wtv ? 0 : 1;
+        p.wtvf = wtv ? X[2] : nullptr;
+        if (grad) {
+            p.xnext = X[1];
+            CKS(launch_x<XM_TVGRAD>(p));
+            CKS(download_real(X[1], grad));
+        }
+        if (value) {
+            p.part = part1;
+            CKS(launch_x<XM_OBJ>(p));
+            std::vector<double> h((size_t)NB1 * NP1);
+            CK(cudaMemcpyAsync(h.data(), part1, sizeof(double) * h.size(),
+                               cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            double s = 0.0;
+            for (int b = 0; b < NB1; ++b) s += h[(size_t)b * NP1 + 1];
+            *value = s;
+        }
+        return CM_OK;
+    }
+
+    int prox(const double* x, const double* t, double* out) override {
+        CK(cudaMemcpyAsync(stage, x, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(stage + L, t, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
+        prox_kernel<<<grid_for(L, 256), 256, 0, stream>>>(stage, stage + L, stage + 2 * L, L);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, stage + 2 * L, sizeof(double) * L, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return CM_OK;
+    }
+
+    int objective(const double* x, const cm_reg_config* c, const double* anc, const double* wsrc,
+                  double* out7) override {
+        result_valid = false;
+        CKS(validate(c));
+        CKS(require_acc());
+        CKS(upload_real(x, X[0]));
+        CKS(upload_real(anc, X[1]));
+        CKS(upload_real(wsrc, X[2]));
+        CKS(spectrum_of(X[0]));
+        CKS(launch_z<ZM_FIT>(part3, nullptr));
+        XParams<R> p = xp();
+        p.xcur = X[0];
+        p.anchor = X[1];
+        p.wsrc = X[2];
+        p.eps = c->eps;
+        p.eps_prime = c->eps_prime;
+        p.mu = c->mu;
+        p.convex = c->convex_mode;
+        p.audit = 1;
+        p.part = part1;
+        CKS(launch_x<XM_OBJ>(p));
+        std::vector<double> h1((size_t)NB1 * NP1), h3((size_t)NB3 * NP3);
+        CK(cudaMemcpyAsync(h1.data(), part1, sizeof(double) * h1.size(), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(h3.data(), part3, sizeof(double) * h3.size(), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        double s[NP1] = {}, q = 0.0, cr = 0.0;
+        for (int b = 0; b < NB1; ++b)
+            for (int k = 0; k < NP1; ++k) s[k] += h1[(size_t)b * NP1 + k];
+        for (int b = 0; b < NB3; ++b) {
+            q += h3[(size_t)b * NP3];
+            cr += h3[(size_t)b * NP3 + 1];
+        }
+        out7[0] = (q - 2.0 * cr) / (double)L;
+        out7[1] = c->alpha * s[0];
+        out7[2] = c->beta * s[1];
+        out7[3] = c->beta * s[2];
+        out7[4] = c->gamma * s[5];
+        out7[5] = c->alpha * s[3];
+        out7[6] = c->beta * s[4];
+        return CM_OK;
+    }
+
+    int fft3(const double* x, double* out) override {
+        result_valid = false;
+        CKS(upload_real(x, X[0]));
+        CKS(spectrum_of(X[0]));
+        CKS(launch_z<ZM_FWD>(nullptr, nullptr));
+        std::vector<C> h(H);
+        CK(cudaMemcpyAsync(h.data(), S, sizeof(C) * H, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        // unpack to the full grid: h in (0, Nh) direct + Friedel mate; column 0
+        // carries F(0,b,c) + i F(Nh,b,c)
+        auto put = [&](int a, int b, int c, double re, double im) {
+            const size_t i = ((size_t)c * N + b) * N + a;
+            out[2 * i] = re;
+            out[2 * i + 1] = im;
+        };
+        for (int c = 0; c < N; ++c)
+            for (int b = 0; b < N; ++b) {
+                const int bm = (N - b) % N, cmt = (N - c) % N;
+                for (int a = 1; a < Nh; ++a) {
+                    const C z = h[((size_t)c * N + b) * Nh + a];
+                    put(a, b, c, z.x, z.y);
+                    put(N - a, bm, cmt, z.x, -z.y);
+                }
+                const C z = h[((size_t)c * N + b) * Nh];
+                const C zm = h[((size_t)cmt * N + bm) * Nh];
+                put(0, b, c, 0.5 * ((double)z.x + zm.x), 0.5 * ((double)z.y - zm.y));
+                put(Nh, b, c, 0.5 * ((double)z.y + zm.y), -0.5 * ((double)z.x - zm.x));
+            }
+        return CM_OK;
+    }
+};
+
+
+} // namespace cm

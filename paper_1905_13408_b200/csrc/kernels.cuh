@@ -1,0 +1,497 @@
+// M-step solver kernels for sm_100a. See DESIGN.md for the schedule.
+//
+// Storage (real-space, x fastest, flat (k*N + j)*N + i as volume.hpp:13):
+//   x      R[N][N][N]
+// Half spectrum, PACKED (Nh = N/2 columns per row):
+//   S      C[N][N][Nh]   column 0 holds X(0) + i X(Nh) of the x-transform,
+//                        i.e. after the y/z transforms F(0,b,c) + i F(Nh,b,c)
+//   W      R[N][N][Nh] + Wn R[N][N]   (h = Nh plane stored separately)
+//   Yh     C[N][N][Nh] + Yn C[N][N]   Yh = (-1)^(a+b+c) * Hermitian part of Y
+//
+// Per iteration i (SURVEY §8(d) canonical 4-kernel schedule):
+//   K3  z-forward, fit partials, G = W.F - Yh, z-inverse        (zpass_kernel)
+//   K4  y-inverse                                               (ypass_kernel<false>)
+//   K1  x C2R -> g; weights + Huber-TV stencil + ISTA/FISTA update + prox
+//       + objective partials; x R2C of x_{i+1}                   (xline_kernel)
+//   FIN fixed-order reduction of partials, trace row, audit     (finalize_kernel)
+//   K2  y-forward                                               (ypass_kernel<true>)
+#pragma once
+
+#include "cm_common.cuh"
+#include "fft_engine.cuh"
+
+namespace cm {
+
+enum XMode { XM_INIT = 0, XM_SWEEP = 1, XM_OBJ = 2, XM_DGRAD = 3, XM_TVGRAD = 4, XM_WEIGHTS = 5 };
+enum ZMode { ZM_FULL = 0, ZM_FIT = 1, ZM_FWD = 2 };
+
+constexpr int NP1 = 11; // xline partial slots
+constexpr int NP3 = 2;  // zpass partial slots
+
+// ---- compile-time geometry ----------------------------------------------------
+__host__ __device__ constexpr int pow2_divisor_le(int v, int cap) {
+    int t = 1;
+    while (t * 2 <= cap && v % (t * 2) == 0) t *= 2;
+    return t;
+}
+
+template <typename R, int N> struct Geo {
+    using C = Cx<R>;
+    static constexpr int Nh = N / 2;
+    // x lines: transform length Nh
+    static constexpr int EX = elems_for(Nh);
+    static constexpr int TX = Nh / EX;
+    static constexpr int LPC = (256 / TX) < 1 ? 1 : (256 / TX);   // lines per CTA
+    static constexpr int PADX = Nh + (Nh >> 3) + 1;                 // padded line buffer (complex)
+    // y / z columns: transform length N
+    static constexpr int EY = elems_for(N);
+    static constexpr int TY = N / EY;
+    static constexpr int SMEM_CAP = 96 * 1024; // per tile buffer budget (bytes)
+    static constexpr int TWY_CAP = (SMEM_CAP / (N * (int)sizeof(C))) < 1 ? 1 : (SMEM_CAP / (N * (int)sizeof(C)));
+    static constexpr int TWY = pow2_divisor_le(Nh, (16 < (1024 / TY) ? 16 : (1024 / TY)) < TWY_CAP ? (16 < (1024 / TY) ? 16 : (1024 / TY)) : TWY_CAP);
+    static constexpr int TW3_LIM = (512 / TY) < 1 ? 1 : (512 / TY);
+    static constexpr int TW3_CAP = TWY_CAP / 2 < 1 ? 1 : TWY_CAP / 2;
+    static constexpr int TW3 = pow2_divisor_le(Nh, (16 < TW3_LIM ? 16 : TW3_LIM) < TW3_CAP ? (16 < TW3_LIM ? 16 : TW3_LIM) : TW3_CAP);
+};
+
+// ---- parameters -----------------------------------------------------------------
+template <typename R> struct XParams {
+    using C = Cx<R>;
+    C* S;               // packed spectrum (in: G rows for SWEEP/DGRAD, out: rows of x_{i+1})
+    const R* xcur;      // point of the stencil / gradient (x_i, or y_k for FISTA)
+    const R* xprev;     // previous iterate for after_{i-1} weights (per_inner audit), or null
+    const R* wsrc;      // weight source (per_inner: xcur; per_m_step: x_init)
+    const R* anchor;    // restraint anchor
+    const R* xold;      // FISTA: x_k (momentum base); null otherwise
+    const R* wtvf;      // explicit w_tv field (component API), or null
+    R* xnext;           // x_{i+1} out (SWEEP) / g or tv-gradient out (DGRAD/TVGRAD)
+    R* ynext;           // FISTA: y_{k+1} out
+    const C* twN;       // exp(-2 pi i q / N), q < N (global; staged into smem)
+    const double* theta; // FISTA momentum per iteration (indexed by st->iter)
+    double* part;       // [gridDim.x][NP1]
+    DevState* st;
+    double lr, alpha, beta, gamma, eps, eps_prime, mu, invL;
+    int convex, audit, fista;
+};
+
+template <typename R> struct ZParams {
+    using C = Cx<R>;
+    C* S;
+    const R* W;
+    const R* Wn;
+    const C* Yh;
+    const C* Yn;
+    const C* twN;
+    double* part; // [grid][NP3]
+    DevState* st;
+};
+
+template <typename R> struct YParams {
+    using C = Cx<R>;
+    C* S;
+    const C* twN;
+    DevState* st;
+};
+
+template <typename C>
+__device__ __forceinline__ void stage_table(C* dst, const C* src, int n) {
+    for (int q = threadIdx.x; q < n; q += blockDim.x) dst[q] = src[q];
+}
+
+// ==================================================================================
+// y pass: FFT along j for every (k, h) column. grid = (Nh/TWY, N)
+// ==================================================================================
+template <typename R, int N, bool FWD>
+__global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY)
+ypass_kernel(YParams<R> p) {
+    using G = Geo<R, N>;
+    using C = Cx<R>;
+    if (p.st && ld_done(p.st)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tw = reinterpret_cast<C*>(smem_raw);
+    C* buf = tw + N;
+    stage_table(tw, p.twN, N);
+    const int col = threadIdx.x % G::TWY;
+    const int t = threadIdx.x / G::TWY;
+    const int h = blockIdx.x * G::TWY + col;
+    const int k = blockIdx.y;
+    C* base = p.S + (size_t)k * N * G::Nh + h;
+    C v[G::EY];
+#pragma unroll
+    for (int m = 0; m < G::EY; ++m) v[m] = base[(size_t)(t + G::TY * m) * G::Nh];
+    __syncthreads();
+    fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw, BlockSync{});
+#pragma unroll
+    for (int m = 0; m < G::EY; ++m) base[(size_t)(t + G::TY * m) * G::Nh] = v[m];
+}
+
+// ==================================================================================
+// z pass: FFT along k for every (b, h) column, fused Fourier-weight multiply and
+// fit partials. A block owns the row pair (b, -b) of one h tile so that the
+// packed column 0 can be unpacked with its Friedel mate. grid = (Nh/TW3, N/2+1)
+// ==================================================================================
+template <typename R, int N, int MODE>
+__global__ void __launch_bounds__(2 * Geo<R, N>::TW3 * Geo<R, N>::TY)
+zpass_kernel(ZParams<R> p) {
+    using G = Geo<R, N>;
+    using C = Cx<R>;
+    constexpr int TW = G::TW3, T = G::TY, E = G::EY, Nh = G::Nh;
+    if (p.st && ld_done(p.st)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tw = reinterpret_cast<C*>(smem_raw);
+    C* buf0 = tw + N;             // [2][N][TW]
+    C* z0 = buf0 + 2 * N * TW;    // [2][N] column-0 values for the mate unpack
+    double* red = reinterpret_cast<double*>(z0 + 2 * N);
+    stage_table(tw, p.twN, N);
+
+    const int col = threadIdx.x % TW;
+    const int t = (threadIdx.x / TW) % T;
+    const int r = threadIdx.x / (TW * T);
+    const int bp = blockIdx.y;
+    const int b = r == 0 ? bp : (N - bp) % N;
+    const bool active = (r == 0) || (b != bp);
+    const int h = blockIdx.x * TW + col;
+    const size_t plane = (size_t)N * Nh;
+    C* base = p.S + (size_t)b * Nh + h;
+    C* buf = buf0 + r * N * TW;
+
+    C v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m)
+        v[m] = active ? base[(size_t)(t + T * m) * plane] : cx<C>(R(0), R(0));
+    __syncthreads();
+    fft_regs<N, E, N, true>(v, t, buf, ColAddr{TW, col}, tw, BlockSync{});
+
+    if constexpr (MODE == ZM_FWD) {
+        if (active)
+#pragma unroll
+            for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
+        return;
+    }
+
+    // column 0: publish both rows so each can read its Friedel mate Z(-b,-c)
+    const bool col0 = (blockIdx.x == 0) && (col == 0);
+    if (col0)
+#pragma unroll
+        for (int m = 0; m < E; ++m) z0[r * N + t + T * m] = v[m];
+    __syncthreads();
+
+    double quad = 0.0, cross = 0.0;
+    if (active) {
+        const int rm = (b == bp && bp == (N - bp) % N) ? r : 1 - r; // self-paired rows
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int c = t + T * m;
+            const size_t gi = ((size_t)c * N + b) * Nh + h;
+            if (!col0) {
+                const R w = p.W[gi];
+                const C y = p.Yh[gi];
+                const C f = v[m];
+                quad += 2.0 * (double)w * ((double)f.x * f.x + (double)f.y * f.y);
+                cross += 2.0 * ((double)y.x * f.x + (double)y.y * f.y);
+                v[m] = cx<C>(w * f.x - y.x, w * f.y - y.y);
+            } else {
+                const C zm = z0[rm * N + (N - c) % N];
+                const C zz = v[m];
+                // F0 = (Z + conj Zm)/2, FN = (Z - conj Zm)/(2i)
+                const C f0 = cx<C>(R(0.5) * (zz.x + zm.x), R(0.5) * (zz.y - zm.y));
+                const C fn = cx<C>(R(0.5) * (zz.y + zm.y), R(-0.5) * (zz.x - zm.x));
+                const size_t ni = (size_t)c * N + b;
+                const R w0 = p.W[gi], wn = p.Wn[ni];
+                const C y0 = p.Yh[gi], yn = p.Yn[ni];
+                quad += (double)w0 * ((double)f0.x * f0.x + (double)f0.y * f0.y) +
+                        (double)wn * ((double)fn.x * fn.x + (double)fn.y * fn.y);
+                cross += ((double)y0.x * f0.x + (double)y0.y * f0.y) +
+                         ((double)yn.x * fn.x + (double)yn.y * fn.y);
+                const C g0 = cx<C>(w0 * f0.x - y0.x, w0 * f0.y - y0.y);
+                const C gn = cx<C>(wn * fn.x - yn.x, wn * fn.y - yn.y);
+                v[m] = cx<C>(g0.x - gn.y, g0.y + gn.x); // g0 + i gn
+            }
+        }
+    }
+    if (p.part) {
+        double acc[2] = {quad, cross};
+        block_sum<2>(acc, red);
+        if (threadIdx.x == 0) {
+            const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+            p.part[bid * NP3 + 0] = acc[0];
+            p.part[bid * NP3 + 1] = acc[1];
+        }
+    }
+    if constexpr (MODE == ZM_FIT) return;
+    __syncthreads();
+    fft_regs<N, E, N, false>(v, t, buf, ColAddr{TW, col}, tw, BlockSync{});
+    if (active)
+#pragma unroll
+        for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
+}
+
+// ==================================================================================
+// x lines: C2R -> data gradient; fused stencil sweep; R2C of the new iterate.
+// ==================================================================================
+template <typename R> struct Vox {
+    const R* x;
+    int N;
+    __device__ __forceinline__ R at(int i, int j, int k) const {
+        return __ldg(x + ((size_t)k * N + j) * N + i);
+    }
+};
+
+// ||D x|| at (i,j,k) with the replicate rule (gradient.cpp:7-24), given x there
+template <typename R>
+__device__ __forceinline__ void grad3(const Vox<R>& v, int i, int j, int k, R xc, R& d1, R& d2,
+                                      R& d3) {
+    d1 = i > 0 ? xc - v.at(i - 1, j, k) : R(0);
+    d2 = j > 0 ? xc - v.at(i, j - 1, k) : R(0);
+    d3 = k > 0 ? xc - v.at(i, j, k - 1) : R(0);
+}
+
+template <typename R> __device__ __forceinline__ R rnorm3(R a, R b, R c) {
+    return sqrt(a * a + b * b + c * c);
+}
+template <typename R> __device__ __forceinline__ R huber(R g, R mu) {
+    return g < mu ? g * g / (R(2) * mu) : g - mu / R(2);
+}
+
+template <typename R, int N, int MODE>
+__global__ void __launch_bounds__(Geo<R, N>::LPC * Geo<R, N>::TX)
+xline_kernel(XParams<R> p) {
+    using G = Geo<R, N>;
+    using C = Cx<R>;
+    constexpr int Nh = G::Nh, E = G::EX, T = G::TX, LPC = G::LPC, PADX = G::PADX;
+    if (p.st && ld_done(p.st)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tw = reinterpret_cast<C*>(smem_raw);
+    C* lines = tw + N;                                   // [LPC][PADX]
+    double* red = reinterpret_cast<double*>(lines + LPC * PADX);
+    stage_table(tw, p.twN, N);
+    __syncthreads();
+
+    const int lg = threadIdx.x / T;  // line within CTA
+    const int t = threadIdx.x % T;
+    const int line = blockIdx.x * LPC + lg;
+    const bool valid = line < N * N;
+    const int j = valid ? line % N : 0;
+    const int k = valid ? line / N : 0;
+    C* buf = lines + lg * PADX;     // exchange buffer (padded layout)
+    R* rl = reinterpret_cast<R*>(buf); // real line view (linear), aliases buf
+    C* Srow = p.S + (size_t)line * Nh;
+    const PadAddr pad{};
+    // Lines of one group never straddle warps (T | 32); __syncwarp is the barrier.
+    const WarpSync wsync{};
+
+    C v[E];
+    if constexpr (MODE == XM_SWEEP || MODE == XM_DGRAD) {
+        // ---- C2R: Q(h) for h = t + T m -> Z(h) = A + i B, inverse FFT_Nh
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = valid ? Srow[t + T * m] : cx<C>(R(0), R(0));
+#pragma unroll
+        for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int hh = t + T * m;
+            const C q = v[m];
+            if (hh == 0) {
+                v[m] = cx<C>(q.x + q.y, q.x - q.y);
+            } else {
+                const C qm = buf[pad(Nh - hh)];
+                const C a = cx<C>(q.x + qm.x, q.y - qm.y);      // Q + conj(Qm)
+                const C d = cx<C>(q.x - qm.x, q.y + qm.y);      // Q - conj(Qm)
+                const C bb = cmulc(d, tw[hh]);                  // * exp(+2 pi i h/N)
+                v[m] = cx<C>(a.x - bb.y, a.y + bb.x);           // A + i B
+            }
+        }
+        __syncwarp();
+        fft_regs<Nh, E, N, false>(v, t, buf, pad, tw, wsync);
+        __syncwarp();
+        // z(p) = g(2p) + i g(2p+1), unnormalised
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int pp = t + T * m;
+            rl[2 * pp] = v[m].x;
+            rl[2 * pp + 1] = v[m].y;
+        }
+        __syncwarp();
+    }
+
+    if constexpr (MODE == XM_DGRAD) {
+        if (valid)
+            for (int i = t; i < N; i += T)
+                p.xnext[(size_t)line * N + i] = rl[i] * R(p.invL);
+        return;
+    }
+
+    double acc[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) acc[q] = 0.0;
+
+    if constexpr (MODE == XM_SWEEP || MODE == XM_OBJ || MODE == XM_TVGRAD ||
+                  MODE == XM_WEIGHTS) {
+        const Vox<R> X{p.xcur, N};
+        const Vox<R> Wv{p.wsrc, N};
+        const bool same_w = (p.wsrc == p.xcur);
+        const R eps = R(p.eps), epsp = R(p.eps_prime), mu = R(p.mu);
+        const R lr = R(p.lr), alpha = R(p.alpha), beta = R(p.beta), gamma = R(p.gamma);
+        const bool want_tv = (MODE == XM_TVGRAD) || (MODE == XM_SWEEP && p.beta > 0.0);
+        const bool audit = (MODE == XM_OBJ) || (MODE == XM_SWEEP && p.audit);
+        R theta = R(0);
+        if (MODE == XM_SWEEP && p.fista) theta = R(p.theta[p.st ? p.st->iter : 0]);
+        // w_tv at a voxel whose own gradient norm is qn (regularizer.cpp:44-59)
+        auto wtv_at = [&](int ii, int jj, int kk, R qn) -> R {
+            if (p.convex) return R(1);
+            if (p.wtvf) return __ldg(p.wtvf + ((size_t)kk * N + jj) * N + ii);
+            if (same_w) return R(1) / (qn + epsp);
+            R e1, e2, e3;
+            grad3(Wv, ii, jj, kk, Wv.at(ii, jj, kk), e1, e2, e3);
+            return R(1) / (rnorm3(e1, e2, e3) + epsp);
+        };
+        if (valid) {
+            for (int i = t; i < N; i += T) {
+                const size_t gi = (size_t)line * N + i;
+                const R xc = X.at(i, j, k);
+                R d1, d2, d3;
+                grad3(X, i, j, k, xc, d1, d2, d3);
+                const R gn = rnorm3(d1, d2, d3);
+                const R wl1 = p.convex ? R(1)
+                                       : R(1) / (fabs(same_w ? xc : Wv.at(i, j, k)) + eps);
+                const R wtv = wtv_at(i, j, k, gn);
+                if constexpr (MODE == XM_WEIGHTS) {
+                    p.xnext[gi] = wl1;
+                    p.ynext[gi] = wtv;
+                    continue;
+                }
+                R tvg = R(0);
+                if (want_tv) {
+                    // D*(s Dx) with s = w_tv / max(mu, ||Dx||) (regularizer.cpp:72-85,
+                    // adjoint gradient.cpp:29-64)
+                    const R s0 = wtv / (mu > gn ? mu : gn);
+                    tvg = s0 * (d1 + d2 + d3);
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        if ((ax == 0 && i == N - 1) || (ax == 1 && j == N - 1) ||
+                            (ax == 2 && k == N - 1))
+                            continue;
+                        const int ii = i + (ax == 0), jj = j + (ax == 1), kk = k + (ax == 2);
+                        const R xq = X.at(ii, jj, kk);
+                        R q1, q2, q3;
+                        grad3(X, ii, jj, kk, xq, q1, q2, q3);
+                        const R qn = rnorm3(q1, q2, q3);
+                        const R sq = wtv_at(ii, jj, kk, qn) / (mu > qn ? mu : qn);
+                        tvg -= sq * (ax == 0 ? q1 : (ax == 1 ? q2 : q3));
+                    }
+                }
+                if constexpr (MODE == XM_TVGRAD) {
+                    p.xnext[gi] = tvg;
+                    continue;
+                }
+                const R av = p.anchor ? __ldg(p.anchor + gi) : R(0);
+                if (audit) {
+                    const double ax = fabs((double)xc);
+                    const double hb = (double)huber(gn, mu);
+                    acc[0] += (double)wl1 * ax;
+                    acc[1] += (double)wtv * hb;
+                    acc[2] += (double)wtv * (double)gn;
+                    acc[3] += (double)log(fabs(xc) + eps);
+                    acc[4] += (double)log(gn + epsp);
+                    const double dd = (double)xc - (double)av;
+                    acc[5] += dd * dd;
+                    if (p.xprev) {
+                        const Vox<R> P{p.xprev, N};
+                        const R pc = P.at(i, j, k);
+                        R e1, e2, e3;
+                        grad3(P, i, j, k, pc, e1, e2, e3);
+                        const double pl1 = 1.0 / (fabs((double)pc) + p.eps);
+                        const double ptv = 1.0 / ((double)rnorm3(e1, e2, e3) + p.eps_prime);
+                        acc[6] += pl1 * ax;
+                        acc[7] += ptv * hb;
+                        acc[8] += ptv * (double)gn;
+                    }
+                }
+                if constexpr (MODE == XM_SWEEP) {
+                    // update + prox (regularizer.cpp:193-205, 103-110)
+                    const R g = rl[i] * R(p.invL);
+                    R gs = R(2) * g + R(2) * gamma * (xc - av);
+                    if (p.beta > 0.0) gs += beta * tvg;
+                    R nx = xc - lr * gs;
+                    if (p.alpha > 0.0) {
+                        const R th = lr * alpha * wl1;
+                        nx = fabs(nx) <= th ? R(0) : nx - copysign(th, nx);
+                    }
+                    R base = xc;
+                    if (p.fista) base = __ldg(p.xold + gi);
+                    const double dx = (double)nx - (double)base;
+                    acc[9] += dx * dx;
+                    acc[10] += (double)nx * (double)nx;
+                    p.xnext[gi] = nx;
+                    R spec = nx;
+                    if (p.fista) {
+                        spec = nx + theta * (nx - base);
+                        p.ynext[gi] = spec;
+                    }
+                    rl[i] = spec; // the new spectrum is taken of x_{i+1} (or y_{k+1})
+                }
+            }
+        }
+    }
+
+    if constexpr (MODE == XM_INIT) {
+        if (valid)
+            for (int i = t; i < N; i += T) rl[i] = __ldg(p.xcur + (size_t)line * N + i);
+    }
+
+    if constexpr (MODE == XM_SWEEP || MODE == XM_INIT) {
+        __syncwarp();
+        // ---- R2C: z(p) = x(2p) + i x(2p+1) -> FFT_Nh -> split into X(h), pack
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int pp = t + T * m;
+            v[m] = cx<C>(rl[2 * pp], rl[2 * pp + 1]);
+        }
+        __syncwarp();
+        fft_regs<Nh, E, N, true>(v, t, buf, pad, tw, wsync);
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int hh = t + T * m;
+            const C z = v[m];
+            C out;
+            if (hh == 0) {
+                out = cx<C>(z.x + z.y, z.x - z.y); // X(0) + i X(Nh)
+            } else {
+                const C zm = buf[pad(Nh - hh)];
+                const C e = cx<C>(R(0.5) * (z.x + zm.x), R(0.5) * (z.y - zm.y)); // (Z + conj Zm)/2
+                // O = (Z - conj Zm)/(2i): d = Z - conj Zm ; O = (d.y/2, -d.x/2)
+                const C o = cx<C>(R(0.5) * (z.y + zm.y), R(-0.5) * (z.x - zm.x));
+                out = cadd(e, cmul(o, tw[hh]));
+            }
+            if (valid) Srow[hh] = out;
+        }
+    }
+
+    if constexpr (MODE == XM_SWEEP || MODE == XM_OBJ) {
+        if (p.part) {
+            block_sum<NP1>(acc, red);
+            if (threadIdx.x == 0)
+#pragma unroll
+                for (int q = 0; q < NP1; ++q) p.part[(size_t)blockIdx.x * NP1 + q] = acc[q];
+        }
+    }
+}
+
+template <typename R, int N> struct XSmem {
+    static constexpr size_t bytes =
+        sizeof(Cx<R>) * (N + Geo<R, N>::LPC * Geo<R, N>::PADX) + sizeof(double) * 32 * NP1;
+};
+template <typename R, int N> struct YSmem {
+    static constexpr size_t bytes = sizeof(Cx<R>) * (N + (size_t)N * Geo<R, N>::TWY);
+};
+template <typename R, int N> struct ZSmem {
+    static constexpr size_t bytes =
+        sizeof(Cx<R>) * (N + 2 * (size_t)N * Geo<R, N>::TW3 + 2 * N) + sizeof(double) * 32 * NP3;
+};
+
+} // namespace cm

@@ -1,0 +1,200 @@
+"""GPU parity tests: the sm_100a solver (through the C ABI) against the
+reference's golden vectors (tests/golden, produced by the unmodified
+reference) and the oracle restatement on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  fp32 (product mode): per-iteration objective fields within 1e-5 relative
+                       (relative to max(|field|, |surrogate|)), final volume
+                       within 1e-4 relative L2.
+  fp64 (parity mode):  1e-9 relative — the reference's own audit slack.
+"""
+import numpy as np
+import pytest
+
+import paper_1905_13408_b200 as cm
+from paper_1905_13408_b200 import synth
+from golden.make_golden import CONFIGS, random_accumulator, random_volume, sha
+from oracle_lib import Oracle, make_cfg
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(__import__("pathlib").Path(__file__).parent / "golden" / "reference_golden.npz")
+TOL = {32: dict(obj=1e-5, vol=1e-4, pt=2e-5), 64: dict(obj=1e-9, vol=1e-9, pt=1e-10)}
+
+
+@pytest.fixture(scope="module")
+def O():
+    return Oracle()
+
+
+def acc_of(w, y, finalized=True):
+    return cm.AccumulatorPair(w.shape[0], y, w, finalized)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def check_trace(rows, ref, tol):
+    got = np.array([np.r_[r.before.as_array(), r.after.as_array(), r.step] for r in rows])
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    for half in (slice(0, 7), slice(7, 14)):
+        g, r = got[:, half], ref[:, half]
+        surr = np.abs(r[:, 0] + r[:, 1] + r[:, 2] + r[:, 4])
+        scale = np.maximum(np.abs(r), surr[:, None])
+        err = np.abs(g - r) / scale
+        assert err.max() <= tol, (half, err.max(), np.unravel_index(err.argmax(), err.shape))
+    np.testing.assert_allclose(got[:, 14], ref[:, 14], rtol=1e-12)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("n", [4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128])
+def test_fft3_matches_reference_convention(n, prec):
+    """fourier.hpp:6-9: unnormalised forward transform (test_grid_fourier KATs)."""
+    x = np.random.default_rng(n).standard_normal((n, n, n))
+    F = cm.fft3(x, precision=prec)
+    want = np.fft.fftn(x)
+    tol = 1e-12 if prec == 64 else 2e-6
+    assert np.abs(F - want).max() <= tol * np.abs(want).max()
+    d = np.zeros((n, n, n))
+    d[0, 0, 0] = 1.0
+    np.testing.assert_allclose(cm.fft3(d, precision=prec), np.ones((n, n, n)), atol=tol)
+
+
+def test_fft3_golden():
+    x = random_volume(6, 3)
+    np.testing.assert_allclose(cm.fft3(x, precision=64), G["fft6"], atol=1e-12)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("n,seed", [(6, 11), (8, 12)])
+def test_data_gradient_and_scales_golden(n, seed, prec):
+    w, y = random_accumulator(n, seed)
+    x = random_volume(n, seed + 100)
+    assert sha(w, y, x) == str(G[f"racc{n}_sha"])
+    acc = acc_of(w, y)
+    g = cm.data_gradient(x, acc, precision=prec)
+    ref = G[f"racc{n}_dgrad"]
+    assert np.abs(g - ref).max() <= TOL[prec]["pt"] * max(1.0, np.abs(ref).max()) * 10
+    s = cm.scale_data(acc, precision=prec)
+    np.testing.assert_allclose([s.s_y, s.s_n], G[f"racc{n}_scales"], rtol=1e-12)
+    ctx = cm.context(n, prec)
+    assert abs(ctx.accumulator_info()[0] - G[f"racc{n}_resid"][0]) < 1e-15
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("n", [16, 32])
+def test_m_step_traces_golden(n, prec):
+    """Per-iteration ObjectiveValue (before/after) and final volume of the
+    reference m_step, four RegConfig modes."""
+    p = synth.synthetic_problem(n)
+    k = f"prob{n}"
+    assert sha(p.weight, p.numerator, p.x0) == str(G[k + "_sha"])
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    np.testing.assert_allclose([s.s_y, s.s_n], G[k + "_scales"], rtol=1e-12)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    np.testing.assert_allclose([base.alpha, base.beta, base.gamma, base.eps, base.eps_prime,
+                                base.mu], G[k + "_cfg"], rtol=1e-12)
+    g = cm.data_gradient(p.x0, acc, precision=prec)
+    ref = G[k + "_dgrad"]
+    assert np.abs(g - ref).max() <= 10 * TOL[prec]["pt"] * np.abs(ref).max()
+    for name, extra in CONFIGS.items():
+        tr_ref = G[f"{k}_{name}_trace"]
+        cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": len(tr_ref),
+                              "fixed_step": float(G[f"{k}_{name}_fixed_step"][0])})
+        for kk, vv in extra.items():
+            setattr(cfg, kk, vv)
+        trace = []
+        x = cm.m_step(acc, p.x0, p.x0, cfg, trace, precision=prec)
+        check_trace(trace, tr_ref, TOL[prec]["obj"])
+        assert rel_l2(x, G[f"{k}_{name}_x"]) <= TOL[prec]["vol"], name
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_penalized_objective_golden(prec):
+    n = 16
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    c = G["prob16_cfg"]
+    cfg = cm.RegConfig(alpha=c[0], beta=c[1], gamma=c[2], eps=c[3], eps_prime=c[4], mu=c[5])
+    xp = p.x0 + 0.05 * random_volume(n, 7)
+    o = cm.penalized_objective(xp, acc, cfg, p.x0, p.x0, precision=prec).as_array()
+    ref = G["prob16_obj"]
+    assert np.max(np.abs(o - ref) / np.maximum(np.abs(ref), 1.0)) <= TOL[prec]["obj"]
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_components_vs_oracle(O, prec):
+    n = 12
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (n, n, n))
+    w = rng.uniform(0.2, 3.0, (n, n, n))
+    tol = TOL[prec]["pt"] * 10
+    a, b = O.compute_weights(x, 0.01, 0.004)
+    got = cm.compute_weights(x, 0.01, 0.004, precision=prec)
+    np.testing.assert_allclose(got.w_l1, a, rtol=tol)
+    np.testing.assert_allclose(got.w_tv, b, rtol=tol)
+    for wt in (None, w):
+        g = cm.smoothed_tv_gradient(x, 0.2, wt, precision=prec)
+        ref = O.smoothed_tv_gradient(x, 0.2, wt)
+        assert np.abs(g - ref).max() <= tol * np.abs(ref).max()
+        v = cm.smoothed_tv_value(x, 0.2, wt, precision=prec)
+        assert abs(v - O.smoothed_tv_value(x, 0.2, wt)) <= tol * abs(v)
+    t = rng.uniform(0, 1, (n, n, n))
+    np.testing.assert_array_equal(cm.prox_l1(x, t, precision=prec), O.prox_l1(x, t))
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_unregularized_convergence_and_l1_kill(prec):
+    """test_regularizer.cpp:331-358."""
+    n = 6
+    w = synth.symmetric_weight(n, 21)
+    target = random_volume(n, 22)
+    acc = acc_of(w, w * synth.fft3_centered(target))
+    z = np.zeros((n, n, n))
+    x = cm.m_step(acc, z, z, cm.RegConfig(inner_iters=50), precision=prec)
+    assert np.abs(x - target).max() < (1e-6 if prec == 64 else 1e-5)
+    cfg = cm.RegConfig(alpha=1e12, beta=0.0, gamma=0.2, eps=0.05, eps_prime=0.02, mu=2e-4,
+                       inner_iters=3)
+    x = cm.m_step(acc, random_volume(n, 23), z, cfg, precision=prec)
+    assert np.all(x == 0.0)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_error_behaviour(prec):
+    n = 6
+    w = synth.symmetric_weight(n, 1)
+    y = w * synth.fft3_centered(random_volume(n, 2))
+    x = random_volume(n, 3)
+    with pytest.raises(cm.NonHermitianAccumulator):
+        cm.data_gradient(x, acc_of(w, y, finalized=False), precision=prec)
+    yb = y.copy()
+    yb[0, 0, 1] += 1.0
+    with pytest.raises(cm.NonHermitianAccumulator):
+        cm.m_step(acc_of(w, yb), x, x, cm.RegConfig(inner_iters=2), precision=prec)
+    with pytest.raises(cm.InvalidArgument):
+        cm.m_step(acc_of(w, y), x, x, cm.RegConfig(alpha=-1.0), precision=prec)
+    with pytest.raises(cm.GridMismatch):
+        cm.m_step(acc_of(w, y), np.zeros((8, 8, 8)), x, cm.RegConfig(), precision=prec)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_config1_64cubed_vs_oracle(O, prec):
+    """BASELINE config 1 at full size: 64^3, 100 iterations, one reweighting pass
+    (per_m_step), lipschitz audit on, against the oracle restatement."""
+    n = 64
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 100
+    cfg.refresh = cm.Refresh.per_m_step
+    trace = []
+    x = cm.m_step(acc, p.x0, p.x0, cfg, trace, precision=prec)
+    c = make_cfg(alpha=cfg.alpha, beta=cfg.beta, gamma=cfg.gamma, eps=cfg.eps,
+                 eps_prime=cfg.eps_prime, mu=cfg.mu, inner_iters=100, refresh=1)
+    rc, xo, tro = O.m_step(p.weight, p.numerator, p.x0, p.x0, c)
+    assert rc == 0
+    check_trace(trace, tro, TOL[prec]["obj"])
+    assert rel_l2(x, xo) <= TOL[prec]["vol"]
