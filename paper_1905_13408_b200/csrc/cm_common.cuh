@@ -51,7 +51,8 @@ struct DevState {
     int tol_kind;      // 0 none, 1 surrogate relative decrease, 2 relative step
     int fista;         // momentum on
     int refresh_inner; // per_inner weights (needs the previous iterate for after_{i-1})
-    int pad0;
+    int done_y;        // stop flag of the y-forward pass: raised by the z pass that
+                       // first sees `done`, so the last y-forward still runs
     double tol;
     double audit_slack; // relative slack of the monotone check (1e-9 in the reference)
     double step;        // l_r (constant within one m_step)

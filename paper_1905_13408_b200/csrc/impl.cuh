@@ -338,7 +338,7 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
     int launch_y(bool fwd, DevState* s) {
-        YParams<R> p{S, twN, s};
+        YParams<R> p{S, twN, s ? (fwd ? &s->done_y : &s->done) : nullptr};
         dim3 grid(Nh / G::TWY, N);
         if (fwd)
             ypass_kernel<R, N, true><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);

@@ -90,7 +90,7 @@ template <typename R> struct YParams {
     using C = Cx<R>;
     C* S;
     const C* twN;
-    DevState* st;
+    const int* stop; // &st->done (inverse pass) or &st->done_y (forward pass), or null
 };
 
 template <typename C>
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY)
 ypass_kernel(YParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
-    if (p.st && ld_done(p.st)) return;
+    if (p.stop && *((volatile const int*)p.stop)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
     C* buf = tw + N;
@@ -136,7 +136,11 @@ zpass_kernel(ZParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
     constexpr int TW = G::TW3, T = G::TY, E = G::EY, Nh = G::Nh;
-    if (p.st && ld_done(p.st)) return;
+    if (p.st && ld_done(p.st)) {
+        // the y-forward pass of the stopping iteration has run; stop the next one
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) p.st->done_y = 1;
+        return;
+    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
     C* buf0 = tw + N;             // [2][N][TW]

@@ -96,9 +96,11 @@ def test_m_step_traces_golden(n, prec):
     base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
     np.testing.assert_allclose([base.alpha, base.beta, base.gamma, base.eps, base.eps_prime,
                                 base.mu], G[k + "_cfg"], rtol=1e-12)
+    # x0 is the exact data-term minimiser (Y = W fft3_centered(x0)), so the
+    # reference gradient is pure roundoff: compare on the scale of x0
     g = cm.data_gradient(p.x0, acc, precision=prec)
     ref = G[k + "_dgrad"]
-    assert np.abs(g - ref).max() <= 10 * TOL[prec]["pt"] * np.abs(ref).max()
+    assert np.abs(g - ref).max() <= TOL[prec]["pt"] * np.abs(p.x0).max()
     for name, extra in CONFIGS.items():
         tr_ref = G[f"{k}_{name}_trace"]
         cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": len(tr_ref),
