@@ -22,6 +22,7 @@
 #include "../../include/cm_api.h"
 #include "finalize.cuh"
 #include "kernels.cuh"
+#include "sweep.cuh"
 
 namespace cm {
 
@@ -230,6 +231,8 @@ struct Impl final : ImplBase {
     R* x0keep = nullptr;
     R* anchor = nullptr;
     R* winit = nullptr;
+    R* wtvf = nullptr;         // per_m_step w_tv field (constant within a solve)
+    int sweep_grid = 0;        // persistent sweep CTAs
     C* S = nullptr;
     R* W = nullptr;
     R* Wn = nullptr;
@@ -258,7 +261,7 @@ struct Impl final : ImplBase {
     }
 
     ~Impl() override {
-        void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, S, W,
+        void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, S, W,
                       Wn, Yh, Yn, twN, stage, part1, part3, part_acc, maxes, st, trace_d,
                       theta_d};
         for (void* p : ps)
@@ -282,7 +285,18 @@ struct Impl final : ImplBase {
         CKS(dalloc(&Yn, NN));
         CKS(dalloc(&twN, N));
         CKS(dalloc(&stage, 3 * L));
-        CKS(dalloc(&part1, (size_t)NB1 * NP1));
+        {
+            using SG = SwGeo<R, N>;
+            CK(cudaFuncSetAttribute(sweep_kernel<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SG::SMEM));
+            int occ = 0, dev = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<R, N>, SG::NT,
+                                                             SG::SMEM));
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            sweep_grid = std::max(1, std::min(SG::NTILES, sms * std::max(occ, 1)));
+        }
+        CKS(dalloc(&part1, (size_t)std::max(NB1, sweep_grid) * NP1));
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
@@ -483,6 +497,19 @@ struct Impl final : ImplBase {
         if (need_winit)
             CK(cudaMemcpyAsync(winit, x0keep, sizeof(R) * L, cudaMemcpyDeviceToDevice, stream));
         const R* wfixed = (c->refresh == 1 && !convex) ? (anchor_is_init ? anchor : winit) : nullptr;
+        if (wfixed) {
+            // frozen weights (Refresh::per_m_step, regularizer.cpp:178-179): the
+            // w_tv field of x_init once per solve; w_l1 comes from x_init itself
+            if (!wtvf) CKS(dalloc(&wtvf, L));
+            XParams<R> wp = xp();
+            wp.xcur = wfixed;
+            wp.wsrc = wfixed;
+            wp.eps = c->eps;
+            wp.eps_prime = c->eps_prime;
+            wp.xnext = fista ? YF[1] : X[2];  // w_l1 scratch, overwritten by the solve
+            wp.ynext = wtvf;
+            CKS(launch_x<XM_WEIGHTS>(wp));
+        }
 
         DevState hs{};
         hs.iter = 0;
@@ -517,7 +544,10 @@ struct Impl final : ImplBase {
 
         auto sweep_and_finalize = [&](int g, cudaEvent_t mid) -> int {
             // K1
-            XParams<R> p = xp();
+            SweepParams<R> p{};
+            p.S = S;
+            p.twN = twN;
+            p.invL = 1.0 / (double)L;
             p.st = st;
             p.lr = lr;
             p.alpha = c->alpha;
@@ -542,14 +572,18 @@ struct Impl final : ImplBase {
                 p.xnext = X[(g + 1) % 3];
                 p.xprev = (audit && refresh_inner) ? X[(g + 2) % 3] : nullptr;
             }
-            p.wsrc = wfixed ? wfixed : p.xcur;
-            CKS(launch_x<XM_SWEEP>(p));
+            if (wfixed) {
+                p.wtvf = wtvf;
+                p.wl1src = wfixed;
+            }
+            sweep_kernel<R, N><<<sweep_grid, SwGeo<R, N>::NT, SwGeo<R, N>::SMEM, stream>>>(p);
+            CK(cudaGetLastError());
             if (mid) CK(cudaEventRecord(mid, stream));
             // FIN
             FinParams f{};
             f.st = st;
             f.part1 = need_part1 ? part1 : nullptr;
-            f.nb1 = NB1;
+            f.nb1 = sweep_grid;
             f.part3 = audit ? part3 : nullptr;
             f.nb3 = NB3;
             f.trace = want_trace ? trace_d : nullptr;

@@ -200,3 +200,85 @@ def test_config1_64cubed_vs_oracle(O, prec):
     assert rc == 0
     check_trace(trace, tro, TOL[prec]["obj"])
     assert rel_l2(x, xo) <= TOL[prec]["vol"]
+
+
+SWEEP_MODES = {
+    "per_inner": dict(),
+    "per_m_step_anchor_differs": dict(refresh=1),
+    "convex": dict(convex_mode=1),
+    "fixed": dict(step_rule=1),
+}
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("n", [12, 48, 96, 128])
+def test_sweep_tiles_and_modes_vs_oracle(O, n, prec):
+    """Tile geometries of the fused sweep (TJ x TK line tiles, i-chunks, idle
+    FFT groups) in every RegConfig mode, anchor != x_init, against the oracle."""
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    anchor = p.x0 + 0.01 * random_volume(n, 99)
+    lr0 = 1.0 / (2.0 * p.weight.max() + 2.0 * base.gamma + 12.0 * base.beta / base.eps_prime / base.mu)
+    for name, extra in SWEEP_MODES.items():
+        cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 8, "fixed_step": 2.0 * lr0, **extra})
+        trace = []
+        x = cm.m_step(acc, p.x0, anchor, cfg, trace, precision=prec)
+        c = make_cfg(alpha=cfg.alpha, beta=cfg.beta, gamma=cfg.gamma, eps=cfg.eps,
+                     eps_prime=cfg.eps_prime, mu=cfg.mu, inner_iters=8,
+                     step_rule=int(cfg.step_rule), fixed_step=cfg.fixed_step,
+                     refresh=int(cfg.refresh), convex_mode=int(cfg.convex_mode))
+        rc, xo, tro = O.m_step(p.weight, p.numerator, p.x0, anchor, c)
+        assert rc == 0
+        check_trace(trace, tro, TOL[prec]["obj"])
+        assert rel_l2(x, xo) <= TOL[prec]["vol"], name
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_fista_reaches_the_ista_fixed_point(prec):
+    """FISTA (opt-in) is judged on the converged volume against a long ISTA run
+    (frozen weights: a convex subproblem)."""
+    n = 16
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    # a better-conditioned instance (smaller TV weight) so ISTA converges in budget
+    base.beta *= 0.01
+    ista = cm.RegConfig(**{**base.__dict__, "inner_iters": 20000, "refresh": cm.Refresh.per_m_step,
+                           "step_rule": cm.StepRule.fixed})
+    lr = 1.0 / (2.0 * p.weight.max() + 2.0 * base.gamma + 12.0 * base.beta / base.eps_prime / base.mu)
+    ista.fixed_step = lr
+    xi = cm.m_step(acc, p.x0, p.x0, ista, precision=prec)
+    fista = cm.RegConfig(**{**ista.__dict__, "inner_iters": 3000, "momentum": 1})
+    st = {}
+    xf = cm.m_step(acc, p.x0, p.x0, fista, precision=prec, stats=st)
+    assert st["iterations"] == 3000
+    assert rel_l2(xf, xi) < 2e-4
+
+
+def test_tolerance_stop_matches_oracle_trace(O):
+    """tol_kind=1 stops at the first iteration whose frozen-weight surrogate
+    decrease falls below tol; the returned volume is that iterate."""
+    n = 16
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=64)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    c = make_cfg(alpha=base.alpha, beta=base.beta, gamma=base.gamma, eps=base.eps,
+                 eps_prime=base.eps_prime, mu=base.mu, inner_iters=400, refresh=1)
+    rc, xo, tro = O.m_step(p.weight, p.numerator, p.x0, p.x0, c)
+    sb = tro[:, 0] + tro[:, 1] + tro[:, 2] + tro[:, 4]
+    sa = tro[:, 7] + tro[:, 8] + tro[:, 9] + tro[:, 11]
+    rel = np.abs(sb - sa) / np.abs(sb)
+    tol = float(np.quantile(rel, 0.5))
+    want = int(np.argmax(rel < tol))  # first trace row whose decrease is below tol
+    cfg = cm.RegConfig(alpha=base.alpha, beta=base.beta, gamma=base.gamma, eps=base.eps,
+                       eps_prime=base.eps_prime, mu=base.mu, inner_iters=400,
+                       refresh=cm.Refresh.per_m_step, tol_kind=1, tol=tol)
+    st = {}
+    cm.m_step(acc, p.x0, p.x0, cfg, precision=64, stats=st)
+    assert st["stop_reason"] == 2
+    # row i compares x_i and x_{i+1}; the solve stops there and returns x_{i+1}
+    assert st["iterations"] == want + 1
