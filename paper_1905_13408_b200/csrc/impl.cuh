@@ -576,6 +576,7 @@ struct Impl final : ImplBase {
                 p.wtvf = wtvf;
                 p.wl1src = wfixed;
             }
+            if (const char* dbgs = std::getenv("CM_DBG_SWEEP")) p.dbg = std::atoi(dbgs);
             sweep_kernel<R, N><<<sweep_grid, SwGeo<R, N>::NT, SwGeo<R, N>::SMEM, stream>>>(p);
             CK(cudaGetLastError());
             if (mid) CK(cudaEventRecord(mid, stream));

@@ -17,9 +17,15 @@
 // +w_tv field in per_m_step); the halo re-reads hit L2.
 #pragma once
 
+#include <type_traits>
+
 #include "cm_common.cuh"
 #include "fft_engine.cuh"
 #include "kernels.cuh"
+
+#ifndef CM_SWEEP_TJ
+#define CM_SWEEP_TJ 4
+#endif
 
 namespace cm {
 
@@ -35,7 +41,7 @@ template <typename R, int N> struct SwGeo {
     static constexpr int Nh = N / 2;
     static constexpr int EX = elems_for(Nh);
     static constexpr int TX = Nh / EX;          // threads per line in the FFT phases
-    static constexpr int TJ = largest_divisor_le(N, 8);
+    static constexpr int TJ = largest_divisor_le(N, CM_SWEEP_TJ);
     static constexpr int TK = 2;
     static constexpr int LPC = TJ * TK;         // lines per tile
     static constexpr int NT0 = LPC * TX;
@@ -43,27 +49,78 @@ template <typename R, int N> struct SwGeo {
     static constexpr int NW = NT / 32;
     static constexpr int LPCB = NT / TX;        // line buffers (>= LPC; extra groups idle)
     static constexpr int CI = largest_divisor_le(N, 128);  // sweep chunk along x
-    static constexpr int PADX = Nh + (Nh >> 3) + 1;
-    static constexpr int XSW = CI + 2;                      // staged x row width
+    static constexpr int PADX = (Nh + (Nh >> 3) + 2) / 2 * 2;  // even: 16-byte aligned lines
+    // staged rows: element c (global i = i0 - 1 + c) at column c + 3, so the
+    // body [i0, i0+CI) starts 16-byte aligned at column 4
+    static constexpr bool VEC = (CI % 4 == 0) && (N % 4 == 0);
+    static constexpr int XSW = ((CI + 2 + 3) + 3) / 4 * 4;   // staged x row width
     static constexpr int XSR = (TK + 2) * (TJ + 2);         // staged x rows
-    static constexpr int XPW = CI + 1;
+    static constexpr int XPW = XSW;
     static constexpr int XPR = (TK + 1) * (TJ + 1);
-    static constexpr int SSW = CI + 1;
+    // fp32 with 128-voxel chunks: every lane owns 4 consecutive voxels (16-byte
+    // shared / global accesses); other sizes and fp64 take the scalar path
+    static constexpr bool V4 = (sizeof(R) == 4) && (CI == 128);
+    static constexpr int SSW = V4 ? CI + 4 : CI + 1;
+    static constexpr size_t FLOATS = ((size_t)XSR * XSW + (size_t)XPR * XPW +
+                                      (size_t)((TK + 1) * (TJ + 1)) * SSW + 3) / 4 * 4;
     static constexpr int SSR = (TK + 1) * (TJ + 1);
     static constexpr int NTILES = (N / TJ) * (N / TK);
     static constexpr size_t SMEM = sizeof(C) * (N + (size_t)LPCB * PADX) +
-                                   sizeof(R) * ((size_t)XSR * XSW + (size_t)XPR * XPW +
-                                                (size_t)SSR * SSW) +
-                                   sizeof(double) * 32 * NP1;
-    static constexpr int MINB = (SMEM * 2 <= 220 * 1024 && NT <= 512) ? 2 : 1;
+                                   sizeof(R) * FLOATS + sizeof(double) * 32 * NP1;
+    static constexpr int MINB = (SMEM * 3 <= 220 * 1024 && NT <= 256) ? 3 : ((SMEM * 2 <= 220 * 1024 && NT <= 512) ? 2 : 1);
 };
 
+// fp32 product mode: single-MUFU approximations (rel. error ~1 ulp; the parity
+// bar is 1e-5). fp64 parity mode: IEEE operations.
 template <typename R> __device__ __forceinline__ R rcp_(R v);
-template <> __device__ __forceinline__ float rcp_<float>(float v) { return __frcp_rn(v); }
+template <> __device__ __forceinline__ float rcp_<float>(float v) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
 template <> __device__ __forceinline__ double rcp_<double>(double v) { return 1.0 / v; }
+template <typename R> __device__ __forceinline__ R sqrt_(R v);
+template <> __device__ __forceinline__ float sqrt_<float>(float v) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+template <> __device__ __forceinline__ double sqrt_<double>(double v) { return sqrt(v); }
 template <typename R> __device__ __forceinline__ R log_(R v);
 template <> __device__ __forceinline__ float log_<float>(float v) { return __logf(v); }
 template <> __device__ __forceinline__ double log_<double>(double v) { return log(v); }
+
+// Stage rows (k0 + kk, j0 + jj), kk in [-1, NRK-2], jj in [-1, RW-2] (RW rows
+// per plane), global i in [i0 - 1, i0 + CI - (full ? 0 : 1)] into dst[row][c + 3]
+// (c = i - i0 + 1): the body [i0, i0 + CI) as 16-byte vectors, halos scalar.
+// Out-of-grid elements are 0 (never used: the replicate rule masks them).
+template <typename R, int N, int CI, int RW>
+__device__ __forceinline__ void stage_rows(R* dst, int nrows, const R* src, int k0, int j0,
+                                           int i0, bool full, int wid, int lane) {
+    constexpr int W = ((CI + 2 + 3) + 3) / 4 * 4;
+    const int nw = blockDim.x >> 5;
+    for (int r = wid; r < nrows; r += nw) {
+        const int kk = r / RW - 1, jj = r - (r / RW) * RW - 1;
+        const int gk = k0 + kk, gj = j0 + jj;
+        const bool rok = gk >= 0 && gk < N && gj >= 0 && gj < N;
+        const R* row = src + ((size_t)(rok ? gk : 0) * N + (rok ? gj : 0)) * N;
+        R* d = dst + r * W;
+        if constexpr ((CI % 4 == 0) && (N % 4 == 0)) {
+            using V = typename std::conditional<sizeof(R) == 4, float4, double2>::type;
+            constexpr int PER = 16 / sizeof(R);
+            for (int v = lane; v < CI / PER; v += 32) {
+                V val;
+                if (rok) val = __ldg(reinterpret_cast<const V*>(row + i0) + v);
+                else val = V{};
+                *reinterpret_cast<V*>(d + 4 + v * PER) = val;
+            }
+        } else {
+            for (int c = lane; c < CI; c += 32) d[4 + c] = rok ? __ldg(row + i0 + c) : R(0);
+        }
+        if (lane == 0) d[3] = (rok && i0 > 0) ? __ldg(row + i0 - 1) : R(0);
+        if (lane == 1 && full) d[4 + CI] = (rok && i0 + CI < N) ? __ldg(row + i0 + CI) : R(0);
+    }
+}
 
 template <typename R> struct SweepParams {
     using C = Cx<R>;
@@ -82,7 +139,213 @@ template <typename R> struct SweepParams {
     DevState* st;
     double lr, alpha, beta, gamma, eps, eps_prime, mu, invL;
     int convex, audit, fista;
+    int dbg;  // timing experiments only: bit0 skip C2R, bit1 skip R2C, bit2 skip staging,
+              // bit3 skip s box, bit4 skip voxel math (results are then wrong)
 };
+
+
+// ---- fp32 4-voxel paths (V4) ---------------------------------------------------------
+__device__ __forceinline__ float4 ld4(const float* q) { return *reinterpret_cast<const float4*>(q); }
+__device__ __forceinline__ void st4(float* q, float a, float b, float c, float d) {
+    *reinterpret_cast<float4*>(q) = make_float4(a, b, c, d);
+}
+
+// TV dual scale s = w_tv / max(mu, |Dx|) on the (TK+1) x (TJ+1) x (CI+1) box
+template <int N, int TJ>
+__device__ __forceinline__ void sbox_v4(float* SS, const float* XS, const float* wtvf, int convex,
+                                        int k0, int j0, int i0, float mu, float epsp, int wid,
+                                        int lane) {
+    constexpr int CI = 128, XSW = ((CI + 2 + 3) + 3) / 4 * 4, SSW = CI + 4;
+    constexpr int SSR = 3 * (TJ + 1);
+    const int nw = blockDim.x >> 5;
+    for (int r = wid; r < SSR; r += nw) {
+        const int kk = r / (TJ + 1), jj = r - kk * (TJ + 1);
+        const int gj = j0 + jj, gk = k0 + kk;
+        const bool rok = gj < N && gk < N;
+        const float* xr = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + 4;
+        float* srow = SS + r * SSW;
+        const float* wrow = (wtvf && rok) ? wtvf + ((size_t)gk * N + gj) * N + i0 : nullptr;
+        const int ii = 4 * lane;
+        float sv[4] = {0.f, 0.f, 0.f, 0.f};
+        if (rok) {
+            const float4 c4 = ld4(xr + ii), y4 = ld4(xr + ii - XSW),
+                         z4 = ld4(xr + ii - (TJ + 2) * XSW);
+            const float xm = xr[ii - 1];
+            const float xc[4] = {c4.x, c4.y, c4.z, c4.w}, xl[4] = {xm, c4.x, c4.y, c4.z};
+            const float xy[4] = {y4.x, y4.y, y4.z, y4.w}, xz[4] = {z4.x, z4.y, z4.z, z4.w};
+            float wt[4] = {1.f, 1.f, 1.f, 1.f};
+            if (wrow) {
+                const float4 w4 = __ldg(reinterpret_cast<const float4*>(wrow + ii));
+                wt[0] = w4.x; wt[1] = w4.y; wt[2] = w4.z; wt[3] = w4.w;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float d1 = (i0 + ii + c) > 0 ? xc[c] - xl[c] : 0.f;
+                const float d2 = gj > 0 ? xc[c] - xy[c] : 0.f;
+                const float d3 = gk > 0 ? xc[c] - xz[c] : 0.f;
+                const float gn = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                const float w = convex ? 1.f : (wrow ? wt[c] : rcp_(gn + epsp));
+                sv[c] = w * rcp_(mu > gn ? mu : gn);
+            }
+        }
+        st4(srow + ii, sv[0], sv[1], sv[2], sv[3]);
+        if (lane == 0) {  // forward halo ii = CI
+            const int gi = i0 + CI;
+            float s1 = 0.f;
+            if (rok && gi < N) {
+                const float* q = xr + CI;
+                const float xc = q[0];
+                const float d1 = xc - q[-1];
+                const float d2 = gj > 0 ? xc - q[-XSW] : 0.f;
+                const float d3 = gk > 0 ? xc - q[-(TJ + 2) * XSW] : 0.f;
+                const float gn = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                const float w = convex ? 1.f : (wtvf ? __ldg(wtvf + ((size_t)gk * N + gj) * N + gi)
+                                                     : rcp_(gn + epsp));
+                s1 = w * rcp_(mu > gn ? mu : gn);
+            }
+            srow[CI] = s1;
+        }
+    }
+}
+
+// one x-line of 128 voxels of the tile: update, prox, partials (4 voxels per lane)
+template <int N, int TJ>
+__device__ __forceinline__ void voxels_v4(const SweepParams<float>& p, float (&fa)[NP1],
+                                          const float* XS, const float* XP, const float* SS,
+                                          float* lbuf, int gk, int gj, int kk, int jj, int i0,
+                                          int lane, bool has_alpha, bool has_beta, float theta) {
+    constexpr int CI = 128, XSW = ((CI + 2 + 3) + 3) / 4 * 4, XPW = XSW, SSW = CI + 4;
+    const int ii = 4 * lane;
+    const int gi0 = i0 + ii;
+    const size_t gidx = ((size_t)gk * N + gj) * N + gi0;
+    const float eps = float(p.eps), epsp = float(p.eps_prime), mu = float(p.mu);
+    const float lr = float(p.lr), alpha = float(p.alpha), beta = float(p.beta);
+    const float gamma = float(p.gamma), invL = float(p.invL);
+    const float* xr = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + 4 + ii;
+    const float4 c4 = ld4(xr), ym4 = ld4(xr - XSW), zm4 = ld4(xr - (TJ + 2) * XSW);
+    const float xm = xr[-1], xq = xr[4];
+    const float xc[4] = {c4.x, c4.y, c4.z, c4.w};
+    const float xl[4] = {xm, c4.x, c4.y, c4.z}, xn[4] = {c4.y, c4.z, c4.w, xq};
+    const float ym[4] = {ym4.x, ym4.y, ym4.z, ym4.w}, zm[4] = {zm4.x, zm4.y, zm4.z, zm4.w};
+    const float4 g4 = ld4(lbuf + gi0);
+    const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
+    const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.anchor + gidx));
+    const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+    float tvg[4] = {0.f, 0.f, 0.f, 0.f};
+    float d1[4], d2[4], d3[4], gn[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        d1[c] = (gi0 + c) > 0 ? xc[c] - xl[c] : 0.f;
+        d2[c] = gj > 0 ? xc[c] - ym[c] : 0.f;
+        d3[c] = gk > 0 ? xc[c] - zm[c] : 0.f;
+        gn[c] = sqrt_(d1[c] * d1[c] + d2[c] * d2[c] + d3[c] * d3[c]);
+    }
+    if (has_beta) {
+        const float* sr = SS + (kk * (TJ + 1) + jj) * SSW + ii;
+        const float4 s4 = ld4(sr), sy4 = ld4(sr + SSW), sz4 = ld4(sr + (TJ + 1) * SSW);
+        const float sq = sr[4];
+        const float4 yp4 = ld4(xr + XSW), zp4 = ld4(xr + (TJ + 2) * XSW);
+        const float s0[4] = {s4.x, s4.y, s4.z, s4.w}, sx[4] = {s4.y, s4.z, s4.w, sq};
+        const float sy[4] = {sy4.x, sy4.y, sy4.z, sy4.w}, sz[4] = {sz4.x, sz4.y, sz4.z, sz4.w};
+        const float yp[4] = {yp4.x, yp4.y, yp4.z, yp4.w}, zp[4] = {zp4.x, zp4.y, zp4.z, zp4.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            float t = s0[c] * (d1[c] + d2[c] + d3[c]);
+            if (gi0 + c < N - 1) t -= sx[c] * (xn[c] - xc[c]);
+            if (gj < N - 1) t -= sy[c] * (yp[c] - xc[c]);
+            if (gk < N - 1) t -= sz[c] * (zp[c] - xc[c]);
+            tvg[c] = t;
+        }
+    }
+    float wl1[4] = {1.f, 1.f, 1.f, 1.f}, wtv[4] = {1.f, 1.f, 1.f, 1.f};
+    if (!p.convex) {
+        float ws[4] = {xc[0], xc[1], xc[2], xc[3]};
+        if (p.wl1src) {
+            if (p.wl1src == p.anchor) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ws[c] = av[c];
+            } else {
+                const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.wl1src + gidx));
+                ws[0] = w4.x; ws[1] = w4.y; ws[2] = w4.z; ws[3] = w4.w;
+            }
+        }
+        if (p.wtvf) {
+            const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.wtvf + gidx));
+            wtv[0] = w4.x; wtv[1] = w4.y; wtv[2] = w4.z; wtv[3] = w4.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) wtv[c] = rcp_(gn[c] + epsp);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) wl1[c] = rcp_(fabsf(ws[c]) + eps);
+    }
+    float base[4] = {xc[0], xc[1], xc[2], xc[3]};
+    if (p.fista) {
+        const float4 o4 = __ldg(reinterpret_cast<const float4*>(p.xold + gidx));
+        base[0] = o4.x; base[1] = o4.y; base[2] = o4.z; base[3] = o4.w;
+    }
+    float nx[4], spec[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        // update + prox (regularizer.cpp:193-205, 103-110)
+        float gs = 2.f * (gg[c] * invL) + 2.f * gamma * (xc[c] - av[c]);
+        if (has_beta) gs += beta * tvg[c];
+        float v = xc[c] - lr * gs;
+        if (has_alpha) {
+            const float th = lr * alpha * wl1[c];
+            v = fabsf(v) <= th ? 0.f : v - copysignf(th, v);
+        }
+        nx[c] = v;
+        spec[c] = p.fista ? v + theta * (v - base[c]) : v;
+        const float dx = v - base[c];
+        fa[9] += dx * dx;
+        fa[10] += v * v;
+    }
+    *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+    if (p.fista)
+        *reinterpret_cast<float4*>(p.ynext + gidx) = make_float4(spec[0], spec[1], spec[2], spec[3]);
+    st4(lbuf + gi0, spec[0], spec[1], spec[2], spec[3]);
+    if (p.audit) {
+        float pl1[4], ptv[4];
+        if (p.xprev) {
+            // backward stencil of x_{i-1} straight from global (L1/L2): no staging barrier
+            const float* pr = p.xprev + gidx;
+            const float4 p4 = __ldg(reinterpret_cast<const float4*>(pr));
+            const float4 py4 = gj > 0 ? __ldg(reinterpret_cast<const float4*>(pr - N)) : p4;
+            const float4 pz4 = gk > 0 ? __ldg(reinterpret_cast<const float4*>(pr - (size_t)N * N)) : p4;
+            const float pm = gi0 > 0 ? __ldg(pr - 1) : p4.x;
+            const float pc[4] = {p4.x, p4.y, p4.z, p4.w}, pl[4] = {pm, p4.x, p4.y, p4.z};
+            const float py[4] = {py4.x, py4.y, py4.z, py4.w}, pz[4] = {pz4.x, pz4.y, pz4.z, pz4.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float e1 = pc[c] - pl[c];
+                const float e2 = pc[c] - py[c];
+                const float e3 = pc[c] - pz[c];
+                pl1[c] = rcp_(fabsf(pc[c]) + eps);
+                ptv[c] = rcp_(sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp);
+            }
+        }
+        const float inv2mu = 0.5f * rcp_(mu);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float ax = fabsf(xc[c]);
+            const float g = gn[c];
+            const float hb = g < mu ? g * g * inv2mu : g - 0.5f * mu;
+            fa[0] += wl1[c] * ax;
+            fa[1] += wtv[c] * hb;
+            fa[2] += wtv[c] * g;
+            fa[3] += __logf(ax + eps);
+            fa[4] += __logf(g + epsp);
+            const float dd = xc[c] - av[c];
+            fa[5] += dd * dd;
+            if (p.xprev) {
+                fa[6] += pl1[c] * ax;
+                fa[7] += ptv[c] * hb;
+                fa[8] += ptv[c] * g;
+            }
+        }
+    }
+}
 
 template <typename R, int N>
 __global__ void __launch_bounds__(SwGeo<R, N>::NT, SwGeo<R, N>::MINB)
@@ -100,7 +363,7 @@ sweep_kernel(SweepParams<R> p) {
     R* XS = reinterpret_cast<R*>(lines + G::LPCB * PADX);     // [TK+2][TJ+2][CI+2]
     R* XP = XS + G::XSR * XSW;                                // [TK+1][TJ+1][CI+1]
     R* SS = XP + G::XPR * XPW;                                // [TK+1][TJ+1][CI+1]
-    double* red = reinterpret_cast<double*>(SS + G::SSR * SSW);
+    double* red = reinterpret_cast<double*>(XS + G::FLOATS);  // 16-byte aligned
     stage_table(tw, p.twN, N);
 
     const int tid = threadIdx.x;
@@ -134,7 +397,7 @@ sweep_kernel(SweepParams<R> p) {
         C* Srow = p.S + ((size_t)my_k * N + my_j) * Nh;
 
         // ---- 1. C2R: G rows -> g (unnormalised) in the line buffers ------------
-        {
+        if (!(p.dbg & 1)) {
             C v[E];
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = fft_active ? Srow[t + T * m] : cx<C>(R(0), R(0));
@@ -169,52 +432,42 @@ sweep_kernel(SweepParams<R> p) {
 
         // ---- 2. sweep in chunks along x -------------------------------------------
         for (int i0 = 0; i0 < N; i0 += CI) {
-            // stage x: rows (kk', jj') in [-1, TK] x [-1, TJ], columns [i0-1, i0+CI]
-            for (int r = wid; r < G::XSR; r += NW) {
-                const int kk = r / (TJ + 2) - 1, jj = r % (TJ + 2) - 1;
-                const int gk = k0 + kk, gj = j0 + jj;
-                const bool rok = gk >= 0 && gk < N && gj >= 0 && gj < N;
-                const R* src = p.xcur + ((size_t)(rok ? gk : 0) * N + (rok ? gj : 0)) * N;
-                for (int c = lane; c < XSW; c += 32) {
-                    const int gi = i0 - 1 + c;
-                    XS[r * XSW + c] = (rok && gi >= 0 && gi < N) ? __ldg(src + gi) : R(0);
-                }
-            }
-            if (p.xprev) {  // rows [-1, TK-1] x [-1, TJ-1], columns [i0-1, i0+CI-1]
-                for (int r = wid; r < G::XPR; r += NW) {
-                    const int kk = r / (TJ + 1) - 1, jj = r % (TJ + 1) - 1;
-                    const int gk = k0 + kk, gj = j0 + jj;
-                    const bool rok = gk >= 0 && gj >= 0;
-                    const R* src = p.xprev + ((size_t)(rok ? gk : 0) * N + (rok ? gj : 0)) * N;
-                    for (int c = lane; c < XPW; c += 32) {
-                        const int gi = i0 - 1 + c;
-                        XP[r * XPW + c] = (rok && gi >= 0) ? __ldg(src + gi) : R(0);
-                    }
-                }
-            }
+            // stage x: rows (kk', jj') in [-1, TK] x [-1, TJ], global i in [i0-1, i0+CI]
+            if (!(p.dbg & 4)) stage_rows<R, N, CI, TJ + 2>(XS, G::XSR, p.xcur, k0, j0, i0, true, wid, lane);
+            // x_prev: rows [-1, TK-1] x [-1, TJ-1], global i in [i0-1, i0+CI-1]
+            if (!G::V4 && p.xprev) stage_rows<R, N, CI, TJ + 1>(XP, G::XPR, p.xprev, k0, j0, i0, false, wid, lane);
             __syncthreads();
-            // s on the box (kk, jj, ii) in [0, TK] x [0, TJ] x [0, CI]
+            // s on the box (kk, jj, ii) in [0, TK] x [0, TJ] x [0, CI]: warp per row
+            if constexpr (G::V4) {
+                if (has_beta && !(p.dbg & 8)) sbox_v4<N, TJ>(SS, XS, p.wtvf, p.convex, k0, j0, i0, mu, epsp, wid, lane);
+            } else {
             if (has_beta) {
-                for (int q = tid; q < G::SSR * SSW; q += NT) {
-                    const int ii = q % SSW, r = q / SSW;
-                    const int kk = r / (TJ + 1), jj = r % (TJ + 1);
-                    const int gi = i0 + ii, gj = j0 + jj, gk = k0 + kk;
-                    R sv = R(0);
-                    if (gi < N && gj < N && gk < N) {
-                        const R* xr = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + (ii + 1);
-                        const R xc = xr[0];
-                        const R d1 = gi > 0 ? xc - xr[-1] : R(0);
-                        const R d2 = gj > 0 ? xc - xr[-XSW] : R(0);
-                        const R d3 = gk > 0 ? xc - xr[-(TJ + 2) * XSW] : R(0);
-                        const R gn = sqrt(d1 * d1 + d2 * d2 + d3 * d3);
-                        R wt = R(1);
-                        if (!p.convex)
-                            wt = p.wtvf ? __ldg(p.wtvf + ((size_t)gk * N + gj) * N + gi)
-                                        : rcp_(gn + epsp);
-                        sv = wt * rcp_(mu > gn ? mu : gn);
+                for (int r = wid; r < G::SSR; r += NW) {
+                    const int kk = r / (TJ + 1), jj = r - kk * (TJ + 1);
+                    const int gj = j0 + jj, gk = k0 + kk;
+                    const bool rok = gj < N && gk < N;
+                    const R* xrow = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + 4;
+                    const R* wrow = p.wtvf ? p.wtvf + ((size_t)(rok ? gk : 0) * N + (rok ? gj : 0)) * N
+                                           : nullptr;
+                    R* srow = SS + r * SSW;
+                    for (int ii = lane; ii <= CI; ii += 32) {
+                        const int gi = i0 + ii;
+                        R sv = R(0);
+                        if (rok && gi < N) {
+                            const R* xr = xrow + ii;
+                            const R xc = xr[0];
+                            const R d1 = gi > 0 ? xc - xr[-1] : R(0);
+                            const R d2 = gj > 0 ? xc - xr[-XSW] : R(0);
+                            const R d3 = gk > 0 ? xc - xr[-(TJ + 2) * XSW] : R(0);
+                            const R gn = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                            R wt = R(1);
+                            if (!p.convex) wt = wrow ? __ldg(wrow + gi) : rcp_(gn + epsp);
+                            sv = wt * rcp_(mu > gn ? mu : gn);
+                        }
+                        srow[ii] = sv;
                     }
-                    SS[q] = sv;
                 }
+            }
             }
             __syncthreads();
             // voxels: warp w -> lines w, w+NW, ...; lane -> x
@@ -223,6 +476,13 @@ sweep_kernel(SweepParams<R> p) {
             R fa[NP1];
 #pragma unroll
             for (int q = 0; q < NP1; ++q) fa[q] = R(0);
+            if constexpr (G::V4) {
+                if (!(p.dbg & 16))
+                for (int l = wid; l < LPC; l += NW)
+                    voxels_v4<N, TJ>(p, fa, XS, XP, SS, reinterpret_cast<float*>(lines + l * PADX),
+                                     k0 + l / TJ, j0 + l % TJ, l / TJ, l % TJ, i0, lane, has_alpha,
+                                     has_beta, theta);
+            } else {
             for (int l = wid; l < LPC; l += NW) {
                 const int kk = l / TJ, jj = l % TJ;
                 const int gk = k0 + kk, gj = j0 + jj;
@@ -231,12 +491,12 @@ sweep_kernel(SweepParams<R> p) {
                 for (int ii = lane; ii < CI; ii += 32) {
                     const int gi = i0 + ii;
                     const size_t gidx = rowoff + gi;
-                    const R* xr = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + (ii + 1);
+                    const R* xr = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + 4 + ii;
                     const R xc = xr[0];
                     const R d1 = gi > 0 ? xc - xr[-1] : R(0);
                     const R d2 = gj > 0 ? xc - xr[-XSW] : R(0);
                     const R d3 = gk > 0 ? xc - xr[-(TJ + 2) * XSW] : R(0);
-                    const R gn = sqrt(d1 * d1 + d2 * d2 + d3 * d3);
+                    const R gn = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                     const R av = __ldg(p.anchor + gidx);
                     R wl1 = R(1), wtv = R(1);
                     if (!p.convex) {
@@ -282,13 +542,13 @@ sweep_kernel(SweepParams<R> p) {
                         const R dd = xc - av;
                         fa[5] += R(dd * dd);
                         if (p.xprev) {
-                            const R* pr = XP + ((kk + 1) * (TJ + 1) + (jj + 1)) * XPW + (ii + 1);
+                            const R* pr = XP + ((kk + 1) * (TJ + 1) + (jj + 1)) * XPW + 4 + ii;
                             const R pc = pr[0];
                             const R e1 = gi > 0 ? pc - pr[-1] : R(0);
                             const R e2 = gj > 0 ? pc - pr[-XPW] : R(0);
                             const R e3 = gk > 0 ? pc - pr[-(TJ + 1) * XPW] : R(0);
                             const R pl1 = rcp_(fabs(pc) + eps);
-                            const R ptv = rcp_(sqrt(e1 * e1 + e2 * e2 + e3 * e3) + epsp);
+                            const R ptv = rcp_(sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp);
                             fa[6] += R(pl1 * ax);
                             fa[7] += R(ptv * hb);
                             fa[8] += R(ptv * gn);
@@ -299,13 +559,14 @@ sweep_kernel(SweepParams<R> p) {
                     fa[10] += R(nx * nx);
                 }
             }
+            }
 #pragma unroll
             for (int q = 0; q < NP1; ++q) acc[q] += (double)fa[q];
             __syncthreads();
         }
 
         // ---- 3. R2C of the new iterate (line buffers) -> spectrum rows -------------
-        {
+        if (!(p.dbg & 2)) {
             C v[E];
 #pragma unroll
             for (int m = 0; m < E; ++m) {

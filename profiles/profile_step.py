@@ -17,7 +17,12 @@ ctx.set_accumulator(cm.AccumulatorPair(n, p.numerator, p.weight, True))
 s = ctx.scale_data()
 cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
 cfg.inner_iters = iters
+if len(sys.argv) > 4:  # timing experiments: never stop on the audit
+    cfg.audit_slack = float(sys.argv[4])
 ctx.set_volumes(p.x0, p.x0)
 ctx.set_profiling(True)  # one launch per kernel (no graph) so ncu sees each
-st = ctx.solve(cfg)
-print("iterations", st.iterations, "solve_ms", st.solve_ms, "profile", ctx.get_profile())
+try:
+    st = ctx.solve(cfg)
+    print("iterations", st.iterations, "solve_ms", st.solve_ms, "profile", ctx.get_profile())
+except cm.Error as e:  # timing experiments may produce garbage iterates
+    print("error", type(e).__name__, "profile", ctx.get_profile())
