@@ -44,19 +44,25 @@ def _compile(src: Path, obj: Path, defs: list[str]) -> str:
     return obj.name
 
 
-def build(sides: list[int] | None = None, jobs: int | None = None, force: bool = False) -> Path:
+def build(sides: list[int] | None = None, jobs: int | None = None, force: bool = False,
+          out: Path | None = None, defines: list[str] | None = None) -> Path:
+    """out/defines: experimental variants (e.g. -DCM_SWEEP_TJ=8) built next to the
+    product library; the product build uses neither."""
     sides = sides or SIDES
+    lib = Path(out) if out else LIB
+    extra = [f"-D{d}" for d in (defines or [])]
+    obj_dir = OBJ if not out else OBJ.parent / ("obj_" + Path(out).stem)
     newest = max(p.stat().st_mtime for p in _sources())
-    if LIB.exists() and not force and LIB.stat().st_mtime > newest and sides == SIDES:
-        return LIB
-    units = [(CSRC / "cm_api.cu", OBJ / "cm_api.o", [])]
+    if lib.exists() and not force and lib.stat().st_mtime > newest and sides == SIDES and not out:
+        return lib
+    units = [(CSRC / "cm_api.cu", obj_dir / "cm_api.o", list(extra))]
     for n in SIDES:
-        defs = [f"-DCM_N={n}"]
+        defs = [f"-DCM_N={n}", *extra]
         src = CSRC / "inst.cu"
         if n not in sides:
             # stub factory: the side is compiled out of this (development) build
             defs.append("-DCM_STUB=1")
-        units.append((src, OBJ / f"inst_{n}{'_stub' if n not in sides else ''}.o", defs))
+        units.append((src, obj_dir / f"inst_{n}{'_stub' if n not in sides else ''}.o", defs))
     jobs = jobs or max(1, os.cpu_count() or 1)
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
         futs = [ex.submit(_compile, s, o, d) for s, o, d in units]
@@ -64,11 +70,11 @@ def build(sides: list[int] | None = None, jobs: int | None = None, force: bool =
             f.result()
     objs = [str(o) for _, o, _ in units]
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs,
-           "-o", str(LIB), "-lcudart"]
+           "-o", str(lib), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    return LIB
+    return lib
 
 
 def main(argv=None) -> None:
@@ -76,9 +82,12 @@ def main(argv=None) -> None:
     ap.add_argument("--sides", default="")
     ap.add_argument("-j", type=int, default=0)
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--out", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args(argv)
     sides = [int(s) for s in a.sides.split(",") if s] or None
-    lib = build(sides, a.j or None, force=a.force or bool(sides))
+    lib = build(sides, a.j or None, force=a.force or bool(sides), out=a.out or None,
+                defines=a.defines)
     print(lib)
 
 

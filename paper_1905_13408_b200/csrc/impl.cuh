@@ -23,6 +23,8 @@
 #include "finalize.cuh"
 #include "kernels.cuh"
 #include "sweep.cuh"
+#include "zpass.cuh"
+#include "tma.cuh"
 
 namespace cm {
 
@@ -222,7 +224,7 @@ struct Impl final : ImplBase {
     static constexpr size_t H = (size_t)N * N * Nh;
     static constexpr size_t NN = (size_t)N * N;
     static constexpr int NB1 = (int)((NN + G::LPC - 1) / G::LPC);
-    static constexpr int NB3 = (Nh / G::TW3) * (N / 2 + 1);
+    static constexpr int NB3 = ZGeo<R, N>::NBM + N / 2 + 1;
     static constexpr int LOOK = 8;
 
     R* X[3] = {};
@@ -232,12 +234,15 @@ struct Impl final : ImplBase {
     R* anchor = nullptr;
     R* winit = nullptr;
     R* wtvf = nullptr;         // per_m_step w_tv field (constant within a solve)
+    CUtensorMap tm_x[5] = {};  // TMA maps of X[0..2], YF[0..1] (fp32 V4 sweep)
+    CUtensorMap tm_g = {};     // TMA map of the packed spectrum rows
     int sweep_grid = 0;        // persistent sweep CTAs
     C* S = nullptr;
     R* W = nullptr;
     R* Wn = nullptr;
     C* Yh = nullptr;
     C* Yn = nullptr;
+    C* Z0 = nullptr;           // forward-transformed packed column 0 [N][N]
     C* twN = nullptr;
     double* stage = nullptr;   // fp64 staging (3L doubles)
     double* part1 = nullptr;
@@ -262,7 +267,7 @@ struct Impl final : ImplBase {
 
     ~Impl() override {
         void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, S, W,
-                      Wn, Yh, Yn, twN, stage, part1, part3, part_acc, maxes, st, trace_d,
+                      Wn, Yh, Yn, Z0, twN, stage, part1, part3, part_acc, maxes, st, trace_d,
                       theta_d};
         for (void* p : ps)
             if (p) cudaFree(p);
@@ -271,6 +276,46 @@ struct Impl final : ImplBase {
     }
 
     long long bytes() const override { return alloc_bytes; }
+
+    // 3D box map over a real volume: box {XSW, TJ+2, TK+2}, zero OOB fill
+    int make_map_x(R* ptr, CUtensorMap* out) {
+        using SG = SwGeo<R, N>;
+        if constexpr (!SG::V4) {
+            return CM_OK;
+        } else {
+            EncodeTiledFn enc = encode_tiled_fn();
+            if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+            const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
+            const cuuint64_t strides[2] = {(cuuint64_t)N * sizeof(R), (cuuint64_t)N * N * sizeof(R)};
+            const cuuint32_t box[3] = {(cuuint32_t)SG::XSW, (cuuint32_t)(SG::TJ + 2),
+                                       (cuuint32_t)(SG::TK + 2)};
+            const cuuint32_t es[3] = {1, 1, 1};
+            CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map (x) encode failed");
+            return CM_OK;
+        }
+    }
+    // 2D map over the packed spectrum rows (8-byte complex elements): box {GW, TJ}
+    int make_map_g() {
+        using SG = SwGeo<R, N>;
+        if constexpr (!SG::V4) {
+            return CM_OK;
+        } else {
+            EncodeTiledFn enc = encode_tiled_fn();
+            if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+            const cuuint64_t dims[2] = {(cuuint64_t)Nh, (cuuint64_t)N * N};
+            const cuuint64_t strides[1] = {(cuuint64_t)Nh * sizeof(C)};
+            const cuuint32_t box[2] = {(cuuint32_t)SG::GW, (cuuint32_t)SG::TJ};
+            const cuuint32_t es[2] = {1, 1};
+            CUresult r = enc(&tm_g, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, S, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map (spectrum) encode failed");
+            return CM_OK;
+        }
+    }
 
     int init() override {
         n = N;
@@ -283,6 +328,7 @@ struct Impl final : ImplBase {
         CKS(dalloc(&Wn, NN));
         CKS(dalloc(&Yh, H));
         CKS(dalloc(&Yn, NN));
+        CKS(dalloc(&Z0, NN));
         CKS(dalloc(&twN, N));
         CKS(dalloc(&stage, 3 * L));
         {
@@ -297,6 +343,8 @@ struct Impl final : ImplBase {
             sweep_grid = std::max(1, std::min(SG::NTILES, sms * std::max(occ, 1)));
         }
         CKS(dalloc(&part1, (size_t)std::max(NB1, sweep_grid) * NP1));
+        for (int q = 0; q < 3; ++q) CKS(make_map_x(X[q], &tm_x[q]));
+        CKS(make_map_g());
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
@@ -327,12 +375,17 @@ struct Impl final : ImplBase {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(ypass_kernel<R, N, false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(zpass_kernel<R, N, ZM_FULL>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(zpass_kernel<R, N, ZM_FIT>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(zpass_kernel<R, N, ZM_FWD>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZSmem<R, N>::bytes));
+        using ZG = ZGeo<R, N>;
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FULL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FWD>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
+        CK(cudaFuncSetAttribute(zcol0_kernel<R, N, ZM_FULL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_COL0));
+        CK(cudaFuncSetAttribute(zcol0_kernel<R, N, ZM_FIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_COL0));
         CK(cudaStreamSynchronize(stream));
         return CM_OK;
     }
@@ -361,12 +414,18 @@ struct Impl final : ImplBase {
         CK(cudaGetLastError());
         return CM_OK;
     }
+    // K3: z pass (main tiles, then the packed column 0 with its Friedel mates)
     template <int MODE>
     int launch_z(double* part, DevState* s) {
-        ZParams<R> p{S, W, Wn, Yh, Yn, twN, part, s};
-        dim3 grid(Nh / G::TW3, N / 2 + 1);
-        zpass_kernel<R, N, MODE><<<grid, 2 * G::TW3 * G::TY, ZSmem<R, N>::bytes, stream>>>(p);
+        using ZG = ZGeo<R, N>;
+        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, part, s};
+        dim3 grid(Nh / ZG::TW, N);
+        zmain_kernel<R, N, MODE><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
         CK(cudaGetLastError());
+        if constexpr (MODE != ZM_FWD) {
+            zcol0_kernel<R, N, MODE><<<N / 2 + 1, ZG::NT0, ZG::SMEM_COL0, stream>>>(p);
+            CK(cudaGetLastError());
+        }
         return CM_OK;
     }
     int upload_real(const double* host, R* dst) {
@@ -460,8 +519,11 @@ struct Impl final : ImplBase {
         if (fista) {
             for (auto& p : XF)
                 if (!p) CKS(dalloc(&p, L));
-            for (auto& p : YF)
-                if (!p) CKS(dalloc(&p, L));
+            for (int q = 0; q < 2; ++q)
+                if (!YF[q]) {
+                    CKS(dalloc(&YF[q], L));
+                    CKS(make_map_x(YF[q], &tm_x[3 + q]));
+                }
         }
         const bool need_winit = (c->refresh == 1) && !convex && !anchor_is_init;
         if (need_winit && !winit) CKS(dalloc(&winit, L));
@@ -561,23 +623,26 @@ struct Impl final : ImplBase {
             p.fista = fista;
             p.anchor = anchor;
             p.part = need_part1 ? part1 : nullptr;
+            const CUtensorMap* tmx = nullptr;
             if (fista) {
                 p.xcur = YF[g % 2];
                 p.xold = XF[g % 2];
                 p.xnext = XF[(g + 1) % 2];
                 p.ynext = YF[(g + 1) % 2];
                 p.theta = theta_d;
+                tmx = &tm_x[3 + g % 2];
             } else {
                 p.xcur = X[g % 3];
                 p.xnext = X[(g + 1) % 3];
                 p.xprev = (audit && refresh_inner) ? X[(g + 2) % 3] : nullptr;
+                tmx = &tm_x[g % 3];
             }
             if (wfixed) {
                 p.wtvf = wtvf;
                 p.wl1src = wfixed;
             }
             if (const char* dbgs = std::getenv("CM_DBG_SWEEP")) p.dbg = std::atoi(dbgs);
-            sweep_kernel<R, N><<<sweep_grid, SwGeo<R, N>::NT, SwGeo<R, N>::SMEM, stream>>>(p);
+            sweep_kernel<R, N><<<sweep_grid, SwGeo<R, N>::NT, SwGeo<R, N>::SMEM, stream>>>(p, *tmx, tm_g);
             CK(cudaGetLastError());
             if (mid) CK(cudaEventRecord(mid, stream));
             // FIN
@@ -631,7 +696,7 @@ struct Impl final : ImplBase {
                     prof_ms[q] += m;
                 }
                 ++prof_iters;
-                launches += 5;
+                launches += 6;
             }
             for (auto& e : pe) cudaEventDestroy(e);
         } else if (use_graph) {
@@ -652,7 +717,7 @@ struct Impl final : ImplBase {
                     if (flags_h[q % LOOK]) break;
                 }
                 CK(cudaGraphLaunch(exec, stream));
-                launches += 5 * chunk;
+                launches += 6 * chunk;
                 CK(cudaMemcpyAsync(&flags_h[q % LOOK], &st->done, sizeof(int),
                                    cudaMemcpyDeviceToHost, stream));
                 CK(cudaEventRecord(ev[q % LOOK], stream));
@@ -664,7 +729,7 @@ struct Impl final : ImplBase {
         } else {
             for (int g = 0; g < K; ++g) {
                 CKS(iteration(g % 6));
-                launches += 5;
+                launches += 6;
             }
         }
 

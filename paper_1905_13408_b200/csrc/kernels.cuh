@@ -126,111 +126,6 @@ ypass_kernel(YParams<R> p) {
 }
 
 // ==================================================================================
-// z pass: FFT along k for every (b, h) column, fused Fourier-weight multiply and
-// fit partials. A block owns the row pair (b, -b) of one h tile so that the
-// packed column 0 can be unpacked with its Friedel mate. grid = (Nh/TW3, N/2+1)
-// ==================================================================================
-template <typename R, int N, int MODE>
-__global__ void __launch_bounds__(2 * Geo<R, N>::TW3 * Geo<R, N>::TY)
-zpass_kernel(ZParams<R> p) {
-    using G = Geo<R, N>;
-    using C = Cx<R>;
-    constexpr int TW = G::TW3, T = G::TY, E = G::EY, Nh = G::Nh;
-    if (p.st && ld_done(p.st)) {
-        // the y-forward pass of the stopping iteration has run; stop the next one
-        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) p.st->done_y = 1;
-        return;
-    }
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C* tw = reinterpret_cast<C*>(smem_raw);
-    C* buf0 = tw + N;             // [2][N][TW]
-    C* z0 = buf0 + 2 * N * TW;    // [2][N] column-0 values for the mate unpack
-    double* red = reinterpret_cast<double*>(z0 + 2 * N);
-    stage_table(tw, p.twN, N);
-
-    const int col = threadIdx.x % TW;
-    const int t = (threadIdx.x / TW) % T;
-    const int r = threadIdx.x / (TW * T);
-    const int bp = blockIdx.y;
-    const int b = r == 0 ? bp : (N - bp) % N;
-    const bool active = (r == 0) || (b != bp);
-    const int h = blockIdx.x * TW + col;
-    const size_t plane = (size_t)N * Nh;
-    C* base = p.S + (size_t)b * Nh + h;
-    C* buf = buf0 + r * N * TW;
-
-    C v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m)
-        v[m] = active ? base[(size_t)(t + T * m) * plane] : cx<C>(R(0), R(0));
-    __syncthreads();
-    fft_regs<N, E, N, true>(v, t, buf, ColAddr{TW, col}, tw, BlockSync{});
-
-    if constexpr (MODE == ZM_FWD) {
-        if (active)
-#pragma unroll
-            for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
-        return;
-    }
-
-    // column 0: publish both rows so each can read its Friedel mate Z(-b,-c)
-    const bool col0 = (blockIdx.x == 0) && (col == 0);
-    if (col0)
-#pragma unroll
-        for (int m = 0; m < E; ++m) z0[r * N + t + T * m] = v[m];
-    __syncthreads();
-
-    double quad = 0.0, cross = 0.0;
-    if (active) {
-        const int rm = (b == bp && bp == (N - bp) % N) ? r : 1 - r; // self-paired rows
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int c = t + T * m;
-            const size_t gi = ((size_t)c * N + b) * Nh + h;
-            if (!col0) {
-                const R w = p.W[gi];
-                const C y = p.Yh[gi];
-                const C f = v[m];
-                quad += 2.0 * (double)w * ((double)f.x * f.x + (double)f.y * f.y);
-                cross += 2.0 * ((double)y.x * f.x + (double)y.y * f.y);
-                v[m] = cx<C>(w * f.x - y.x, w * f.y - y.y);
-            } else {
-                const C zm = z0[rm * N + (N - c) % N];
-                const C zz = v[m];
-                // F0 = (Z + conj Zm)/2, FN = (Z - conj Zm)/(2i)
-                const C f0 = cx<C>(R(0.5) * (zz.x + zm.x), R(0.5) * (zz.y - zm.y));
-                const C fn = cx<C>(R(0.5) * (zz.y + zm.y), R(-0.5) * (zz.x - zm.x));
-                const size_t ni = (size_t)c * N + b;
-                const R w0 = p.W[gi], wn = p.Wn[ni];
-                const C y0 = p.Yh[gi], yn = p.Yn[ni];
-                quad += (double)w0 * ((double)f0.x * f0.x + (double)f0.y * f0.y) +
-                        (double)wn * ((double)fn.x * fn.x + (double)fn.y * fn.y);
-                cross += ((double)y0.x * f0.x + (double)y0.y * f0.y) +
-                         ((double)yn.x * fn.x + (double)yn.y * fn.y);
-                const C g0 = cx<C>(w0 * f0.x - y0.x, w0 * f0.y - y0.y);
-                const C gn = cx<C>(wn * fn.x - yn.x, wn * fn.y - yn.y);
-                v[m] = cx<C>(g0.x - gn.y, g0.y + gn.x); // g0 + i gn
-            }
-        }
-    }
-    if (p.part) {
-        double acc[2] = {quad, cross};
-        block_sum<2>(acc, red);
-        if (threadIdx.x == 0) {
-            const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-            p.part[bid * NP3 + 0] = acc[0];
-            p.part[bid * NP3 + 1] = acc[1];
-        }
-    }
-    if constexpr (MODE == ZM_FIT) return;
-    __syncthreads();
-    fft_regs<N, E, N, false>(v, t, buf, ColAddr{TW, col}, tw, BlockSync{});
-    if (active)
-#pragma unroll
-        for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
-}
-
-// ==================================================================================
 // x lines: C2R -> data gradient; fused stencil sweep; R2C of the new iterate.
 // ==================================================================================
 template <typename R> struct Vox {
@@ -492,10 +387,6 @@ template <typename R, int N> struct XSmem {
 };
 template <typename R, int N> struct YSmem {
     static constexpr size_t bytes = sizeof(Cx<R>) * (N + (size_t)N * Geo<R, N>::TWY);
-};
-template <typename R, int N> struct ZSmem {
-    static constexpr size_t bytes =
-        sizeof(Cx<R>) * (N + 2 * (size_t)N * Geo<R, N>::TW3 + 2 * N) + sizeof(double) * 32 * NP3;
 };
 
 } // namespace cm

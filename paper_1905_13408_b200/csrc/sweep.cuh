@@ -22,6 +22,7 @@
 #include "cm_common.cuh"
 #include "fft_engine.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 #ifndef CM_SWEEP_TJ
 #define CM_SWEEP_TJ 4
@@ -49,25 +50,39 @@ template <typename R, int N> struct SwGeo {
     static constexpr int NW = NT / 32;
     static constexpr int LPCB = NT / TX;        // line buffers (>= LPC; extra groups idle)
     static constexpr int CI = largest_divisor_le(N, 128);  // sweep chunk along x
+    static constexpr int NCH = N / CI;
     static constexpr int PADX = (Nh + (Nh >> 3) + 2) / 2 * 2;  // even: 16-byte aligned lines
     // staged rows: element c (global i = i0 - 1 + c) at column c + 3, so the
     // body [i0, i0+CI) starts 16-byte aligned at column 4
-    static constexpr bool VEC = (CI % 4 == 0) && (N % 4 == 0);
     static constexpr int XSW = ((CI + 2 + 3) + 3) / 4 * 4;   // staged x row width
     static constexpr int XSR = (TK + 2) * (TJ + 2);         // staged x rows
     static constexpr int XPW = XSW;
     static constexpr int XPR = (TK + 1) * (TJ + 1);
     // fp32 with 128-voxel chunks: every lane owns 4 consecutive voxels (16-byte
-    // shared / global accesses); other sizes and fp64 take the scalar path
+    // shared / global accesses) and the x halo boxes arrive by TMA, double
+    // buffered; other sizes and fp64 take the synchronous scalar path
     static constexpr bool V4 = (sizeof(R) == 4) && (CI == 128);
     static constexpr int SSW = V4 ? CI + 4 : CI + 1;
-    static constexpr size_t FLOATS = ((size_t)XSR * XSW + (size_t)XPR * XPW +
-                                      (size_t)((TK + 1) * (TJ + 1)) * SSW + 3) / 4 * 4;
     static constexpr int SSR = (TK + 1) * (TJ + 1);
     static constexpr int NTILES = (N / TJ) * (N / TK);
-    static constexpr size_t SMEM = sizeof(C) * (N + (size_t)LPCB * PADX) +
-                                   sizeof(R) * FLOATS + sizeof(double) * 32 * NP1;
-    static constexpr int MINB = (SMEM * 3 <= 220 * 1024 && NT <= 256) ? 3 : ((SMEM * 2 <= 220 * 1024 && NT <= 512) ? 2 : 1);
+    // TMA boxes
+    static constexpr int GW = Nh < 256 ? Nh : 256;          // spectrum row box width
+    static constexpr int NHB = Nh / GW;
+    static constexpr uint32_t XBOX_BYTES = (uint32_t)(XSW * (TJ + 2) * (TK + 2) * sizeof(R));
+    static constexpr uint32_t GBYTES = (uint32_t)(LPC * Nh * sizeof(C));
+    // shared memory layout (bytes)
+    static constexpr size_t al(size_t v, size_t a) { return (v + a - 1) / a * a; }
+    static constexpr size_t OFF_LINES = al(sizeof(C) * N, 128);
+    static constexpr size_t OFF_XS = al(OFF_LINES + sizeof(C) * (size_t)LPCB * PADX, 128);
+    static constexpr size_t XS_BYTES = sizeof(R) * (size_t)XSR * XSW;
+    static constexpr size_t OFF_XP = al(OFF_XS + (V4 ? 2 : 1) * XS_BYTES, 128);
+    static constexpr size_t OFF_SS = al(OFF_XP + (V4 ? 0 : sizeof(R) * (size_t)XPR * XPW), 128);
+    static constexpr size_t OFF_G = al(OFF_SS + sizeof(R) * (size_t)SSR * SSW, 128);
+    static constexpr size_t OFF_RED = al(OFF_G + (V4 ? (size_t)GBYTES : 0), 128);
+    static constexpr size_t OFF_BAR = al(OFF_RED + sizeof(double) * 32 * NP1, 16);
+    static constexpr size_t SMEM = OFF_BAR + 4 * sizeof(uint64_t);
+    static constexpr int MINB = (SMEM * 3 <= 220 * 1024 && NT <= 256) ? 3
+                                : ((SMEM * 2 <= 220 * 1024 && NT <= 512) ? 2 : 1);
 };
 
 // fp32 product mode: single-MUFU approximations (rel. error ~1 ulp; the parity
@@ -221,6 +236,18 @@ __device__ __forceinline__ void voxels_v4(const SweepParams<float>& p, float (&f
     const float eps = float(p.eps), epsp = float(p.eps_prime), mu = float(p.mu);
     const float lr = float(p.lr), alpha = float(p.alpha), beta = float(p.beta);
     const float gamma = float(p.gamma), invL = float(p.invL);
+    const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.anchor + gidx));
+    // global loads first (before any store) so their latency overlaps the math:
+    // backward stencil of x_{i-1} (L1/L2) for the weights of after_{i-1}
+    float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f), py4 = p4, pz4 = p4;
+    float pm = 0.f;
+    if (p.audit && p.xprev) {
+        const float* pr = p.xprev + gidx;
+        p4 = __ldg(reinterpret_cast<const float4*>(pr));
+        py4 = gj > 0 ? __ldg(reinterpret_cast<const float4*>(pr - N)) : p4;
+        pz4 = gk > 0 ? __ldg(reinterpret_cast<const float4*>(pr - (size_t)N * N)) : p4;
+        pm = gi0 > 0 ? __ldg(pr - 1) : p4.x;
+    }
     const float* xr = XS + ((kk + 1) * (TJ + 2) + (jj + 1)) * XSW + 4 + ii;
     const float4 c4 = ld4(xr), ym4 = ld4(xr - XSW), zm4 = ld4(xr - (TJ + 2) * XSW);
     const float xm = xr[-1], xq = xr[4];
@@ -229,7 +256,6 @@ __device__ __forceinline__ void voxels_v4(const SweepParams<float>& p, float (&f
     const float ym[4] = {ym4.x, ym4.y, ym4.z, ym4.w}, zm[4] = {zm4.x, zm4.y, zm4.z, zm4.w};
     const float4 g4 = ld4(lbuf + gi0);
     const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
-    const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.anchor + gidx));
     const float av[4] = {a4.x, a4.y, a4.z, a4.w};
     float tvg[4] = {0.f, 0.f, 0.f, 0.f};
     float d1[4], d2[4], d3[4], gn[4];
@@ -308,12 +334,6 @@ __device__ __forceinline__ void voxels_v4(const SweepParams<float>& p, float (&f
     if (p.audit) {
         float pl1[4], ptv[4];
         if (p.xprev) {
-            // backward stencil of x_{i-1} straight from global (L1/L2): no staging barrier
-            const float* pr = p.xprev + gidx;
-            const float4 p4 = __ldg(reinterpret_cast<const float4*>(pr));
-            const float4 py4 = gj > 0 ? __ldg(reinterpret_cast<const float4*>(pr - N)) : p4;
-            const float4 pz4 = gk > 0 ? __ldg(reinterpret_cast<const float4*>(pr - (size_t)N * N)) : p4;
-            const float pm = gi0 > 0 ? __ldg(pr - 1) : p4.x;
             const float pc[4] = {p4.x, p4.y, p4.z, p4.w}, pl[4] = {pm, p4.x, p4.y, p4.z};
             const float py[4] = {py4.x, py4.y, py4.z, py4.w}, pz[4] = {pz4.x, pz4.y, pz4.z, pz4.w};
 #pragma unroll
@@ -349,7 +369,8 @@ __device__ __forceinline__ void voxels_v4(const SweepParams<float>& p, float (&f
 
 template <typename R, int N>
 __global__ void __launch_bounds__(SwGeo<R, N>::NT, SwGeo<R, N>::MINB)
-sweep_kernel(SweepParams<R> p) {
+sweep_kernel(SweepParams<R> p, const __grid_constant__ CUtensorMap tmx,
+             const __grid_constant__ CUtensorMap tmg) {
     using G = SwGeo<R, N>;
     using C = Cx<R>;
     constexpr int Nh = G::Nh, E = G::EX, T = G::TX, TJ = G::TJ, TK = G::TK, LPC = G::LPC;
@@ -357,13 +378,15 @@ sweep_kernel(SweepParams<R> p) {
     constexpr int XSW = G::XSW, XPW = G::XPW, SSW = G::SSW;
     if (p.st && ld_done(p.st)) return;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
-    C* lines = tw + N;                                        // [LPCB][PADX]
-    R* XS = reinterpret_cast<R*>(lines + G::LPCB * PADX);     // [TK+2][TJ+2][CI+2]
-    R* XP = XS + G::XSR * XSW;                                // [TK+1][TJ+1][CI+1]
-    R* SS = XP + G::XPR * XPW;                                // [TK+1][TJ+1][CI+1]
-    double* red = reinterpret_cast<double*>(XS + G::FLOATS);  // 16-byte aligned
+    C* lines = reinterpret_cast<C*>(smem_raw + G::OFF_LINES);   // [LPCB][PADX]
+    R* XS0 = reinterpret_cast<R*>(smem_raw + G::OFF_XS);        // [2][TK+2][TJ+2][XSW]
+    R* XP = reinterpret_cast<R*>(smem_raw + G::OFF_XP);         // [TK+1][TJ+1][XPW]
+    R* SS = reinterpret_cast<R*>(smem_raw + G::OFF_SS);         // [TK+1][TJ+1][SSW]
+    C* Gs = reinterpret_cast<C*>(smem_raw + G::OFF_G);          // TMA-staged spectrum rows
+    double* red = reinterpret_cast<double*>(smem_raw + G::OFF_RED);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + G::OFF_BAR);  // x box [2], rows
     stage_table(tw, p.twN, N);
 
     const int tid = threadIdx.x;
@@ -387,9 +410,39 @@ sweep_kernel(SweepParams<R> p) {
     double acc[NP1];
 #pragma unroll
     for (int q = 0; q < NP1; ++q) acc[q] = 0.0;
+
+    // TMA issue helpers (one elected thread); step = (tile, chunk) of this CTA
+    auto issue_x = [&](int tile_, int chunk_, int b) {
+        const int tj0 = (tile_ % (N / TJ)) * TJ, tk0 = (tile_ / (N / TJ)) * TK;
+        mbar_expect_tx(&bar[b], G::XBOX_BYTES);
+        tma_load_3d(reinterpret_cast<unsigned char*>(XS0) + b * G::XS_BYTES, &tmx,
+                    chunk_ * CI - 4, tj0 - 1, tk0 - 1, &bar[b]);
+    };
+    auto issue_g = [&](int tile_) {
+        const int tj0 = (tile_ % (N / TJ)) * TJ, tk0 = (tile_ / (N / TJ)) * TK;
+        mbar_expect_tx(&bar[2], G::GBYTES);
+        for (int kk = 0; kk < TK; ++kk)
+            for (int hb = 0; hb < G::NHB; ++hb)
+                tma_load_2d(Gs + (kk * G::NHB + hb) * TJ * G::GW, &tmg, hb * G::GW,
+                            (tk0 + kk) * N + tj0, &bar[2]);
+    };
+    if constexpr (G::V4) {
+        if (tid == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            mbar_init(&bar[2], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+        if (tid == 0 && blockIdx.x < G::NTILES) {
+            issue_g(blockIdx.x);
+            issue_x(blockIdx.x, 0, 0);
+        }
+    }
     __syncthreads();
 
-    for (int tile = blockIdx.x; tile < G::NTILES; tile += gridDim.x) {
+    int q_tile = 0;
+    for (int tile = blockIdx.x; tile < G::NTILES; tile += gridDim.x, ++q_tile) {
         const int j0 = (tile % (N / TJ)) * TJ;
         const int k0 = (tile / (N / TJ)) * TK;
         // line lg of the tile: (kk, jj) = (lg / TJ, lg % TJ)
@@ -399,8 +452,20 @@ sweep_kernel(SweepParams<R> p) {
         // ---- 1. C2R: G rows -> g (unnormalised) in the line buffers ------------
         if (!(p.dbg & 1)) {
             C v[E];
+            if constexpr (G::V4) {
+                mbar_wait(&bar[2], q_tile & 1);
+                const int kk = lg / TJ, jj = lg % TJ;
 #pragma unroll
-            for (int m = 0; m < E; ++m) v[m] = fft_active ? Srow[t + T * m] : cx<C>(R(0), R(0));
+                for (int m = 0; m < E; ++m) {
+                    const int hh = t + T * m;
+                    v[m] = fft_active
+                               ? Gs[((kk * G::NHB + hh / G::GW) * TJ + jj) * G::GW + hh % G::GW]
+                               : cx<C>(R(0), R(0));
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = fft_active ? Srow[t + T * m] : cx<C>(R(0), R(0));
+            }
 #pragma unroll
             for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
             __syncwarp();
@@ -429,13 +494,36 @@ sweep_kernel(SweepParams<R> p) {
             }
         }
         __syncthreads();
+        if constexpr (G::V4) {  // the staged rows are consumed: prefetch the next tile's
+            if (tid == 0 && tile + (int)gridDim.x < G::NTILES) issue_g(tile + gridDim.x);
+        }
 
         // ---- 2. sweep in chunks along x -------------------------------------------
-        for (int i0 = 0; i0 < N; i0 += CI) {
-            // stage x: rows (kk', jj') in [-1, TK] x [-1, TJ], global i in [i0-1, i0+CI]
-            if (!(p.dbg & 4)) stage_rows<R, N, CI, TJ + 2>(XS, G::XSR, p.xcur, k0, j0, i0, true, wid, lane);
+        // per-tile partials in R (fp32 in product mode: N/32 * LPC/NW terms per
+        // thread), folded into the fp64 totals once per tile
+        R fa[NP1];
+#pragma unroll
+        for (int q = 0; q < NP1; ++q) fa[q] = R(0);
+        for (int ci = 0; ci < G::NCH; ++ci) {
+            const int i0 = ci * CI;
+            const int step = q_tile * G::NCH + ci;
+            R* XS = XS0 + (G::V4 ? (step & 1) * G::XSR * XSW : 0);
+            if constexpr (G::V4) {
+                // prefetch the next step's box into the other buffer (its readers
+                // passed the barrier that ended the previous step), then wait
+                if (tid == 0) {
+                    if (ci + 1 < G::NCH) issue_x(tile, ci + 1, (step + 1) & 1);
+                    else if (tile + (int)gridDim.x < G::NTILES)
+                        issue_x(tile + gridDim.x, 0, (step + 1) & 1);
+                }
+                mbar_wait(&bar[step & 1], (step >> 1) & 1);
+            } else {
+                // stage x: rows (kk', jj') in [-1, TK] x [-1, TJ], global i in [i0-1, i0+CI]
+                stage_rows<R, N, CI, TJ + 2>(XS, G::XSR, p.xcur, k0, j0, i0, true, wid, lane);
+            }
             // x_prev: rows [-1, TK-1] x [-1, TJ-1], global i in [i0-1, i0+CI-1]
-            if (!G::V4 && p.xprev) stage_rows<R, N, CI, TJ + 1>(XP, G::XPR, p.xprev, k0, j0, i0, false, wid, lane);
+            if (!G::V4 && p.xprev)
+                stage_rows<R, N, CI, TJ + 1>(XP, G::XPR, p.xprev, k0, j0, i0, false, wid, lane);
             __syncthreads();
             // s on the box (kk, jj, ii) in [0, TK] x [0, TJ] x [0, CI]: warp per row
             if constexpr (G::V4) {
@@ -471,11 +559,6 @@ sweep_kernel(SweepParams<R> p) {
             }
             __syncthreads();
             // voxels: warp w -> lines w, w+NW, ...; lane -> x
-            // per-chunk partials in R (fp32 in product mode: <= CI/32 * LPC/NW
-            // terms per thread), folded into fp64 totals after every chunk
-            R fa[NP1];
-#pragma unroll
-            for (int q = 0; q < NP1; ++q) fa[q] = R(0);
             if constexpr (G::V4) {
                 if (!(p.dbg & 16))
                 for (int l = wid; l < LPC; l += NW)
@@ -560,10 +643,10 @@ sweep_kernel(SweepParams<R> p) {
                 }
             }
             }
-#pragma unroll
-            for (int q = 0; q < NP1; ++q) acc[q] += (double)fa[q];
             __syncthreads();
         }
+#pragma unroll
+        for (int q = 0; q < NP1; ++q) acc[q] += (double)fa[q];
 
         // ---- 3. R2C of the new iterate (line buffers) -> spectrum rows -------------
         if (!(p.dbg & 2)) {
