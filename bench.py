@@ -175,19 +175,25 @@ def load_problem(n: int, rank: int, world: int):
 
 
 # ---- algorithmic bytes per launch ------------------------------
+KERNELS = ("z_pass", "y_inverse", "x_c2r", "stencil", "finalize", "x_r2c", "y_forward")
+
+
 def kernel_bytes(n: int, rsize: int, audit_prev: bool):
-    """Algorithmic HBM bytes per launch of each per-iteration kernel, packed
-    half spectrum (H' = n^2 * n/2 complex) and real volumes of L = n^3."""
+    """Algorithmic HBM bytes per launch of each per-iteration kernel. Packed half
+    spectrum: H' = n^2 * n/2 complex (+ the n^2 Nyquist planes of W and Yh);
+    real volumes: L = n^3."""
     L = n ** 3
-    c = 2 * rsize            # complex element
+    c = 2 * rsize
     Hp = n * n * (n // 2)
     nyq = n * n
     return {
-        "K3_zpass": Hp * c * 2 + (Hp + nyq) * rsize + (Hp + nyq) * c,  # S rw, W, Yh
-        "K4_yinv": Hp * c * 2,
-        "K1_xline": Hp * c * 2 + L * rsize * (4 if audit_prev else 3),  # S rw, x, anchor, x_next (+x_prev)
-        "FIN": 0,
-        "K2_yfwd": Hp * c * 2,
+        "z_pass": Hp * c * 2 + (Hp + nyq) * rsize + (Hp + nyq) * c,  # S r/w, W, Yh
+        "y_inverse": Hp * c * 2,
+        "x_c2r": Hp * c + L * rsize,                                  # S in, g out
+        "stencil": L * rsize * (5 if audit_prev else 4),              # g, x, anchor, (x_prev) in; x out
+        "finalize": 0,
+        "x_r2c": L * rsize + Hp * c,
+        "y_forward": Hp * c * 2,
     }
 
 
@@ -311,7 +317,7 @@ def run_ours(args):
     ctx.solve(pcfg)
     ms5, it = ctx.get_profile()
     ctx.set_profiling(False)
-    names = ["K3_zpass", "K4_yinv", "K1_xline", "FIN", "K2_yfwd"]
+    names = list(KERNELS)
     avg = {k: ms5[q] / it for q, k in enumerate(names)}
     rsize = 4 if args.precision == 32 else 8
     kb = kernel_bytes(n, rsize, audit_prev=True)

@@ -117,9 +117,10 @@ int cm_get_volume(cm_ctx* ctx, double* x_out);
 
 /* Diagnostics: when on, cm_solve launches every kernel individually between
  * CUDA events on the context stream (no graph) and accumulates per-kernel
- * device time: ms5 = {K3 z-pass, K4 y-inverse, K1 x-line sweep, FIN, K2 y-forward}. */
+ * device time, ms7 = {z pass (tile + column-0 kernels), y inverse, x C2R,
+ * stencil sweep, finalize, x R2C, y forward}. */
 int cm_set_profiling(cm_ctx* ctx, int on);
-int cm_get_profile(const cm_ctx* ctx, double* ms5, int* iters);
+int cm_get_profile(const cm_ctx* ctx, double* ms7, int* iters);
 
 /* m_step (regularizer.hpp:98-100) in one call: upload, solve, download. */
 int cm_m_step(cm_ctx* ctx, const double* weight, const double* numerator, int finalized,

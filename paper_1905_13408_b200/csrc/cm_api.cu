@@ -175,9 +175,9 @@ int cm_set_profiling(cm_ctx* ctx, int on) {
     return CM_OK;
 }
 
-int cm_get_profile(const cm_ctx* ctx, double* ms5, int* iters) {
+int cm_get_profile(const cm_ctx* ctx, double* ms7, int* iters) {
     if (!ctx || !ctx->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
-    for (int q = 0; q < 5; ++q) ms5[q] = ctx->impl->prof_ms[q];
+    for (int q = 0; q < 7; ++q) ms7[q] = ctx->impl->prof_ms[q];
     if (iters) *iters = ctx->impl->prof_iters;
     return CM_OK;
 }

@@ -22,7 +22,8 @@
 #include "../../include/cm_api.h"
 #include "finalize.cuh"
 #include "kernels.cuh"
-#include "sweep.cuh"
+#include "stencil.cuh"
+#include "xfft.cuh"
 #include "zpass.cuh"
 #include "tma.cuh"
 
@@ -208,7 +209,7 @@ struct ImplBase {
     bool acc_set = false, acc_finalized = false, vol_set = false, anchor_is_init = false;
     double residue = 0.0, max_weight = 0.0, s_y = 0.0, s_n = 0.0;
     int profiling = 0;      // per-kernel CUDA-event timing (no graph)
-    double prof_ms[5] = {}; // K3 K4 K1 FIN K2 accumulated device ms
+    double prof_ms[8] = {}; // zmain+zcol0, y-inv, x-C2R, stencil, FIN, x-R2C, y-fwd (ms)
     int prof_iters = 0;
     int last_iter = 0;      // iterations behind the resident result
     int last_fista = 0;
@@ -234,9 +235,13 @@ struct Impl final : ImplBase {
     R* anchor = nullptr;
     R* winit = nullptr;
     R* wtvf = nullptr;         // per_m_step w_tv field (constant within a solve)
-    CUtensorMap tm_x[5] = {};  // TMA maps of X[0..2], YF[0..1] (fp32 V4 sweep)
-    CUtensorMap tm_g = {};     // TMA map of the packed spectrum rows
-    int sweep_grid = 0;        // persistent sweep CTAs
+    R* gbuf = nullptr;         // data gradient in real space (x-line C2R output)
+    CUtensorMap tm_x[5] = {};  // TMA x-box maps of X[0..2], YF[0..1] (fp32 stencil)
+    CUtensorMap tm_p[3] = {};  // x_prev boxes of X[0..2]
+    CUtensorMap tm_gt = {};    // g tiles
+    CUtensorMap tm_at = {};    // anchor tiles
+    int sweep_grid = 0;        // persistent stencil CTAs
+    int xfft_grid = 0;         // persistent x-line transform CTAs
     C* S = nullptr;
     R* W = nullptr;
     R* Wn = nullptr;
@@ -266,7 +271,7 @@ struct Impl final : ImplBase {
     }
 
     ~Impl() override {
-        void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, S, W,
+        void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, gbuf, S, W,
                       Wn, Yh, Yn, Z0, twN, stage, part1, part3, part_acc, maxes, st, trace_d,
                       theta_d};
         for (void* p : ps)
@@ -277,42 +282,26 @@ struct Impl final : ImplBase {
 
     long long bytes() const override { return alloc_bytes; }
 
-    // 3D box map over a real volume: box {XSW, TJ+2, TK+2}, zero OOB fill
-    int make_map_x(R* ptr, CUtensorMap* out) {
-        using SG = SwGeo<R, N>;
+    // 3D box map over a real volume, zero OOB fill. kind 0: x box {XSW, TJ+2, TK+2};
+    // 1: x_prev box {XSW, TJ+1, TK+1}; 2: interior tile {CI, TJ, TK}
+    int make_map_x(R* ptr, CUtensorMap* out, int kind = 0) {
+        using SG = StGeo<R, N>;
         if constexpr (!SG::V4) {
             return CM_OK;
         } else {
+            const cuuint32_t bw = kind == 2 ? (cuuint32_t)SG::CI : (cuuint32_t)SG::XSW;
+            const cuuint32_t bj = (cuuint32_t)(SG::TJ + (kind == 0 ? 2 : (kind == 1 ? 1 : 0)));
+            const cuuint32_t bk = (cuuint32_t)(SG::TK + (kind == 0 ? 2 : (kind == 1 ? 1 : 0)));
             EncodeTiledFn enc = encode_tiled_fn();
             if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
             const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
             const cuuint64_t strides[2] = {(cuuint64_t)N * sizeof(R), (cuuint64_t)N * N * sizeof(R)};
-            const cuuint32_t box[3] = {(cuuint32_t)SG::XSW, (cuuint32_t)(SG::TJ + 2),
-                                       (cuuint32_t)(SG::TK + 2)};
+            const cuuint32_t box[3] = {bw, bj, bk};
             const cuuint32_t es[3] = {1, 1, 1};
             CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map (x) encode failed");
-            return CM_OK;
-        }
-    }
-    // 2D map over the packed spectrum rows (8-byte complex elements): box {GW, TJ}
-    int make_map_g() {
-        using SG = SwGeo<R, N>;
-        if constexpr (!SG::V4) {
-            return CM_OK;
-        } else {
-            EncodeTiledFn enc = encode_tiled_fn();
-            if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-            const cuuint64_t dims[2] = {(cuuint64_t)Nh, (cuuint64_t)N * N};
-            const cuuint64_t strides[1] = {(cuuint64_t)Nh * sizeof(C)};
-            const cuuint32_t box[2] = {(cuuint32_t)SG::GW, (cuuint32_t)SG::TJ};
-            const cuuint32_t es[2] = {1, 1};
-            CUresult r = enc(&tm_g, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, S, dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map (spectrum) encode failed");
             return CM_OK;
         }
     }
@@ -332,19 +321,32 @@ struct Impl final : ImplBase {
         CKS(dalloc(&twN, N));
         CKS(dalloc(&stage, 3 * L));
         {
-            using SG = SwGeo<R, N>;
-            CK(cudaFuncSetAttribute(sweep_kernel<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            using SG = StGeo<R, N>;
+            CK(cudaFuncSetAttribute(stencil_kernel<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SG::SMEM));
             int occ = 0, dev = 0, sms = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel<R, N>, SG::NT,
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_kernel<R, N>, SG::NT,
                                                              SG::SMEM));
             CK(cudaGetDevice(&dev));
             CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             sweep_grid = std::max(1, std::min(SG::NTILES, sms * std::max(occ, 1)));
+            CK(cudaFuncSetAttribute(xfft_kernel<R, N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)XGeo<R, N>::SMEM));
+            CK(cudaFuncSetAttribute(xfft_kernel<R, N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)XGeo<R, N>::SMEM));
+            int occx = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, xfft_kernel<R, N, 0>,
+                                                             XGeo<R, N>::NT, XGeo<R, N>::SMEM));
+            xfft_grid = sms * std::max(occx, 1);
         }
+        CKS(dalloc(&gbuf, L));
         CKS(dalloc(&part1, (size_t)std::max(NB1, sweep_grid) * NP1));
-        for (int q = 0; q < 3; ++q) CKS(make_map_x(X[q], &tm_x[q]));
-        CKS(make_map_g());
+        for (int q = 0; q < 3; ++q) {
+            CKS(make_map_x(X[q], &tm_x[q], 0));
+            CKS(make_map_x(X[q], &tm_p[q], 1));
+        }
+        CKS(make_map_x(gbuf, &tm_gt, 2));
+        CKS(make_map_x(anchor, &tm_at, 2));
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
@@ -359,13 +361,7 @@ struct Impl final : ImplBase {
             tw[q].y = R(std::sin(a));
         }
         CK(cudaMemcpyAsync(twN, tw.data(), sizeof(C) * N, cudaMemcpyHostToDevice, stream));
-        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_INIT>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_SWEEP>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_OBJ>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_DGRAD>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_TVGRAD>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
@@ -414,6 +410,19 @@ struct Impl final : ImplBase {
         CK(cudaGetLastError());
         return CM_OK;
     }
+    // x-line transforms: dir 0 C2R (S -> g * invL), dir 1 R2C (real -> S)
+    int launch_xfft(int dir, R* real, const int* stop) {
+        using XG = XGeo<R, N>;
+        XfParams<R> p{S, real, twN, stop, 1.0 / (double)L};
+        const int grid = std::min(XG::NB, xfft_grid);
+        if (dir == 0)
+            xfft_kernel<R, N, 0><<<grid, XG::NT, XG::SMEM, stream>>>(p);
+        else
+            xfft_kernel<R, N, 1><<<grid, XG::NT, XG::SMEM, stream>>>(p);
+        CK(cudaGetLastError());
+        return CM_OK;
+    }
+
     // K3: z pass (main tiles, then the packed column 0 with its Friedel mates)
     template <int MODE>
     int launch_z(double* part, DevState* s) {
@@ -596,20 +605,25 @@ struct Impl final : ImplBase {
         int launches = 0;
 
         // spectrum of the starting point: x R2C, y forward
-        {
-            XParams<R> p = xp();
-            p.xcur = fista ? YF[0] : X[0];
-            CKS(launch_x<XM_INIT>(p));
-            CKS(launch_y(true, nullptr));
-            launches += 2;
-        }
+        CKS(launch_xfft(1, fista ? YF[0] : X[0], nullptr));
+        CKS(launch_y(true, nullptr));
+        launches += 2;
 
+        cudaEvent_t pev[8] = {};
+        if (profiling)
+            for (auto& e : pev) CK(cudaEventCreate(&e));
+        auto mark = [&](int q) -> int {
+            if (profiling) CK(cudaEventRecord(pev[q], stream));
+            return CM_OK;
+        };
         auto sweep_and_finalize = [&](int g, cudaEvent_t mid) -> int {
-            // K1
-            SweepParams<R> p{};
-            p.S = S;
-            p.twN = twN;
-            p.invL = 1.0 / (double)L;
+            (void)mid;
+            // K1a: x-line C2R -> data gradient (real space, / L)
+            CKS(launch_xfft(0, gbuf, &st->done));
+            CKS(mark(3));
+            // K1b: stencil sweep
+            StencilParams<R> p{};
+            p.g = gbuf;
             p.st = st;
             p.lr = lr;
             p.alpha = c->alpha;
@@ -621,9 +635,13 @@ struct Impl final : ImplBase {
             p.convex = convex;
             p.audit = audit;
             p.fista = fista;
+            p.trace_full = want_trace;
+            p.steptol = hs.tol_kind == 2;
             p.anchor = anchor;
             p.part = need_part1 ? part1 : nullptr;
             const CUtensorMap* tmx = nullptr;
+            const CUtensorMap* tmp = nullptr;
+            R* spec_src = nullptr;
             if (fista) {
                 p.xcur = YF[g % 2];
                 p.xold = XF[g % 2];
@@ -631,20 +649,24 @@ struct Impl final : ImplBase {
                 p.ynext = YF[(g + 1) % 2];
                 p.theta = theta_d;
                 tmx = &tm_x[3 + g % 2];
+                tmp = tmx;
+                spec_src = YF[(g + 1) % 2];
             } else {
                 p.xcur = X[g % 3];
                 p.xnext = X[(g + 1) % 3];
                 p.xprev = (audit && refresh_inner) ? X[(g + 2) % 3] : nullptr;
                 tmx = &tm_x[g % 3];
+                tmp = &tm_p[(g + 2) % 3];
+                spec_src = X[(g + 1) % 3];
             }
             if (wfixed) {
                 p.wtvf = wtvf;
                 p.wl1src = wfixed;
             }
-            if (const char* dbgs = std::getenv("CM_DBG_SWEEP")) p.dbg = std::atoi(dbgs);
-            sweep_kernel<R, N><<<sweep_grid, SwGeo<R, N>::NT, SwGeo<R, N>::SMEM, stream>>>(p, *tmx, tm_g);
+            stencil_kernel<R, N><<<sweep_grid, StGeo<R, N>::NT, StGeo<R, N>::SMEM, stream>>>(
+                p, *tmx, *tmp, tm_gt, tm_at);
             CK(cudaGetLastError());
-            if (mid) CK(cudaEventRecord(mid, stream));
+            CKS(mark(4));
             // FIN
             FinParams f{};
             f.st = st;
@@ -660,6 +682,10 @@ struct Impl final : ImplBase {
             f.epilogue = 0;
             finalize_kernel<<<1, 256, 0, stream>>>(f);
             CK(cudaGetLastError());
+            CKS(mark(5));
+            // K1c: x-line R2C of the new iterate (FISTA: of y_{k+1})
+            CKS(launch_xfft(1, spec_src, &st->done_y));
+            CKS(mark(6));
             return CM_OK;
         };
         auto iteration = [&](int g) -> int {
@@ -675,30 +701,27 @@ struct Impl final : ImplBase {
         const int nchunks = (K + chunk - 1) / chunk;
         if (profiling) {
             // per-kernel timing: same kernels, launched one by one between events
-            cudaEvent_t pe[6];
-            for (auto& e : pe) CK(cudaEventCreate(&e));
-            for (int q = 0; q < 5; ++q) prof_ms[q] = 0.0;
+            for (int q = 0; q < 8; ++q) prof_ms[q] = 0.0;
             prof_iters = 0;
             for (int g = 0; g < K; ++g) {
-                CK(cudaEventRecord(pe[0], stream));
+                CKS(mark(0));
                 CKS(launch_z<ZM_FULL>(audit ? part3 : nullptr, st));
-                CK(cudaEventRecord(pe[1], stream));
+                CKS(mark(1));
                 CKS(launch_y(false, st));
-                CK(cudaEventRecord(pe[2], stream));
-                CKS(sweep_and_finalize(g, pe[3]));
-                CK(cudaEventRecord(pe[4], stream));
+                CKS(mark(2));
+                CKS(sweep_and_finalize(g, nullptr));
                 CKS(launch_y(true, st));
-                CK(cudaEventRecord(pe[5], stream));
-                CK(cudaEventSynchronize(pe[5]));
-                for (int q = 0; q < 5; ++q) {
+                CKS(mark(7));
+                CK(cudaEventSynchronize(pev[7]));
+                for (int q = 0; q < 7; ++q) {
                     float m = 0.f;
-                    CK(cudaEventElapsedTime(&m, pe[q], pe[q + 1]));
+                    CK(cudaEventElapsedTime(&m, pev[q], pev[q + 1]));
                     prof_ms[q] += m;
                 }
                 ++prof_iters;
-                launches += 6;
+                launches += 8;
             }
-            for (auto& e : pe) cudaEventDestroy(e);
+            for (auto& e : pev) cudaEventDestroy(e);
         } else if (use_graph) {
             cudaGraph_t graph;
             cudaGraphExec_t exec;
@@ -717,7 +740,7 @@ struct Impl final : ImplBase {
                     if (flags_h[q % LOOK]) break;
                 }
                 CK(cudaGraphLaunch(exec, stream));
-                launches += 6 * chunk;
+                launches += 8 * chunk;
                 CK(cudaMemcpyAsync(&flags_h[q % LOOK], &st->done, sizeof(int),
                                    cudaMemcpyDeviceToHost, stream));
                 CK(cudaEventRecord(ev[q % LOOK], stream));
@@ -729,7 +752,7 @@ struct Impl final : ImplBase {
         } else {
             for (int g = 0; g < K; ++g) {
                 CKS(iteration(g % 6));
-                launches += 6;
+                launches += 8;
             }
         }
 
@@ -811,10 +834,8 @@ struct Impl final : ImplBase {
     }
 
     // ---- component entry points ---------------------------------------------------------
-    int spectrum_of(const R* x) { // S <- x R2C, y forward, z forward (packed full spectrum)
-        XParams<R> p = xp();
-        p.xcur = x;
-        CKS(launch_x<XM_INIT>(p));
+    int spectrum_of(R* x) { // S <- x R2C, y forward (the z pass follows)
+        CKS(launch_xfft(1, x, nullptr));
         CKS(launch_y(true, nullptr));
         return CM_OK;
     }
@@ -825,9 +846,7 @@ struct Impl final : ImplBase {
         CKS(spectrum_of(X[0]));
         CKS(launch_z<ZM_FULL>(nullptr, nullptr));
         CKS(launch_y(false, nullptr));
-        XParams<R> p = xp();
-        p.xnext = X[1];
-        CKS(launch_x<XM_DGRAD>(p));
+        CKS(launch_xfft(0, X[1], nullptr));
         result_valid = false; // X[] reused as scratch; x0keep / anchor untouched
         return download_real(X[1], out);
     }

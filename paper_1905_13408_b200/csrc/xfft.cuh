@@ -1,0 +1,124 @@
+// x-line real transforms (sm_100a): C2R of the packed half spectrum into the
+// data gradient g = Re ifft3(...) / L, and R2C of a real volume into the packed
+// half spectrum. One group of TX threads per line (warp-synchronous), lines
+// loaded straight into registers (t + TX*m order: coalesced), registers out.
+//
+// A real line of N samples is transformed as N/2 complex samples
+// z(p) = x(2p) + i x(2p+1); the split / merge with the mate h <-> N/2 - h uses
+// one shared-memory exchange. The x-Nyquist value X(N/2) is packed into the
+// imaginary part of column 0 (kernels.cuh layout).
+#pragma once
+
+#include "cm_common.cuh"
+#include "fft_engine.cuh"
+#include "kernels.cuh"
+
+namespace cm {
+
+template <typename R, int N> struct XGeo {
+    static constexpr int Nh = N / 2;
+    static constexpr int E = elems_for(Nh);
+    static constexpr int T = Nh / E;
+    static constexpr int LPC = (256 / T) < 1 ? 1 : (256 / T);  // lines per CTA
+    static constexpr int NT = LPC * T < 32 ? 32 : LPC * T;
+    static constexpr int LPCB = NT / T;
+    static constexpr int PADX = (Nh + (Nh >> 3) + 2) / 2 * 2;
+    static constexpr size_t SMEM = sizeof(Cx<R>) * (N + (size_t)LPCB * PADX);
+    static constexpr int NB = (N * N + LPC - 1) / LPC;
+};
+
+template <typename R> struct XfParams {
+    using C = Cx<R>;
+    C* S;
+    R* real;            // C2R: g out (scaled by `scale`); R2C: volume in
+    const C* twN;
+    const int* stop;    // &st->done (C2R) / &st->done_y (R2C) or null
+    double scale;
+};
+
+// DIR 0: C2R (S -> real * scale), DIR 1: R2C (real -> S)
+template <typename R, int N, int DIR>
+__global__ void __launch_bounds__(XGeo<R, N>::NT) xfft_kernel(XfParams<R> p) {
+    using X = XGeo<R, N>;
+    using C = Cx<R>;
+    constexpr int Nh = X::Nh, E = X::E, T = X::T;
+    if (p.stop && *((volatile const int*)p.stop)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* tw = reinterpret_cast<C*>(smem_raw);
+    C* lines = tw + N;
+    stage_table(tw, p.twN, N);
+    __syncthreads();
+    const int lg = threadIdx.x / T, t = threadIdx.x % T;
+    C* buf = lines + lg * X::PADX;
+    const PadAddr pad{};
+    const WarpSync wsync{};
+    // persistent: the twiddle table is staged once per CTA
+    for (int grp = blockIdx.x; grp < X::NB; grp += gridDim.x) {
+    const int line = grp * X::LPC + lg;
+    const bool valid = (lg < X::LPC) && (line < N * N);
+    C* Srow = p.S + (size_t)(valid ? line : 0) * Nh;
+    R* xrow = p.real + (size_t)(valid ? line : 0) * N;
+    C v[E];
+    if constexpr (DIR == 0) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = valid ? Srow[t + T * m] : cx<C>(R(0), R(0));
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int hh = t + T * m;
+            const C q = v[m];
+            if (hh == 0) {
+                v[m] = cx<C>(q.x + q.y, q.x - q.y);
+            } else {
+                const C qm = buf[pad(Nh - hh)];
+                const C a = cx<C>(q.x + qm.x, q.y - qm.y);   // Q + conj(Qm)
+                const C d = cx<C>(q.x - qm.x, q.y + qm.y);   // Q - conj(Qm)
+                const C bb = cmulc(d, tw[hh]);               // * exp(+2 pi i h / N)
+                v[m] = cx<C>(a.x - bb.y, a.y + bb.x);        // A + i B
+            }
+        }
+        __syncwarp();
+        fft_regs<Nh, E, N, false>(v, t, buf, pad, tw, wsync);
+        const R sc = R(p.scale);
+        if (valid)
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int pp = t + T * m;
+                *reinterpret_cast<C*>(xrow + 2 * pp) = cx<C>(v[m].x * sc, v[m].y * sc);
+            }
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int pp = t + T * m;
+            v[m] = valid ? *reinterpret_cast<const C*>(xrow + 2 * pp) : cx<C>(R(0), R(0));
+        }
+        __syncwarp();
+        fft_regs<Nh, E, N, true>(v, t, buf, pad, tw, wsync);
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int hh = t + T * m;
+            const C z = v[m];
+            C out;
+            if (hh == 0) {
+                out = cx<C>(z.x + z.y, z.x - z.y);  // X(0) + i X(N/2)
+            } else {
+                const C zm = buf[pad(Nh - hh)];
+                const C e = cx<C>(R(0.5) * (z.x + zm.x), R(0.5) * (z.y - zm.y));
+                const C o = cx<C>(R(0.5) * (z.y + zm.y), R(-0.5) * (z.x - zm.x));
+                out = cadd(e, cmul(o, tw[hh]));
+            }
+            if (valid) Srow[hh] = out;
+        }
+    }
+    __syncwarp();
+    }
+}
+
+} // namespace cm

@@ -286,9 +286,11 @@ class Context:
     def set_profiling(self, on: bool) -> None:
         _check(self.lib.cm_set_profiling(self.ptr, int(bool(on))))
 
+    PROFILE_KERNELS = ("z_pass", "y_inverse", "x_c2r", "stencil", "finalize", "x_r2c", "y_forward")
+
     def get_profile(self) -> tuple[list[float], int]:
-        """Accumulated per-kernel device ms {K3, K4, K1, FIN, K2} and iterations."""
-        ms = (C.c_double * 5)()
+        """Accumulated per-kernel device ms (PROFILE_KERNELS order) and iterations."""
+        ms = (C.c_double * 7)()
         it = C.c_int()
         _check(self.lib.cm_get_profile(self.ptr, ms, C.byref(it)))
         return list(ms), it.value

@@ -282,3 +282,28 @@ def test_tolerance_stop_matches_oracle_trace(O):
     assert st["stop_reason"] == 2
     # row i compares x_i and x_{i+1}; the solve stops there and returns x_{i+1}
     assert st["iterations"] == want + 1
+
+
+@pytest.mark.parametrize("n", [128, 256])
+def test_vector_path_without_trace_matches_trace_run(n):
+    """The fp32 4-voxel stencil path skips trace-only terms when no trace is
+    requested; the iterates, the audit and the tolerance stop must not change."""
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=32)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 12})
+    trace = []
+    x_tr = cm.m_step(acc, p.x0, p.x0, cfg, trace, precision=32)
+    x_nt = cm.m_step(acc, p.x0, p.x0, cfg, precision=32)
+    np.testing.assert_array_equal(x_tr, x_nt)
+    sb = np.array([r.before.surrogate() for r in trace])
+    sa = np.array([r.after.surrogate() for r in trace])
+    assert np.all(sa <= sb + 1e-6 * np.abs(sb))  # monotone frozen-weight surrogate
+    rel = np.abs(sb - sa) / np.abs(sb)
+    tol = float(np.sort(rel)[len(rel) // 2])
+    want = int(np.argmax(rel < tol))
+    st = {}
+    cm.m_step(acc, p.x0, p.x0, cm.RegConfig(**{**cfg.__dict__, "tol_kind": 1, "tol": tol}),
+              precision=32, stats=st)
+    assert st["stop_reason"] == 2 and st["iterations"] == want + 1
