@@ -15,9 +15,18 @@
 
 namespace cm {
 
+#ifndef CM_XFFT_E16
+#define CM_XFFT_E16 1
+#endif
+
+// x lines favour fewer, wider stages (radix-16): one exchange for 256 points
+__host__ __device__ constexpr int xelems_for(int LEN) {
+    return (CM_XFFT_E16 && LEN >= 256 && (LEN & (LEN - 1)) == 0) ? 16 : elems_for(LEN);
+}
+
 template <typename R, int N> struct XGeo {
     static constexpr int Nh = N / 2;
-    static constexpr int E = elems_for(Nh);
+    static constexpr int E = xelems_for(Nh);
     static constexpr int T = Nh / E;
     static constexpr int LPC = (256 / T) < 1 ? 1 : (256 / T);  // lines per CTA
     static constexpr int NT = LPC * T < 32 ? 32 : LPC * T;
