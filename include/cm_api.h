@@ -148,6 +148,16 @@ int cm_penalized_objective(cm_ctx* ctx, const double* x, const cm_reg_config* cf
 /* fft3 (fourier.hpp:11): unnormalised forward transform, full complex grid */
 int cm_fft3(cm_ctx* ctx, const double* x, double* out_interleaved);
 
+/* Transform-free components for ANY side n >= 1 (the reference accepts odd and
+ * tiny volumes here, test_regularizer.cpp:141-161, 245); fp64 on the current
+ * device, no context. Same semantics as the context versions above. */
+int cm_compute_weights_n(int n, const double* x, double eps, double eps_prime, int convex,
+                         double* w_l1, double* w_tv);
+int cm_smoothed_tv_value_n(int n, const double* x, double mu, const double* w_tv, double* out);
+int cm_smoothed_tv_gradient_n(int n, const double* x, double mu, const double* w_tv,
+                              double* out);
+int cm_prox_l1_n(long long count, const double* x, const double* thresholds, double* out);
+
 #ifdef __cplusplus
 }
 #endif

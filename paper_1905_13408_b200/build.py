@@ -55,7 +55,8 @@ def build(sides: list[int] | None = None, jobs: int | None = None, force: bool =
     newest = max(p.stat().st_mtime for p in _sources())
     if lib.exists() and not force and lib.stat().st_mtime > newest and sides == SIDES and not out:
         return lib
-    units = [(CSRC / "cm_api.cu", obj_dir / "cm_api.o", list(extra))]
+    units = [(CSRC / "cm_api.cu", obj_dir / "cm_api.o", list(extra)),
+             (CSRC / "generic.cu", obj_dir / "generic.o", list(extra))]
     for n in SIDES:
         defs = [f"-DCM_N={n}", *extra]
         src = CSRC / "inst.cu"
