@@ -31,6 +31,42 @@ template <typename C> __device__ __forceinline__ C cconj(C a) { return cx<C>(a.x
 template <typename C, typename R> __device__ __forceinline__ C cscale(C a, R s) {
     return cx<C>(a.x * s, a.y * s);
 }
+#ifndef CM_FADD2
+#define CM_FADD2 1
+#endif
+#ifndef CM_PACKED_TW
+#define CM_PACKED_TW 0
+#endif
+#if CM_FADD2
+// fp32 complex add / sub as packed FADD2 (sm_100a fp32x2 pipe)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<unsigned long long*>(&a);
+    unsigned long long rb = *reinterpret_cast<unsigned long long*>(&b), rd;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<float2*>(&rd);
+}
+#endif
+
+// Twiddle sources for the FFT engine. Plain: a table of w = exp(-2 pi i q/TWN)
+// (conj for the inverse). Packed (fp32): per entry {w, i w} of the direction
+// in use, so u * w = FFMA2(u.y, i w, FMUL2(u.x, w)) — two packed instructions.
+template <typename C, bool FWD> struct TwPlain {
+    const C* tw;
+    __device__ __forceinline__ C mul(C u, int q) const {
+        const C w = tw[q];
+        return FWD ? cmul(u, w) : cmulc(u, w);
+    }
+};
+struct TwPacked {
+    const float4* tw4;
+    __device__ __forceinline__ float2 mul(float2 u, int q) const {
+        const float4 w = tw4[q];
+        return __ffma2_rn(make_float2(u.y, u.y), make_float2(w.z, w.w),
+                          __fmul2_rn(make_float2(u.x, u.x), make_float2(w.x, w.y)));
+    }
+};
+
 // multiply by -i (fwd=true) or +i
 template <bool FWD, typename C> __device__ __forceinline__ C cmul_mi(C a) {
     return FWD ? cx<C>(a.y, -a.x) : cx<C>(-a.y, a.x);

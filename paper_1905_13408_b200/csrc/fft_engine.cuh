@@ -14,6 +14,8 @@
 // twiddles) and 3.
 #pragma once
 
+#include <type_traits>
+
 #include "cm_common.cuh"
 
 namespace cm {
@@ -82,7 +84,12 @@ __device__ __forceinline__ C tw_const(C z) {
     } else {
         constexpr double c = kCos16(k);
         constexpr double s = FWD ? -kSin16(k) : kSin16(k); // exp(-i a): (cos a, -sin a)
-        return cx<C>(z.x * Rt(c) - z.y * Rt(s), z.x * Rt(s) + z.y * Rt(c));
+        if constexpr (sizeof(Rt) == 4) {
+            return __ffma2_rn(make_float2(z.y, z.y), make_float2(float(-s), float(c)),
+                              __fmul2_rn(make_float2(z.x, z.x), make_float2(float(c), float(s))));
+        } else {
+            return cx<C>(z.x * Rt(c) - z.y * Rt(s), z.x * Rt(s) + z.y * Rt(c));
+        }
     }
 }
 
@@ -148,9 +155,9 @@ template <int R, bool FWD, typename C> struct Dft {
 // Sync: functor performing the barrier that covers all threads of a sequence.
 template <int LEN, int E, int TWN, bool FWD, int SI, int NS>
 struct FftStage {
-    template <typename C, typename Addr, typename Sync>
+    template <typename C, typename Addr, typename Tw, typename Sync>
     static __device__ __forceinline__ void run(C (&v)[E], int t, C* buf, const Addr& addr,
-                                               const C* tw, const Sync& sync) {
+                                               const Tw& tw, const Sync& sync) {
         constexpr int R = radix_at(LEN, E, SI);
         static_assert(R > 0, "LEN/E have no radix plan");
         constexpr int Q = E / R;
@@ -166,10 +173,7 @@ struct FftStage {
             for (int r = 0; r < R; ++r) u[r] = v[q + r * Q];
             if constexpr (NS > 1) {
 #pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    const C w = tw[r * k * TWSTEP];
-                    u[r] = FWD ? cmul(u[r], w) : cmulc(u[r], w);
-                }
+                for (int r = 1; r < R; ++r) u[r] = tw.mul(u[r], r * k * TWSTEP);
             }
             Dft<R, FWD, C>::run(u);
             if constexpr (LAST) {
@@ -191,12 +195,19 @@ struct FftStage {
     }
 };
 
-template <int LEN, int E, int TWN, bool FWD, typename C, typename Addr, typename Sync>
+// tw: a twiddle source (TwPlain / TwPacked) of direction FWD, or a plain table
+template <int LEN, int E, int TWN, bool FWD, typename C, typename Addr, typename Tw,
+          typename Sync>
 __device__ __forceinline__ void fft_regs(C (&v)[E], int t, C* buf, const Addr& addr,
-                                         const C* tw, const Sync& sync) {
+                                         const Tw& tw, const Sync& sync) {
     static_assert(LEN % E == 0, "E must divide LEN");
     static_assert(TWN % LEN == 0, "twiddle table length must be a multiple of LEN");
-    if constexpr (LEN > 1) FftStage<LEN, E, TWN, FWD, 0, 1>::run(v, t, buf, addr, tw, sync);
+    if constexpr (std::is_pointer<Tw>::value) {
+        const TwPlain<C, FWD> src{tw};
+        if constexpr (LEN > 1) FftStage<LEN, E, TWN, FWD, 0, 1>::run(v, t, buf, addr, src, sync);
+    } else {
+        if constexpr (LEN > 1) FftStage<LEN, E, TWN, FWD, 0, 1>::run(v, t, buf, addr, tw, sync);
+    }
 }
 
 // Elements per thread for a transform of length LEN.

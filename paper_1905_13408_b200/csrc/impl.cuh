@@ -249,6 +249,8 @@ struct Impl final : ImplBase {
     C* Yn = nullptr;
     C* Z0 = nullptr;           // forward-transformed packed column 0 [N][N]
     C* twN = nullptr;
+    float4* twF4 = nullptr;    // packed {w, i w} forward / inverse tables (fp32)
+    float4* twI4 = nullptr;
     double* stage = nullptr;   // fp64 staging (3L doubles)
     double* part1 = nullptr;
     double* part3 = nullptr;
@@ -272,7 +274,7 @@ struct Impl final : ImplBase {
 
     ~Impl() override {
         void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, gbuf, S, W,
-                      Wn, Yh, Yn, Z0, twN, stage, part1, part3, part_acc, maxes, st, trace_d,
+                      Wn, Yh, Yn, Z0, twN, twF4, twI4, stage, part1, part3, part_acc, maxes, st, trace_d,
                       theta_d};
         for (void* p : ps)
             if (p) cudaFree(p);
@@ -361,6 +363,19 @@ struct Impl final : ImplBase {
             tw[q].y = R(std::sin(a));
         }
         CK(cudaMemcpyAsync(twN, tw.data(), sizeof(C) * N, cudaMemcpyHostToDevice, stream));
+        if constexpr (sizeof(R) == 4) {
+            std::vector<float4> f(N), iv(N);
+            for (int q = 0; q < N; ++q) {
+                const double a = -2.0 * M_PI * (double)q / (double)N;
+                const float c = (float)std::cos(a), sn = (float)std::sin(a);
+                f[q] = make_float4(c, sn, -sn, c);     // w, i w
+                iv[q] = make_float4(c, -sn, sn, c);    // conj w, i conj w
+            }
+            CKS(dalloc(&twF4, N));
+            CKS(dalloc(&twI4, N));
+            CK(cudaMemcpy(twF4, f.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(twI4, iv.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
+        }
         CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_OBJ>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_TVGRAD>,
@@ -401,7 +416,7 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
     int launch_y(bool fwd, DevState* s) {
-        YParams<R> p{S, twN, s ? (fwd ? &s->done_y : &s->done) : nullptr};
+        YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr};
         dim3 grid(Nh / G::TWY, N);
         if (fwd)
             ypass_kernel<R, N, true><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
@@ -413,7 +428,7 @@ struct Impl final : ImplBase {
     // x-line transforms: dir 0 C2R (S -> g * invL), dir 1 R2C (real -> S)
     int launch_xfft(int dir, R* real, const int* stop) {
         using XG = XGeo<R, N>;
-        XfParams<R> p{S, real, twN, stop, 1.0 / (double)L};
+        XfParams<R> p{S, real, twN, dir == 0 ? twI4 : twF4, stop, 1.0 / (double)L};
         const int grid = std::min(XG::NB, xfft_grid);
         if (dir == 0)
             xfft_kernel<R, N, 0><<<grid, XG::NT, XG::SMEM, stream>>>(p);
@@ -427,7 +442,7 @@ struct Impl final : ImplBase {
     template <int MODE>
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
-        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, part, s};
+        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s};
         dim3 grid(Nh / ZG::TW, N);
         zmain_kernel<R, N, MODE><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
         CK(cudaGetLastError());

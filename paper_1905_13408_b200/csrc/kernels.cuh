@@ -90,6 +90,7 @@ template <typename R> struct YParams {
     using C = Cx<R>;
     C* S;
     const C* twN;
+    const float4* tw4;  // packed table of the pass direction (fp32)
     const int* stop; // &st->done (inverse pass) or &st->done_y (forward pass), or null
 };
 
@@ -97,6 +98,20 @@ template <typename C>
 __device__ __forceinline__ void stage_table(C* dst, const C* src, int n) {
     for (int q = threadIdx.x; q < n; q += blockDim.x) dst[q] = src[q];
 }
+
+// twiddle source of a kernel: packed {w, i w} tables in fp32, plain table in fp64
+template <typename R, bool FWD>
+__device__ __forceinline__ auto tw_src(const Cx<R>* plain, const float4* packed) {
+    if constexpr (sizeof(R) == 4 && CM_PACKED_TW) {
+        return TwPacked{packed};
+    } else {
+        return TwPlain<Cx<R>, FWD>{plain};
+    }
+}
+template <typename R> __host__ __device__ constexpr size_t packed_tw_bytes(int n, int tables) {
+    return (sizeof(R) == 4 && CM_PACKED_TW) ? (size_t)16 * n * tables : 0;
+}
+template <typename R> __host__ __device__ constexpr bool use_packed_tw() { return sizeof(R) == 4 && CM_PACKED_TW; }
 
 // ==================================================================================
 // y pass: FFT along j for every (k, h) column. grid = (Nh/TWY, N)
@@ -110,7 +125,9 @@ ypass_kernel(YParams<R> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
     C* buf = tw + N;
-    stage_table(tw, p.twN, N);
+    float4* tw4 = reinterpret_cast<float4*>(buf + N * G::TWY);
+    if constexpr (use_packed_tw<R>()) stage_table(tw4, p.tw4, N);
+    else stage_table(tw, p.twN, N);
     const int col = threadIdx.x % G::TWY;
     const int t = threadIdx.x / G::TWY;
     const int h = blockIdx.x * G::TWY + col;
@@ -120,7 +137,8 @@ ypass_kernel(YParams<R> p) {
 #pragma unroll
     for (int m = 0; m < G::EY; ++m) v[m] = base[(size_t)(t + G::TY * m) * G::Nh];
     __syncthreads();
-    fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw, BlockSync{});
+    fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw_src<R, FWD>(tw, tw4),
+                               BlockSync{});
 #pragma unroll
     for (int m = 0; m < G::EY; ++m) base[(size_t)(t + G::TY * m) * G::Nh] = v[m];
 }
@@ -386,7 +404,8 @@ template <typename R, int N> struct XSmem {
         sizeof(Cx<R>) * (N + Geo<R, N>::LPC * Geo<R, N>::PADX) + sizeof(double) * 32 * NP1;
 };
 template <typename R, int N> struct YSmem {
-    static constexpr size_t bytes = sizeof(Cx<R>) * (N + (size_t)N * Geo<R, N>::TWY);
+    static constexpr size_t bytes =
+        sizeof(Cx<R>) * (N + (size_t)N * Geo<R, N>::TWY) + packed_tw_bytes<R>(N, 1);
 };
 
 } // namespace cm

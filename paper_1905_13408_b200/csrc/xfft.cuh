@@ -32,7 +32,7 @@ template <typename R, int N> struct XGeo {
     static constexpr int NT = LPC * T < 32 ? 32 : LPC * T;
     static constexpr int LPCB = NT / T;
     static constexpr int PADX = (Nh + (Nh >> 3) + 2) / 2 * 2;
-    static constexpr size_t SMEM = sizeof(Cx<R>) * (N + (size_t)LPCB * PADX);
+    static constexpr size_t SMEM = sizeof(Cx<R>) * (N + (size_t)LPCB * PADX) + packed_tw_bytes<R>(N, 1);
     static constexpr int NB = (N * N + LPC - 1) / LPC;
 };
 
@@ -41,6 +41,7 @@ template <typename R> struct XfParams {
     C* S;
     R* real;            // C2R: g out (scaled by `scale`); R2C: volume in
     const C* twN;
+    const float4* tw4;  // packed table of the transform direction (fp32)
     const int* stop;    // &st->done (C2R) / &st->done_y (R2C) or null
     double scale;
 };
@@ -55,7 +56,9 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT) xfft_kernel(XfParams<R> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
     C* lines = tw + N;
+    float4* tw4 = reinterpret_cast<float4*>(lines + X::LPCB * X::PADX);
     stage_table(tw, p.twN, N);
+    if constexpr (use_packed_tw<R>()) stage_table(tw4, p.tw4, N);
     __syncthreads();
     const int lg = threadIdx.x / T, t = threadIdx.x % T;
     C* buf = lines + lg * X::PADX;
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT) xfft_kernel(XfParams<R> p) {
             }
         }
         __syncwarp();
-        fft_regs<Nh, E, N, false>(v, t, buf, pad, tw, wsync);
+        fft_regs<Nh, E, N, false>(v, t, buf, pad, tw_src<R, false>(tw, tw4), wsync);
         const R sc = R(p.scale);
         if (valid)
 #pragma unroll
@@ -105,7 +108,7 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT) xfft_kernel(XfParams<R> p) {
             v[m] = valid ? *reinterpret_cast<const C*>(xrow + 2 * pp) : cx<C>(R(0), R(0));
         }
         __syncwarp();
-        fft_regs<Nh, E, N, true>(v, t, buf, pad, tw, wsync);
+        fft_regs<Nh, E, N, true>(v, t, buf, pad, tw_src<R, true>(tw, tw4), wsync);
         __syncwarp();
 #pragma unroll
         for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];

@@ -26,25 +26,39 @@ template <typename R> struct ZMParams {
     const C* Yh;
     const C* Yn;
     const C* twN;
+    const float4* twF4; // packed forward / inverse tables (fp32)
+    const float4* twI4;
     double* part;   // [nblocks_main + N/2 + 1][NP3]
     DevState* st;
 };
 
+#ifndef CM_Z_E8
+#define CM_Z_E8 1
+#endif
+
 template <typename R, int N> struct ZGeo {
-    static constexpr int TW = Geo<R, N>::TWY;
-    static constexpr int T = Geo<R, N>::TY;
+    // 8 elements per thread for power-of-two sides >= 256 so that W and Yh of
+    // the whole column fit in registers next to it (prefetched before the
+    // forward FFT); other sides keep the y-pass plan
+    static constexpr bool E8 = CM_Z_E8 && N >= 256 && (N & (N - 1)) == 0 && sizeof(R) == 4;
+    static constexpr int E = E8 ? 8 : Geo<R, N>::EY;
+    static constexpr int T = N / E;
+    static constexpr int TW = E8 ? (16 < 1024 / T ? 16 : 1024 / T) : Geo<R, N>::TWY;
     static constexpr int NT = TW * T;
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
-    static constexpr size_t SMEM_MAIN = sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64;
+    static constexpr size_t SMEM_MAIN =
+        sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
+    static constexpr int MINB = NT >= 1024 ? 1 : 2;
     static constexpr int NT0 = 2 * Geo<R, N>::TY < 64 ? 64 : 2 * Geo<R, N>::TY;
-    static constexpr size_t SMEM_COL0 = sizeof(Cx<R>) * (N + 5 * (size_t)N) + sizeof(double) * 64;
+    static constexpr size_t SMEM_COL0 =
+        sizeof(Cx<R>) * (N + 5 * (size_t)N) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 1);
 };
 
 template <typename R, int N, int MODE>
-__global__ void __launch_bounds__(ZGeo<R, N>::NT, 2) zmain_kernel(ZMParams<R> p) {
+__global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel(ZMParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
-    constexpr int TW = ZGeo<R, N>::TW, T = G::TY, E = G::EY, Nh = G::Nh;
+    constexpr int TW = ZGeo<R, N>::TW, T = ZGeo<R, N>::T, E = ZGeo<R, N>::E, Nh = G::Nh;
     if (p.st && ld_done(p.st)) {
         // the y-forward pass of the stopping iteration has run; stop the next one
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) p.st->done_y = 1;
@@ -54,7 +68,14 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, 2) zmain_kernel(ZMParams<R> p)
     C* tw = reinterpret_cast<C*>(smem_raw);
     C* buf = tw + N;
     double* red = reinterpret_cast<double*>(buf + N * TW);
-    stage_table(tw, p.twN, N);
+    float4* twF = reinterpret_cast<float4*>(red + 64);
+    float4* twI = twF + N;
+    if constexpr (use_packed_tw<R>()) {
+        stage_table(twF, p.twF4, N);
+        stage_table(twI, p.twI4, N);
+    } else {
+        stage_table(tw, p.twN, N);
+    }
     const int col = threadIdx.x % TW;
     const int t = threadIdx.x / TW;
     const int h = blockIdx.x * TW + col;
@@ -64,8 +85,21 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, 2) zmain_kernel(ZMParams<R> p)
     C v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = base[(size_t)(t + T * m) * plane];
+    // W and Yh of this column are independent of the transform: with the small
+    // plan they are loaded now and land while the forward FFT runs
+    R w[E];
+    C y[E];
+    constexpr bool PREFETCH = ZGeo<R, N>::E8 && MODE != ZM_FWD;
+    if constexpr (PREFETCH) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const size_t gi = ((size_t)(t + T * m) * N + b) * Nh + h;
+            w[m] = __ldg(p.W + gi);
+            y[m] = __ldg(p.Yh + gi);
+        }
+    }
     __syncthreads();
-    fft_regs<N, E, N, true>(v, t, buf, ColAddr{TW, col}, tw, BlockSync{});
+    fft_regs<N, E, N, true>(v, t, buf, ColAddr{TW, col}, tw_src<R, true>(tw, twF), BlockSync{});
     if constexpr (MODE == ZM_FWD) {
 #pragma unroll
         for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
@@ -76,14 +110,13 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, 2) zmain_kernel(ZMParams<R> p)
 #pragma unroll
         for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
     } else {
-        // W and Yh of this column: issue every load before the math
-        R w[E];
-        C y[E];
+        if constexpr (!PREFETCH) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const size_t gi = ((size_t)(t + T * m) * N + b) * Nh + h;
-            w[m] = __ldg(p.W + gi);
-            y[m] = p.Yh[gi];
+            for (int m = 0; m < E; ++m) {
+                const size_t gi = ((size_t)(t + T * m) * N + b) * Nh + h;
+                w[m] = __ldg(p.W + gi);
+                y[m] = p.Yh[gi];
+            }
         }
 #pragma unroll
         for (int m = 0; m < E; ++m) {
@@ -104,7 +137,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, 2) zmain_kernel(ZMParams<R> p)
     }
     if constexpr (MODE == ZM_FIT) return;
     __syncthreads();
-    fft_regs<N, E, N, false>(v, t, buf, ColAddr{TW, col}, tw, BlockSync{});
+    fft_regs<N, E, N, false>(v, t, buf, ColAddr{TW, col}, tw_src<R, false>(tw, twI), BlockSync{});
     if (h != 0)
 #pragma unroll
         for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
@@ -122,7 +155,9 @@ zcol0_kernel(ZMParams<R> p) {
     C* z0s = tw + N;          // [2][N]
     C* bufs = z0s + 2 * N;    // [3][N] (third: scratch of idle threads)
     double* red = reinterpret_cast<double*>(bufs + 3 * N);
-    stage_table(tw, p.twN, N);
+    float4* twI = reinterpret_cast<float4*>(red + 64);
+    if constexpr (use_packed_tw<R>()) stage_table(twI, p.twI4, N);
+    else stage_table(tw, p.twN, N);
     const int bp = blockIdx.x;
     const int r = threadIdx.x / T;             // 0, 1 (and idle threads for tiny N)
     const int t = threadIdx.x % T;
@@ -172,7 +207,8 @@ zcol0_kernel(ZMParams<R> p) {
     }
     if constexpr (MODE == ZM_FIT) return;
     __syncthreads();
-    fft_regs<N, E, N, false>(v, t, bufs + (r < 2 ? r : 2) * N, ColAddr{1, 0}, tw, BlockSync{});
+    fft_regs<N, E, N, false>(v, t, bufs + (r < 2 ? r : 2) * N, ColAddr{1, 0},
+                             tw_src<R, false>(tw, twI), BlockSync{});
     if (active && r < 2)
 #pragma unroll
         for (int m = 0; m < E; ++m) p.S[((size_t)(t + T * m) * N + b) * Nh] = v[m];
