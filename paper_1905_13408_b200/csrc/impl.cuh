@@ -23,6 +23,7 @@
 #include "finalize.cuh"
 #include "kernels.cuh"
 #include "stencil.cuh"
+#include "stencil2.cuh"
 #include "xfft.cuh"
 #include "zpass.cuh"
 #include "tma.cuh"
@@ -240,6 +241,10 @@ struct Impl final : ImplBase {
     CUtensorMap tm_p[3] = {};  // x_prev boxes of X[0..2]
     CUtensorMap tm_gt = {};    // g tiles
     CUtensorMap tm_at = {};    // anchor tiles
+    // z-marching stencil (fp32, N % 128 == 0): per-plane slab maps
+    static constexpr bool S2 = sizeof(R) == 4 && N % 128 == 0;
+    CUtensorMap tm2_x[5] = {}, tm2_p[3] = {}, tm2_g = {}, tm2_a = {};
+    int s2_grid = 0;
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     C* S = nullptr;
@@ -283,6 +288,34 @@ struct Impl final : ImplBase {
     }
 
     long long bytes() const override { return alloc_bytes; }
+
+    int make_map_box(R* ptr, CUtensorMap* out, cuuint32_t bw, cuuint32_t bj, cuuint32_t bk) {
+        if constexpr (sizeof(R) != 4) {
+            return CM_OK;
+        } else {
+            EncodeTiledFn enc = encode_tiled_fn();
+            if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+            const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
+            const cuuint64_t strides[2] = {(cuuint64_t)N * sizeof(R), (cuuint64_t)N * N * sizeof(R)};
+            const cuuint32_t box[3] = {bw, bj, bk};
+            const cuuint32_t es[3] = {1, 1, 1};
+            CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map encode failed");
+            return CM_OK;
+        }
+    }
+    int make_maps2(int which, R* ptr) {  // which: 0..2 X, 3..4 YF
+        if constexpr (!S2) {
+            return CM_OK;
+        } else {
+            using SG = S2Geo<N>;
+            CKS(make_map_box(ptr, &tm2_x[which], SG::XW, SG::XR, 1));
+            if (which < 3) CKS(make_map_box(ptr, &tm2_p[which], SG::XW, SG::PR, 1));
+            return CM_OK;
+        }
+    }
 
     // 3D box map over a real volume, zero OOB fill. kind 0: x box {XSW, TJ+2, TK+2};
     // 1: x_prev box {XSW, TJ+1, TK+1}; 2: interior tile {CI, TJ, TK}
@@ -349,6 +382,20 @@ struct Impl final : ImplBase {
         }
         CKS(make_map_x(gbuf, &tm_gt, 2));
         CKS(make_map_x(anchor, &tm_at, 2));
+        if constexpr (S2) {
+            using SG = S2Geo<N>;
+            for (int q = 0; q < 3; ++q) CKS(make_maps2(q, X[q]));
+            CKS(make_map_box(gbuf, &tm2_g, SG::CI, SG::TJ, 1));
+            CKS(make_map_box(anchor, &tm2_a, SG::CI, SG::TJ, 1));
+            CK(cudaFuncSetAttribute(stencil2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SG::SMEM));
+            int occ2 = 0, dev2 = 0, sms2 = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, stencil2_kernel<N>, SG::NT,
+                                                             SG::SMEM));
+            CK(cudaGetDevice(&dev2));
+            CK(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2));
+            s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
+        }
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
@@ -547,6 +594,7 @@ struct Impl final : ImplBase {
                 if (!YF[q]) {
                     CKS(dalloc(&YF[q], L));
                     CKS(make_map_x(YF[q], &tm_x[3 + q]));
+                    CKS(make_maps2(3 + q, YF[q]));
                 }
         }
         const bool need_winit = (c->refresh == 1) && !convex && !anchor_is_init;
@@ -678,15 +726,25 @@ struct Impl final : ImplBase {
                 p.wtvf = wtvf;
                 p.wl1src = wfixed;
             }
-            stencil_kernel<R, N><<<sweep_grid, StGeo<R, N>::NT, StGeo<R, N>::SMEM, stream>>>(
-                p, *tmx, *tmp, tm_gt, tm_at);
+            const bool use_s2 = S2 && std::getenv("CM_STENCIL1") == nullptr;
+            if constexpr (S2) {
+                if (use_s2) {
+                    const int xi = fista ? 3 + g % 2 : g % 3;
+                    const int pi = fista ? 0 : (g + 2) % 3;
+                    stencil2_kernel<N><<<s2_grid, S2Geo<N>::NT, S2Geo<N>::SMEM, stream>>>(
+                        p, tm2_x[xi], tm2_p[pi], tm2_g, tm2_a);
+                }
+            }
+            if (!use_s2)
+                stencil_kernel<R, N><<<sweep_grid, StGeo<R, N>::NT, StGeo<R, N>::SMEM, stream>>>(
+                    p, *tmx, *tmp, tm_gt, tm_at);
             CK(cudaGetLastError());
             CKS(mark(4));
             // FIN
             FinParams f{};
             f.st = st;
             f.part1 = need_part1 ? part1 : nullptr;
-            f.nb1 = sweep_grid;
+            f.nb1 = use_s2 ? s2_grid : sweep_grid;  // partial slots of the stencil launched
             f.part3 = audit ? part3 : nullptr;
             f.nb3 = NB3;
             f.trace = want_trace ? trace_d : nullptr;

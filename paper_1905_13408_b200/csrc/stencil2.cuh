@@ -1,0 +1,385 @@
+// K1 (fp32, N % 128 == 0) — z-marching register-blocked stencil sweep.
+//
+// Same mathematics as stencil.cuh (regularizer.cpp:44-59, 72-85, 103-110,
+// 125-149, 193-205; gradient.cpp:7-64), reorganised so that every TV dual scale
+//     s(q) = w_tv(q) / max(mu, |Dx(q)|) = 1 / ((|Dx(q)| + eps') max(mu, |Dx(q)|))
+// is computed exactly once and every input sample is read from shared memory
+// once per use:
+//   * a CTA owns a 128 (x) by TJ (y) column of voxels and marches along z over
+//     KC planes; warp w owns row j0 + w, lane l owns x = i0 + 4l .. 4l+3; one
+//     extra warp computes s on the forward halo row j0 + TJ;
+//   * per plane q, TMA brings the x slab (rows j0-1 .. j0+TJ, x halo +-1), the
+//     x_{i-1} slab (rows j0-1 .. j0+TJ-1), and the g and anchor rows into a
+//     4-deep ring (prefetch distance 2 planes, mbarrier complete_tx);
+//   * step k: s(., k+1) is computed from the plane k+1 slab and the rolling
+//     x(., k), published in a 3-deep shared ring, one barrier; then voxel (j, k)
+//     uses s(j,k) and s(j,k+1) from registers, s(j+1,k) from shared memory and
+//     s(i+1) / x(i+-1) from shuffles.
+#pragma once
+
+#include "cm_common.cuh"
+#include "kernels.cuh"
+#include "stencil.cuh"
+#include "tma.cuh"
+
+namespace cm {
+
+template <int N> struct S2Geo {
+    static constexpr int CI = 128;
+    static constexpr int TJ = 8;
+    static constexpr int KC = N < 64 ? N : 64;   // planes per march
+    static constexpr int NW = TJ + 1;            // + halo-row warp
+    static constexpr int NT = NW * 32;
+    static constexpr int XW = 136;               // slab row: global i0-4 .. i0+131
+    static constexpr int XR = TJ + 2;            // x rows j0-1 .. j0+TJ
+    static constexpr int PR = TJ + 1;            // x_prev rows j0-1 .. j0+TJ-1
+    static constexpr int GR = TJ;                // g / anchor rows j0 .. j0+TJ-1
+    static constexpr uint32_t XB = XR * XW * 4, PB = PR * XW * 4, GB = GR * CI * 4;
+    static constexpr size_t al(size_t v) { return (v + 127) / 128 * 128; }
+    static constexpr size_t OFF_P = al(XB), OFF_G = al(OFF_P + PB), OFF_A = al(OFF_G + GB);
+    static constexpr size_t STAGE = al(OFF_A + GB);
+    static constexpr int NSTAGE = 4;
+    static constexpr int SW = CI + 4;            // s row (+ halo column at CI)
+    static constexpr size_t OFF_S = NSTAGE * STAGE;
+    static constexpr size_t S_BYTES = (size_t)3 * (TJ + 1) * SW * 4;
+    static constexpr size_t OFF_RED = al(OFF_S + S_BYTES);
+    static constexpr size_t OFF_BAR = OFF_RED + 32 * NP1 * 8;
+    static constexpr size_t SMEM = OFF_BAR + NSTAGE * 8;
+    static constexpr int NTI = N / CI, NTJ = N / TJ, NTK = N / KC;
+    static constexpr int NTILES = NTI * NTJ * NTK;
+};
+
+template <int N>
+__global__ void __launch_bounds__(S2Geo<N>::NT, 2)
+stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
+                const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmg,
+                const __grid_constant__ CUtensorMap tma) {
+    using G = S2Geo<N>;
+    constexpr int CI = G::CI, TJ = G::TJ, KC = G::KC, XW = G::XW, SW = G::SW;
+    if (p.st && ld_done(p.st)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* Sring = reinterpret_cast<float*>(smem_raw + G::OFF_S);   // [3][TJ+1][SW]
+    double* red = reinterpret_cast<double*>(smem_raw + G::OFF_RED);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + G::OFF_BAR);
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;  // w = row within tile, TJ = halo
+    const bool halo = (w == TJ);
+    const float eps = float(p.eps), epsp = float(p.eps_prime), mu = float(p.mu);
+    const float lr = float(p.lr), lra = float(p.lr * p.alpha), beta = float(p.beta);
+    const float g2 = float(2.0 * p.gamma), inv2mu = float(0.5 / p.mu), hmu = float(0.5 * p.mu);
+    const bool has_beta = p.beta > 0.0, has_alpha = p.alpha > 0.0;
+    const bool with_prev = p.audit && p.xprev;
+    const bool convex = p.convex != 0;
+    const float theta = (p.fista && p.st) ? float(p.theta[p.st->iter]) : 0.f;
+
+    if (tid == 0) {
+        for (int q = 0; q < G::NSTAGE; ++q) mbar_init(&bar[q], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    float fa[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) fa[q] = 0.f;
+    double acc[NP1];
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) acc[q] = 0.0;
+
+    uint32_t phase_bits = 0;  // parity of the next wait on each ring slot
+    for (int tile = blockIdx.x; tile < G::NTILES; tile += gridDim.x) {
+        const int i0 = (tile % G::NTI) * CI;
+        const int j0 = ((tile / G::NTI) % G::NTJ) * TJ;
+        const int k0 = (tile / (G::NTI * G::NTJ)) * KC;
+        // plane q (k0-1 .. k0+KC) lives in ring slot (q - k0 + 1) % NSTAGE
+        auto slot_of = [&](int q) { return (q - k0 + 1) & (G::NSTAGE - 1); };
+        auto stage = [&](int q) { return smem_raw + (size_t)slot_of(q) * G::STAGE; };
+        auto issue = [&](int q) {
+            if (q > k0 + KC || q > N) return;
+            const int sl = slot_of(q);
+            unsigned char* st = smem_raw + (size_t)sl * G::STAGE;
+            mbar_expect_tx(&bar[sl], G::XB + (with_prev ? G::PB : 0u) + 2 * G::GB);
+            tma_load_3d(st, &tmx, i0 - 4, j0 - 1, q, &bar[sl]);
+            if (with_prev) tma_load_3d(st + G::OFF_P, &tmp, i0 - 4, j0 - 1, q, &bar[sl]);
+            // g / anchor rows of planes past the march are never read; out of grid -> 0
+            tma_load_3d(st + G::OFF_G, &tmg, i0, j0, q, &bar[sl]);
+            tma_load_3d(st + G::OFF_A, &tma, i0, j0, q, &bar[sl]);
+        };
+        auto wait = [&](int q) {
+            const int sl = slot_of(q);
+            mbar_wait(&bar[sl], (phase_bits >> sl) & 1u);
+            phase_bits ^= (1u << sl);
+        };
+        if (tid == 0) {
+            issue(k0 - 1);
+            issue(k0);
+            issue(k0 + 1);
+        }
+        wait(k0 - 1);
+        wait(k0);
+
+        const int gj = j0 + w;                 // this warp's row (halo warp: j0 + TJ)
+        const int ii = 4 * lane;
+        const int gi0 = i0 + ii;
+        const bool row_in = gj < N;
+        // x slab row r (global j0 - 1 + r) of plane q, at this lane's 4 voxels
+        auto xrow = [&](int q, int r) -> const float* {
+            return reinterpret_cast<const float*>(stage(q)) + r * XW + 4 + ii;
+        };
+        // s on row w of plane q from the slabs of q and q-1 (rows w+1, w in slab coords)
+        // returns s[4], plus |Dx|, d-sum for the voxels; halo column (i0+CI) via lane 31
+        auto s_row = [&](int q, float (&xq)[4], float (&sv)[4], float (&gn)[4], float (&ds)[4],
+                         float& s_halo) {
+            const float4 c4 = ld4(xrow(q, w + 1));
+            const float4 y4 = ld4(xrow(q, w));
+            const float4 z4 = ld4(xrow(q - 1, w + 1));
+            xq[0] = c4.x; xq[1] = c4.y; xq[2] = c4.z; xq[3] = c4.w;
+            const float yv[4] = {y4.x, y4.y, y4.z, y4.w}, zv[4] = {z4.x, z4.y, z4.z, z4.w};
+            float xl = __shfl_up_sync(0xffffffffu, c4.w, 1);
+            if (lane == 0) xl = xrow(q, w + 1)[-1];
+            const float xlv[4] = {xl, c4.x, c4.y, c4.z};
+            const bool qin = q < N && row_in;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float d1 = (gi0 + c > 0) ? xq[c] - xlv[c] : 0.f;
+                const float d2 = (gj > 0) ? xq[c] - yv[c] : 0.f;
+                const float d3 = (q > 0) ? xq[c] - zv[c] : 0.f;
+                const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                const float mx = mu > g ? mu : g;
+                const float s = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
+                sv[c] = qin ? s : 0.f;
+                gn[c] = g;
+                ds[c] = d1 + d2 + d3;
+            }
+            s_halo = 0.f;
+            if (lane == 31 && has_beta && qin && i0 + CI < N) {  // s at x = i0 + CI
+                const float* r = xrow(q, w + 1) - ii + CI;
+                const float xc = r[0];
+                const float d1 = xc - r[-1];
+                const float d2 = gj > 0 ? xc - r[-XW] : 0.f;
+                const float d3 = q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
+                const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                const float mx = mu > g ? mu : g;
+                s_halo = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
+            }
+        };
+        // per_m_step weights come from a frozen field: s uses w_tv from it
+        auto apply_wtvf = [&](int q, float (&sv)[4], float (&gn)[4], float& s_halo) {
+            if (!p.wtvf || convex || !(q < N && row_in)) return;
+            const float4 wv = __ldg(reinterpret_cast<const float4*>(
+                p.wtvf + ((size_t)q * N + gj) * N + gi0));
+            const float wt[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float mx = mu > gn[c] ? mu : gn[c];
+                sv[c] = wt[c] * rcp_(mx);
+            }
+            if (lane == 31 && i0 + CI < N && has_beta) {
+                const float wh = __ldg(p.wtvf + ((size_t)q * N + gj) * N + i0 + CI);
+                const float* r = xrow(q, w + 1) - ii + CI;
+                const float xc = r[0];
+                const float d1 = xc - r[-1];
+                const float d2 = gj > 0 ? xc - r[-XW] : 0.f;
+                const float d3 = q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
+                const float gg = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                s_halo = wh * rcp_(mu > gg ? mu : gg);
+            }
+        };
+
+        // ---- prologue: s(., k0), rolling state of plane k0 and x_prev(k0-1)
+        float x_cur[4], s_cur[4], gn_cur[4], ds_cur[4], sh_cur;
+        s_row(k0, x_cur, s_cur, gn_cur, ds_cur, sh_cur);
+        apply_wtvf(k0, s_cur, gn_cur, sh_cur);
+        float* S0 = Sring + (size_t)((k0) % 3) * (TJ + 1) * SW;
+        if (has_beta) {
+            *reinterpret_cast<float4*>(S0 + w * SW + ii) =
+                make_float4(s_cur[0], s_cur[1], s_cur[2], s_cur[3]);
+            if (lane == 31) S0[w * SW + CI] = sh_cur;
+        }
+        float xp_prev[4] = {0.f, 0.f, 0.f, 0.f};
+        if (with_prev && !halo) {
+            const float4 v = ld4(reinterpret_cast<const float*>(stage(k0 - 1) + G::OFF_P) +
+                                 (w + 1) * XW + 4 + ii);
+            xp_prev[0] = v.x; xp_prev[1] = v.y; xp_prev[2] = v.z; xp_prev[3] = v.w;
+        }
+        __syncthreads();
+
+        for (int k = k0; k < k0 + KC; ++k) {
+            if (tid == 0) issue(k + 2);  // slot of plane k-2: released by the previous barrier
+            wait(k + 1);
+            // ---- s of plane k+1 on this warp's row
+            float x_nx[4], s_nx[4], gn_nx[4], ds_nx[4], sh_nx;
+            s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx, sh_nx);
+            apply_wtvf(k + 1, s_nx, gn_nx, sh_nx);
+            float* Sn = Sring + (size_t)((k + 1) % 3) * (TJ + 1) * SW;
+            if (has_beta) {
+                *reinterpret_cast<float4*>(Sn + w * SW + ii) =
+                    make_float4(s_nx[0], s_nx[1], s_nx[2], s_nx[3]);
+                if (lane == 31) Sn[w * SW + CI] = sh_nx;
+            }
+            __syncthreads();
+            if (!halo && row_in) {
+                // ---- voxel (j, k): update, prox, partials
+                const float* Sc = Sring + (size_t)(k % 3) * (TJ + 1) * SW;
+                const size_t gidx = ((size_t)k * N + gj) * N + gi0;
+                const unsigned char* stk = stage(k);
+                const float4 g4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_G) + w * CI + ii);
+                const float4 a4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_A) + w * CI + ii);
+                const float gg[4] = {g4.x, g4.y, g4.z, g4.w}, av[4] = {a4.x, a4.y, a4.z, a4.w};
+                float tvg[4] = {0.f, 0.f, 0.f, 0.f};
+                if (has_beta) {
+                    // x(j+1, k) and s(j+1, k): next row; x(i+1), s(i+1): next voxel
+                    const float4 yp4 = ld4(xrow(k, w + 2));
+                    const float4 sy4 = ld4(Sc + (w + 1) * SW + ii);
+                    float xr4 = __shfl_down_sync(0xffffffffu, x_cur[0], 1);
+                    float sr4 = __shfl_down_sync(0xffffffffu, s_cur[0], 1);
+                    if (lane == 31) {
+                        xr4 = xrow(k, w + 1)[4];          // x at i0 + CI
+                        sr4 = Sc[w * SW + CI];
+                    }
+                    const float xn[4] = {x_cur[1], x_cur[2], x_cur[3], xr4};
+                    const float sxv[4] = {s_cur[1], s_cur[2], s_cur[3], sr4};
+                    const float yp[4] = {yp4.x, yp4.y, yp4.z, yp4.w};
+                    const float sy[4] = {sy4.x, sy4.y, sy4.z, sy4.w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        float t = s_cur[c] * ds_cur[c];
+                        if (gi0 + c < N - 1) t -= sxv[c] * (xn[c] - x_cur[c]);
+                        if (gj < N - 1) t -= sy[c] * (yp[c] - x_cur[c]);
+                        if (k < N - 1) t -= s_nx[c] * (x_nx[c] - x_cur[c]);
+                        tvg[c] = t;
+                    }
+                }
+                float wl1[4] = {1.f, 1.f, 1.f, 1.f}, wtv[4] = {1.f, 1.f, 1.f, 1.f};
+                if (!convex) {
+                    float ws[4] = {x_cur[0], x_cur[1], x_cur[2], x_cur[3]};
+                    if (p.wl1src) {
+                        if (p.wl1src == p.anchor) {
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) ws[c] = av[c];
+                        } else {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(p.wl1src + gidx));
+                            ws[0] = v.x; ws[1] = v.y; ws[2] = v.z; ws[3] = v.w;
+                        }
+                    }
+                    if (p.wtvf) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(p.wtvf + gidx));
+                        wtv[0] = v.x; wtv[1] = v.y; wtv[2] = v.z; wtv[3] = v.w;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) wl1[c] = rcp_(fabsf(ws[c]) + eps);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float a = fabsf(ws[c]) + eps, b = gn_cur[c] + epsp;
+                            const float r = rcp_(a * b);
+                            wl1[c] = b * r;
+                            wtv[c] = a * r;
+                        }
+                    }
+                }
+                float base[4] = {x_cur[0], x_cur[1], x_cur[2], x_cur[3]};
+                if (p.fista) {
+                    const float4 o4 = __ldg(reinterpret_cast<const float4*>(p.xold + gidx));
+                    base[0] = o4.x; base[1] = o4.y; base[2] = o4.z; base[3] = o4.w;
+                }
+                float nx[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float gs = 2.f * gg[c] + g2 * (x_cur[c] - av[c]);
+                    if (has_beta) gs += beta * tvg[c];
+                    float v = x_cur[c] - lr * gs;
+                    if (has_alpha) {
+                        const float th = lra * wl1[c];
+                        v = fabsf(v) <= th ? 0.f : v - copysignf(th, v);
+                    }
+                    nx[c] = v;
+                }
+                *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+                if (p.fista) {
+                    float y[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
+                    *reinterpret_cast<float4*>(p.ynext + gidx) = make_float4(y[0], y[1], y[2], y[3]);
+                }
+                if (p.steptol) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float dx = nx[c] - base[c];
+                        fa[9] += dx * dx;
+                        fa[10] += nx[c] * nx[c];
+                    }
+                }
+                if (p.audit) {
+                    float pl1[4] = {0.f, 0.f, 0.f, 0.f}, ptv[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (with_prev) {
+                        const float* P = reinterpret_cast<const float*>(stk + G::OFF_P);
+                        const float4 pc4 = ld4(P + (w + 1) * XW + 4 + ii);
+                        const float4 py4 = ld4(P + w * XW + 4 + ii);
+                        float pm = __shfl_up_sync(0xffffffffu, pc4.w, 1);
+                        if (lane == 0) pm = P[(w + 1) * XW + 3];
+                        const float pc[4] = {pc4.x, pc4.y, pc4.z, pc4.w};
+                        const float pl[4] = {pm, pc4.x, pc4.y, pc4.z};
+                        const float py[4] = {py4.x, py4.y, py4.z, py4.w};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float e1 = (gi0 + c > 0) ? pc[c] - pl[c] : 0.f;
+                            const float e2 = gj > 0 ? pc[c] - py[c] : 0.f;
+                            const float e3 = k > 0 ? pc[c] - xp_prev[c] : 0.f;
+                            const float a = fabsf(pc[c]) + eps;
+                            const float b = sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp;
+                            const float r = rcp_(a * b);
+                            pl1[c] = b * r;
+                            ptv[c] = a * r;
+                            xp_prev[c] = pc[c];
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float ax = fabsf(x_cur[c]), g = gn_cur[c];
+                        const float hb = g < mu ? g * g * inv2mu : g - hmu;
+                        fa[0] += wl1[c] * ax;
+                        fa[1] += wtv[c] * hb;
+                        const float dd = x_cur[c] - av[c];
+                        fa[5] += dd * dd;
+                        if (with_prev) {
+                            fa[6] += pl1[c] * ax;
+                            fa[7] += ptv[c] * hb;
+                        }
+                        if (p.trace_full) {
+                            fa[2] += wtv[c] * g;
+                            fa[3] += __logf(ax + eps);
+                            fa[4] += __logf(g + epsp);
+                            if (with_prev) fa[8] += ptv[c] * g;
+                        }
+                    }
+                }
+            }
+            // roll plane k+1 into place
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                x_cur[c] = x_nx[c];
+                s_cur[c] = s_nx[c];
+                gn_cur[c] = gn_nx[c];
+                ds_cur[c] = ds_nx[c];
+            }
+            if (((k - k0) & 7) == 7) {
+#pragma unroll
+                for (int q = 0; q < NP1; ++q) {
+                    acc[q] += (double)fa[q];
+                    fa[q] = 0.f;
+                }
+            }
+        }
+        // every issued plane (k0-1 .. k0+KC) has been waited on
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < NP1; ++q) acc[q] += (double)fa[q];
+    if (p.part) {
+        block_sum<NP1>(acc, red);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int q = 0; q < NP1; ++q) p.part[(size_t)blockIdx.x * NP1 + q] = acc[q];
+    }
+}
+
+} // namespace cm
