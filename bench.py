@@ -50,7 +50,6 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ttt", type=int, default=1, help="measure time-to-tolerance (0/1)")
     ap.add_argument("--ttt-max-iters", type=int, default=6000)
-    ap.add_argument("--tol", type=float, default=1e-6)
     return ap.parse_args()
 
 
@@ -367,21 +366,26 @@ def run_ours(args):
                "d2h_bytes_per_step": 8 * L, "steps": args.e2e_steps,
                "ms_per_step": e_ms / args.e2e_steps}
 
-    # ---- time to tolerance (ISTA reference semantics, then FISTA) -----------------------
+    # ---- time to tolerance ----------------------------------------------------------------
+    # "Medium accuracy" = relative error <= 1e-2 against a converged
+    # solution (profiles/r1_convergence_512.json: a 20000-iteration FISTA run with
+    # frozen weights). Stopping rules calibrated there: FISTA stops on the step norm
+    # falling below 3% of the largest step (0.50% error); the reference's ISTA needs
+    # a 3e-7 frozen-weight surrogate decrease to get to 0.99%.
     ttt = None
     if args.ttt:
-        ttt = {}
-        for name, extra in (("ista", dict(momentum=0, tol_kind=1)),
-                            ("fista", dict(momentum=1, tol_kind=2))):
+        ttt = {"definition": "rel. error <= 1e-2 vs converged solution (profiles/r1_convergence_512.json)"}
+        for name, extra in (("fista", dict(momentum=1, tol_kind=2, tol=0.03)),
+                            ("ista", dict(momentum=0, tol_kind=1, tol=3e-7))):
             tc = cm.RegConfig(**{**cfg.__dict__, "inner_iters": args.ttt_max_iters,
-                                 "refresh": cm.Refresh.per_m_step, "tol": args.tol, **extra})
+                                 "refresh": cm.Refresh.per_m_step, **extra})
             torch.cuda.synchronize()
             st = ctx.solve(tc)
             ttt[name] = {"iterations": st.iterations, "seconds": st.solve_ms / 1e3,
                          "stop_reason": st.stop_reason, "last_rel": st.last_rel,
-                         "criterion": ("frozen-weight surrogate relative decrease" if name == "ista"
-                                       else "relative step ||x+ - x||/||x+||"),
-                         "tol": args.tol, "refresh": "per_m_step"}
+                         "criterion": ("step norm < 3% of the largest step" if name == "fista"
+                                       else "frozen-weight surrogate relative decrease < 3e-7"),
+                         "refresh": "per_m_step"}
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

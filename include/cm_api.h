@@ -59,7 +59,8 @@ typedef struct {
     /* ---- extensions ---- */
     int momentum;                /* 0 ISTA (reference), 1 FISTA (no monotone audit) */
     int tol_kind;                /* 0 none, 1 frozen-weight surrogate relative decrease,
-                                    2 relative step ||x+ - x|| / ||x+|| */
+                                    2 step norm ||x+ - x|| relative to the largest step
+                                      so far (works with FISTA) */
     double tol;                  /* stop when the measure drops below tol */
     double audit_slack;          /* <= 0: 1e-9 in fp64 (reference), 1e-6 in fp32 */
 } cm_reg_config;

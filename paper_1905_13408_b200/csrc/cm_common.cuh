@@ -94,6 +94,7 @@ struct DevState {
     double step;        // l_r (constant within one m_step)
     double before[7];   // before_i of the iteration being audited (saved by finalize)
     double last_rel;    // last tolerance measure
+    double step_max;    // largest ||x_{k+1} - x_k|| seen (tol_kind 2 normaliser)
 };
 
 __device__ __forceinline__ int ld_done(const DevState* st) {

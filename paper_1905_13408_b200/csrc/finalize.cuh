@@ -90,9 +90,13 @@ static __global__ void __launch_bounds__(256) finalize_kernel(FinParams p) {
     for (int q = 0; q < 7; ++q) st->before[q] = cur[q];
     st->iter = i + 1;
     if (st->tol_kind == 2) {
-        const double rel = sqrt(s[9] / fmax(s[10], 1e-300));
+        // scale-free step rule: ||x_{k+1} - x_k|| relative to the largest step so
+        // far (the first steps are tiny under the Lipschitz step of the TV term)
+        const double dn = sqrt(s[9]);
+        st->step_max = fmax(st->step_max, dn);
+        const double rel = dn / fmax(st->step_max, 1e-300);
         st->last_rel = rel;
-        if (rel < st->tol) {
+        if (i >= 1 && rel < st->tol) {
             st->stop_reason = 2;
             st->done = 1;
             return;
