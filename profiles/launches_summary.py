@@ -21,7 +21,7 @@ for r in rows:
 
 MAP = [(r"zmain_kernel<\w+, \d+, 0>", "z_pass"), (r"zcol0_kernel<\w+, \d+, 0>", "z_pass"),
        (r"ypass_kernel<\w+, \d+, 0>", "y_inverse"), (r"xfft_kernel<\w+, \d+, 0>", "x_c2r"),
-       (r"stencil_kernel", "stencil"), (r"^finalize_kernel", "finalize"),
+       (r"stencil2?_kernel", "stencil"), (r"^finalize_kernel", "finalize"),
        (r"xfft_kernel<\w+, \d+, 1>", "x_r2c"), (r"ypass_kernel<\w+, \d+, 1>", "y_forward")]
 per = collections.defaultdict(lambda: {"time_us": 0.0, "dram_bytes": 0.0, "launches": 0})
 lines = ["| kernel (launch name) | launches | avg time (us) | DRAM read+write per launch (GB) |", "|---|---|---|---|"]
