@@ -159,6 +159,30 @@ int cm_smoothed_tv_gradient_n(int n, const double* x, double mu, const double* w
                               double* out);
 int cm_prox_l1_n(long long count, const double* x, const double* thresholds, double* out);
 
+/* ---- z-slab distributed solver (one process per GPU) ----
+ * The same m_step, split over `world` ranks: rank r owns the real-space planes
+ * k in [r n/world, (r+1) n/world) and the spectrum rows b in the same range;
+ * the transposes are NCCL all-to-alls, the stencil needs one ghost plane per
+ * side. fp32, n a multiple of 128, n/world a multiple of 64.
+ * nccl_id: 128 bytes from cm_nccl_unique_id on rank 0, broadcast by the caller
+ * (e.g. torch.distributed); NULL emulates all `world` ranks inside this process
+ * on `device` (decomposition tests on one GPU). Every rank passes the full
+ * accumulator and volumes (as the reference's BackProjector state is full-grid);
+ * cm_dctx_get_volume writes only the planes of the ranks this process hosts. */
+typedef struct cm_dctx cm_dctx;
+int cm_nccl_unique_id(unsigned char* id128);
+int cm_dctx_create(int n, int world, int rank, int device, const unsigned char* nccl_id,
+                   cm_dctx** out);
+int cm_dctx_destroy(cm_dctx* d);
+/* planes per rank, first plane of this process, ranks hosted by this process */
+int cm_dctx_layout(const cm_dctx* d, int* planes_per_rank, int* first_plane, int* ranks_here);
+int cm_dctx_set_accumulator(cm_dctx* d, const double* weight, const double* numerator,
+                            int finalized);
+int cm_dctx_set_volumes(cm_dctx* d, const double* x_init, const double* x_anchor);
+int cm_dctx_solve(cm_dctx* d, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
+                  cm_solve_stats* stats);
+int cm_dctx_get_volume(cm_dctx* d, double* x_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,4 +13,7 @@ from .regularizer import (  # noqa: F401
     prox_l1, scale_data, smoothed_tv_gradient, smoothed_tv_value, validate_reg_config,
 )
 
+from . import slab  # noqa: F401,E402
+from .slab import SlabContext, SlabPlan  # noqa: F401,E402
+
 __version__ = "0.1.0"

@@ -87,6 +87,14 @@ def load() -> C.CDLL:
         "cm_smoothed_tv_value_n": [C.c_int, P, C.c_double, P, _dp],
         "cm_smoothed_tv_gradient_n": [C.c_int, P, C.c_double, P, P],
         "cm_prox_l1_n": [C.c_longlong, P, P, P],
+        "cm_nccl_unique_id": [P],
+        "cm_dctx_create": [C.c_int, C.c_int, C.c_int, C.c_int, P, C.POINTER(P)],
+        "cm_dctx_destroy": [P],
+        "cm_dctx_layout": [P, _ip, _ip, _ip],
+        "cm_dctx_set_accumulator": [P, P, P, C.c_int],
+        "cm_dctx_set_volumes": [P, P, P],
+        "cm_dctx_solve": [P, C.POINTER(cm_reg_config), P, C.c_int, C.POINTER(cm_solve_stats)],
+        "cm_dctx_get_volume": [P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

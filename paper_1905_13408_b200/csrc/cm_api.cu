@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/cm_api.h"
+#include "dist.cuh"
 #include "impl.cuh"
 
 namespace cm {
@@ -21,6 +22,19 @@ int fail(int code, const std::string& msg) {
     X(256) X(384) X(512) X(768) X(1024)
 #define CM_DECL(NN) ImplBase* make_impl_##NN(int precision);
 CM_SIDES(CM_DECL)
+
+#define CM_DDECL(NN) DistBase* make_dist_##NN();
+CM_SIDES(CM_DDECL)
+
+static DistBase* make_dist(int n) {
+    switch (n) {
+#define CM_DCASE(NN) \
+    case NN: return make_dist_##NN();
+        CM_SIDES(CM_DCASE)
+#undef CM_DCASE
+        default: return nullptr;
+    }
+}
 
 static ImplBase* make_impl(int n, int precision) {
     switch (n) {
@@ -237,6 +251,101 @@ int cm_penalized_objective(cm_ctx* ctx, const double* x, const cm_reg_config* cf
 int cm_fft3(cm_ctx* ctx, const double* x, double* out_interleaved) {
     CTX_GUARD(ctx);
     return ctx->impl->fft3(x, out_interleaved);
+}
+
+// ---- z-slab distributed solver ------------------------------------------------------
+struct cm_dctx {
+    std::unique_ptr<DistBase> impl;
+    int n = 0;
+};
+
+int cm_nccl_unique_id(unsigned char* id128) {
+    if (!id128) return fail(CM_ERR_INVALID_ARGUMENT, "null id");
+    std::string err;
+    if (!nccl_api().load(&err)) return fail(CM_ERR_NCCL, err);
+    ncclUniqueId id;
+    if (nccl_api().GetUniqueId(&id) != ncclSuccess) return fail(CM_ERR_NCCL, "ncclGetUniqueId failed");
+    std::memcpy(id128, id.internal, sizeof(id.internal));
+    return CM_OK;
+}
+
+int cm_dctx_create(int n, int world, int rank, int device, const unsigned char* nccl_id,
+                   cm_dctx** out) {
+    if (!out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(CM_ERR_INVALID_ARGUMENT, "bad world/rank");
+    if (n % 128 != 0 || n % world != 0 || (n / world) % 64 != 0)
+        return fail(CM_ERR_UNSUPPORTED, "z-slab solver needs n % 128 == 0 and n/world % 64 == 0");
+    CK(cudaSetDevice(device));
+    auto d = std::make_unique<cm_dctx>();
+    d->n = n;
+    d->impl.reset(make_dist(n));
+    if (!d->impl) return fail(CM_ERR_UNSUPPORTED, "no z-slab build for side " + std::to_string(n));
+    d->impl->device = device;
+    if (nccl_id) {
+        ncclUniqueId id;
+        std::memcpy(id.internal, nccl_id, sizeof(id.internal));
+        int st = 0;
+        auto c = std::make_unique<NcclComm>(world, rank, id, &st);
+        if (st) return fail(CM_ERR_NCCL, "NCCL init failed: " + c->err);
+        d->impl->comm = std::move(c);
+    } else {
+        if (rank != 0) return fail(CM_ERR_INVALID_ARGUMENT, "emulated ranks: pass rank 0");
+        d->impl->comm = std::make_unique<EmuComm>(world);
+    }
+    const int rc = d->impl->init();
+    if (rc != CM_OK) return rc;
+    *out = d.release();
+    return CM_OK;
+}
+
+#define DCTX_GUARD(d)                                                                      \
+    do {                                                                                   \
+        if (!(d) || !(d)->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");      \
+        if (cudaSetDevice((d)->impl->device) != cudaSuccess)                               \
+            return fail(CM_ERR_CUDA, "cudaSetDevice failed");                              \
+    } while (0)
+
+int cm_dctx_destroy(cm_dctx* d) {
+    if (!d) return CM_OK;
+    if (d->impl) cudaSetDevice(d->impl->device);
+    delete d;
+    return CM_OK;
+}
+
+int cm_dctx_layout(const cm_dctx* d, int* planes_per_rank, int* first_plane, int* ranks_here) {
+    if (!d || !d->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
+    const Comm& c = *d->impl->comm;
+    if (planes_per_rank) *planes_per_rank = d->n / c.P;
+    if (first_plane) *first_plane = c.rank0 * (d->n / c.P);
+    if (ranks_here) *ranks_here = c.nv;
+    return CM_OK;
+}
+
+int cm_dctx_set_accumulator(cm_dctx* d, const double* weight, const double* numerator,
+                            int finalized) {
+    DCTX_GUARD(d);
+    if (!weight || !numerator) return fail(CM_ERR_INVALID_ARGUMENT, "null accumulator");
+    return d->impl->set_accumulator(weight, numerator, finalized);
+}
+
+int cm_dctx_set_volumes(cm_dctx* d, const double* x_init, const double* x_anchor) {
+    DCTX_GUARD(d);
+    if (!x_init || !x_anchor) return fail(CM_ERR_INVALID_ARGUMENT, "null volume");
+    return d->impl->set_volumes(x_init, x_anchor);
+}
+
+int cm_dctx_solve(cm_dctx* d, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
+                  cm_solve_stats* stats) {
+    DCTX_GUARD(d);
+    return d->impl->solve(cfg, trace, trace_cap, stats);
+}
+
+int cm_dctx_get_volume(cm_dctx* d, double* x_out) {
+    DCTX_GUARD(d);
+    if (!x_out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    return d->impl->get_volume(x_out);
 }
 
 } // extern "C"

@@ -1,0 +1,735 @@
+// z-slab distributed M-step solver, fp32, N % 128 == 0.
+//
+// Rank r of P owns real-space planes k in [r NK, (r+1) NK) (NK = N/P, one ghost
+// plane on each side) and, for the z pass, spectrum rows b in [r NB, (r+1) NB)
+// (NB = N/P). One iteration on every rank:
+//   z pass on its b rows (all c)            zmain_kernel (nrows = NB)
+//   all-gather of the packed column-0 pencils, Friedel pairing per row   zcol0r
+//   all-to-all  (b-slab -> z-slab)
+//   y inverse: destination-major -> natural  ypass_kernel<false, DM>
+//   x C2R -> g, stencil sweep (ghost planes), halo exchange of x_{i+1}
+//   finalize: local partials -> all-reduce -> audit/trace/tolerance
+//   x R2C, y forward: natural -> destination-major (the all-to-all send layout)
+//   all-to-all  (z-slab -> b-slab)
+// The y passes read/write the destination-major layout [s][k][b_local][h], so
+// both transposes are single all-to-alls with no pack/unpack kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.cuh"
+#include "impl.cuh"
+
+namespace cm {
+
+// packed column 0 of one local row b (global rb0 + b_local): Friedel pairing
+// against the all-gathered pencils, multiply, fit partials, inverse z FFT
+template <int N, int MODE>
+__global__ void __launch_bounds__(Geo<float, N>::TY < 32 ? 32 : Geo<float, N>::TY)
+zcol0r_kernel(ZMParams<float> p, const float2* Z0full, int rb0) {
+    using G = Geo<float, N>;
+    using C = float2;
+    constexpr int T = G::TY, E = G::EY, Nh = G::Nh;
+    if (p.st && ld_done(p.st)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    C* tw = reinterpret_cast<C*>(smem_raw);
+    C* buf = tw + N;  // [2][N]: the second half is scratch of idle threads (N < 512)
+    double* red = reinterpret_cast<double*>(buf + 2 * N);
+    stage_table(tw, p.twN, N);
+    __syncthreads();
+    const int bl = blockIdx.x, b = rb0 + bl, bm = (N - b) % N;
+    const int t = threadIdx.x;
+    const bool act = t < T;
+    C v[E];
+    double quad = 0.0, cross = 0.0;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int c = (act ? t : 0) + T * m;
+        const C zz = Z0full[(size_t)b * N + c];
+        const C zm = Z0full[(size_t)bm * N + (N - c) % N];
+        const C f0 = make_float2(0.5f * (zz.x + zm.x), 0.5f * (zz.y - zm.y));
+        const C fn = make_float2(0.5f * (zz.y + zm.y), -0.5f * (zz.x - zm.x));
+        const size_t gi = ((size_t)c * p.nrows + bl) * Nh;
+        const size_t ni = (size_t)c * p.nrows + bl;
+        const float w0 = p.W[gi], wn = p.Wn[ni];
+        const C y0 = p.Yh[gi], yn = p.Yn[ni];
+        if (act) {
+            quad += (double)w0 * ((double)f0.x * f0.x + (double)f0.y * f0.y) +
+                    (double)wn * ((double)fn.x * fn.x + (double)fn.y * fn.y);
+            cross += ((double)y0.x * f0.x + (double)y0.y * f0.y) +
+                     ((double)yn.x * fn.x + (double)yn.y * fn.y);
+        }
+        const C g0 = make_float2(w0 * f0.x - y0.x, w0 * f0.y - y0.y);
+        const C gn = make_float2(wn * fn.x - yn.x, wn * fn.y - yn.y);
+        v[m] = make_float2(g0.x - gn.y, g0.y + gn.x);
+    }
+    if (p.part) {
+        double acc[2] = {quad, cross};
+        block_sum<2>(acc, red);
+        if (threadIdx.x == 0) {
+            const int slot = (Nh / ZGeo<float, N>::TW) * p.nrows + bl;
+            p.part[slot * NP3 + 0] = acc[0];
+            p.part[slot * NP3 + 1] = acc[1];
+        }
+    }
+    if constexpr (MODE == ZM_FIT) return;
+    __syncthreads();
+    fft_regs<N, E, N, false>(v, act ? t : 0, buf + (act ? 0 : N), ColAddr{1, 0}, tw, BlockSync{});
+    if (act)
+#pragma unroll
+        for (int m = 0; m < E; ++m) p.S[((size_t)(t + T * m) * p.nrows + bl) * Nh] = v[m];
+}
+
+// Full-grid fp64 accumulator -> this rank's b rows of the packed half spectrum
+// (same projection and sign as convert_acc_kernel); statistics over the full grid
+// are taken once by the owner of the staging copy.
+__global__ static void convert_rows_kernel(int n, int rb0, int nrows, const double* __restrict__ W,
+                                           const double* __restrict__ Y, float* Wm, float* Wn,
+                                           float2* Ym, float2* Yn) {
+    const int nh = n / 2;
+    const size_t total = (size_t)n * nrows * (nh + 1);
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(q % (nh + 1));
+        const size_t bc = q / (nh + 1);
+        const int bl = (int)(bc % nrows), c = (int)(bc / nrows);
+        const int b = rb0 + bl;
+        const int am = a ? n - a : 0, bm = b ? n - b : 0, cm_ = c ? n - c : 0;
+        const size_t i = ((size_t)c * n + b) * n + a;
+        const size_t m = ((size_t)cm_ * n + bm) * n + am;
+        const double wp = 0.5 * (W[i] + W[m]);
+        const double sg = ((a + b + c) & 1) ? -1.0 : 1.0;
+        const double pr = sg * 0.5 * (Y[2 * i] + Y[2 * m]), pi = sg * 0.5 * (Y[2 * i + 1] - Y[2 * m + 1]);
+        if (a < nh) {
+            const size_t o = ((size_t)c * nrows + bl) * nh + a;
+            Wm[o] = float(wp);
+            Ym[o] = make_float2(float(pr), float(pi));
+        } else {
+            const size_t o = (size_t)c * nrows + bl;
+            Wn[o] = float(wp);
+            Yn[o] = make_float2(float(pr), float(pi));
+        }
+    }
+}
+
+// w_tv of a frozen weight source on this rank's planes (ghosted layout)
+__global__ static void wtv_field_kernel(const float* x, int n, int koff, int nk, float epsp,
+                                        float* out) {
+    const size_t L = (size_t)n * n * nk;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < L;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(q % n), j = (int)((q / n) % n), kl = (int)(q / ((size_t)n * n));
+        const size_t c = ((size_t)(kl + 1) * n + j) * n + i;
+        const float xc = x[c];
+        const float d1 = i > 0 ? xc - x[c - 1] : 0.f;
+        const float d2 = j > 0 ? xc - x[c - n] : 0.f;
+        const float d3 = koff + kl > 0 ? xc - x[c - (size_t)n * n] : 0.f;
+        out[c] = 1.f / (sqrtf(d1 * d1 + d2 * d2 + d3 * d3) + epsp);
+    }
+}
+
+struct DistBase {
+    virtual ~DistBase() = default;
+    virtual int init() = 0;
+    virtual int set_accumulator(const double* w, const double* y, int finalized) = 0;
+    virtual int set_volumes(const double* xi, const double* xa) = 0;
+    virtual int solve(const cm_reg_config* c, cm_trace_row* tr, int cap, cm_solve_stats* st) = 0;
+    virtual int get_volume(double* out) = 0;
+    std::unique_ptr<Comm> comm;
+    int device = 0;
+};
+
+template <int N>
+struct DistImpl final : DistBase {
+    using R = float;
+    using C = float2;
+    static constexpr int Nh = N / 2;
+    static constexpr size_t NN = (size_t)N * N;
+    using SG = S2Geo<N>;
+    using ZG = ZGeo<R, N>;
+    using XG = XGeo<R, N>;
+    static_assert(N % 128 == 0, "z-slab solver: 128-wide stencil tiles");
+    static_assert(!use_packed_tw<R>(), "z-slab kernels use the plain twiddle table");
+
+    struct Rank {
+        int r = 0;        // global rank
+        int koff = 0;     // first plane
+        int rb0 = 0;      // first spectrum row
+        R* X[3] = {};
+        R* XF[2] = {};
+        R* YF[2] = {};
+        R* x0keep = nullptr;
+        R* anchor = nullptr;
+        R* g = nullptr;
+        R* wtvf = nullptr;
+        C* Snat = nullptr;
+        C* Ssend = nullptr;
+        C* Srecv = nullptr;
+        R* W = nullptr;
+        R* Wn = nullptr;
+        C* Yh = nullptr;
+        C* Yn = nullptr;
+        C* Z0 = nullptr;
+        C* Z0full = nullptr;
+        C* twN = nullptr;
+        float4* twF4 = nullptr;
+        float4* twI4 = nullptr;
+        double* part1 = nullptr;
+        double* part3 = nullptr;
+        double* sums = nullptr;
+        DevState* st = nullptr;
+        double* trace = nullptr;
+        double* theta = nullptr;
+        CUtensorMap tmx[5] = {}, tmp[3] = {}, tmg = {}, tma = {};
+    };
+
+    int P = 1, NK = N, NB = N;
+    std::vector<Rank> ranks;
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    double* stage = nullptr;   // full-grid fp64 staging (shared by virtual ranks)
+    unsigned long long* stats_mx = nullptr;
+    double* stats_part = nullptr;
+    bool acc_set = false, acc_fin = false, vol_set = false, anchor_is_init = false;
+    double residue = 0.0, max_weight = 0.0;
+    int grid_s2 = 1, grid_x = 1, last_iter = 0, last_fista = 0;
+    bool result_valid = false;
+    int trace_cap = 0, theta_cap = 0;
+
+    ~DistImpl() override {
+        for (void* p : allocs) cudaFree(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    template <typename T>
+    int dalloc(T** p, size_t count) {
+        CK(cudaMalloc((void**)p, sizeof(T) * std::max<size_t>(count, 1)));
+        allocs.push_back(*p);
+        return CM_OK;
+    }
+    size_t ghosted() const { return (size_t)(NK + 2) * NN; }
+
+    int map(R* ptr, int zdim, cuuint32_t bw, cuuint32_t bj, CUtensorMap* out) {
+        EncodeTiledFn enc = encode_tiled_fn();
+        if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)zdim};
+        const cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)NN * 4};
+        const cuuint32_t box[3] = {bw, bj, 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        if (enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return fail(CM_ERR_CUDA, "tensor map encode failed");
+        return CM_OK;
+    }
+
+    int init() override {
+        P = comm->P;
+        NK = N / P;
+        NB = N / P;
+        if (N % P != 0 || NK % SG::KC != 0)
+            return fail(CM_ERR_INVALID_ARGUMENT, "z-slab decomposition needs N/P a multiple of 64");
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        std::vector<C> tw(N);
+        for (int q = 0; q < N; ++q) {
+            const double a = -2.0 * M_PI * q / N;
+            tw[q] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        ranks.resize(comm->nv);
+        for (int v = 0; v < comm->nv; ++v) {
+            Rank& k = ranks[v];
+            k.r = comm->rank0 + v;
+            k.koff = k.r * NK;
+            k.rb0 = k.r * NB;
+            for (auto& x : k.X) CKS(dalloc(&x, ghosted()));
+            CKS(dalloc(&k.x0keep, ghosted()));
+            CKS(dalloc(&k.anchor, ghosted()));
+            CKS(dalloc(&k.g, ghosted()));
+            const size_t H = (size_t)NK * N * Nh;
+            CKS(dalloc(&k.Snat, H));
+            CKS(dalloc(&k.Ssend, H));
+            CKS(dalloc(&k.Srecv, H));
+            CKS(dalloc(&k.W, (size_t)N * NB * Nh));
+            CKS(dalloc(&k.Wn, (size_t)N * NB));
+            CKS(dalloc(&k.Yh, (size_t)N * NB * Nh));
+            CKS(dalloc(&k.Yn, (size_t)N * NB));
+            CKS(dalloc(&k.Z0, (size_t)NB * N));
+            CKS(dalloc(&k.Z0full, NN));
+            CKS(dalloc(&k.twN, N));
+            CKS(dalloc(&k.part1, (size_t)std::max(SG::NTILES, 148 * 4) * NP1));
+            CKS(dalloc(&k.part3, (size_t)((Nh / ZG::TW) * NB + NB) * NP3));
+            CKS(dalloc(&k.sums, NP1 + NP3));
+            CKS(dalloc(&k.st, 1));
+            for (auto& x : k.X) CK(cudaMemsetAsync(x, 0, ghosted() * 4, stream));
+            CK(cudaMemsetAsync(k.g, 0, ghosted() * 4, stream));
+            CK(cudaMemcpyAsync(k.twN, tw.data(), sizeof(C) * N, cudaMemcpyHostToDevice, stream));
+            for (int q = 0; q < 3; ++q) {
+                CKS(map(k.X[q], NK + 2, SG::XW, SG::XR, &k.tmx[q]));
+                CKS(map(k.X[q], NK + 2, SG::XW, SG::PR, &k.tmp[q]));
+            }
+            CKS(map(k.g, NK + 2, SG::CI, SG::TJ, &k.tmg));
+            CKS(map(k.anchor, NK + 2, SG::CI, SG::TJ, &k.tma));
+        }
+        CK(cudaFuncSetAttribute(stencil2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)SG::SMEM));
+        CK(cudaFuncSetAttribute(xfft_kernel<R, N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)XG::SMEM));
+        CK(cudaFuncSetAttribute(xfft_kernel<R, N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)XG::SMEM));
+        CK(cudaFuncSetAttribute(ypass_kernel<R, N, true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(ypass_kernel<R, N, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FULL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
+        int occ = 0, sms = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2_kernel<N>, SG::NT, SG::SMEM));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        const int ntiles = SG::NTI * SG::NTJ * (NK / SG::KC);
+        grid_s2 = std::max(1, std::min(ntiles, sms * std::max(occ, 1)));
+        int occx = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, xfft_kernel<R, N, 0>, XG::NT, XG::SMEM));
+        grid_x = sms * std::max(occx, 1);
+        CK(cudaStreamSynchronize(stream));
+        return CM_OK;
+    }
+
+    // ---- data upload ---------------------------------------------------------------
+    int set_accumulator(const double* w, const double* y, int finalized) override {
+        const size_t L = NN * N;
+        if (!stage) CKS(dalloc(&stage, 3 * L));
+        if (!stats_mx) {
+            CKS(dalloc(&stats_mx, 4));
+            CKS(dalloc(&stats_part, 2 * 148 * 32));
+        }
+        CK(cudaMemcpyAsync(stage, w, 8 * L, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(stage + L, y, 16 * L, cudaMemcpyHostToDevice, stream));
+        // residue and max weight over the full grid (every process holds the whole
+        // accumulator, as the reference's BackProjector does)
+        CK(cudaMemsetAsync(stats_mx, 0, 32, stream));
+        convert_acc_kernel<R><<<grid_for(NN * (Nh + 1), 256), 256, 0, stream>>>(
+            N, stage, stage + L, nullptr, nullptr, nullptr, nullptr, stats_part, stats_mx);
+        CK(cudaGetLastError());
+        for (Rank& k : ranks) {
+            convert_rows_kernel<<<grid_for(NN * (Nh + 1) / P, 256), 256, 0, stream>>>(
+                N, k.rb0, NB, stage, stage + L, k.W, k.Wn, k.Yh, k.Yn);
+            CK(cudaGetLastError());
+        }
+        unsigned long long h[4];
+        CK(cudaMemcpyAsync(h, stats_mx, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        double worst, scale, wmax;
+        std::memcpy(&worst, &h[0], 8);
+        std::memcpy(&scale, &h[1], 8);
+        std::memcpy(&wmax, &h[2], 8);
+        residue = scale > 0.0 ? worst / scale : 0.0;
+        max_weight = wmax;
+        acc_set = true;
+        acc_fin = finalized != 0;
+        return CM_OK;
+    }
+
+    // host full volume -> this rank's ghosted planes (zero outside the grid)
+    int upload_slab(const double* host, R* dst, const Rank& k) {
+        const size_t L = NN * N;
+        if (!stage) CKS(dalloc(&stage, 3 * L));
+        CK(cudaMemsetAsync(dst, 0, ghosted() * 4, stream));
+        const int k_lo = std::max(0, k.koff - 1), k_hi = std::min(N, k.koff + NK + 1);
+        CK(cudaMemcpyAsync(stage, host + (size_t)k_lo * NN, 8 * NN * (k_hi - k_lo),
+                           cudaMemcpyHostToDevice, stream));
+        const size_t cnt = NN * (k_hi - k_lo);
+        to_real_kernel<R><<<grid_for(cnt, 256), 256, 0, stream>>>(
+            stage, dst + (size_t)(k_lo - (k.koff - 1)) * NN, cnt);
+        CK(cudaGetLastError());
+        return CM_OK;
+    }
+
+    int set_volumes(const double* xi, const double* xa) override {
+        anchor_is_init = xi == xa;
+        for (Rank& k : ranks) {
+            CKS(upload_slab(xi, k.x0keep, k));
+            CKS(upload_slab(xa, k.anchor, k));
+        }
+        CK(cudaStreamSynchronize(stream));
+        vol_set = true;
+        return CM_OK;
+    }
+
+    // ---- per-phase launches on every local rank ---------------------------------------
+    SpecLayout nat_layout() const { return {(long long)N * Nh, 0, N}; }
+    SpecLayout dm_layout() const { return {(long long)NB * Nh, (long long)NK * NB * Nh, NB}; }
+
+    int z_pass(bool fit_only, bool with_part) {
+        for (Rank& k : ranks) {
+            ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, k.twF4, k.twI4,
+                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB};
+            dim3 grid(Nh / ZG::TW, NB);
+            if (fit_only)
+                zmain_kernel<R, N, ZM_FIT><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+            else
+                zmain_kernel<R, N, ZM_FULL><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+            CK(cudaGetLastError());
+        }
+        std::vector<void*> mine, all;
+        for (Rank& k : ranks) {
+            mine.push_back(k.Z0);
+            all.push_back(k.Z0full);
+        }
+        if (comm->all_gather(mine, all, sizeof(C) * NB * N, stream))
+            return fail(CM_ERR_NCCL, "all_gather (column 0) failed");
+        const int nt = Geo<R, N>::TY < 32 ? 32 : Geo<R, N>::TY;
+        const size_t sm = sizeof(C) * 3 * N + 64 * 8;
+        for (Rank& k : ranks) {
+            ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, k.twF4, k.twI4,
+                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB};
+            if (fit_only)
+                zcol0r_kernel<N, ZM_FIT><<<NB, nt, sm, stream>>>(p, k.Z0full, k.rb0);
+            else
+                zcol0r_kernel<N, ZM_FULL><<<NB, nt, sm, stream>>>(p, k.Z0full, k.rb0);
+            CK(cudaGetLastError());
+        }
+        return CM_OK;
+    }
+    int a2a(bool forward) {  // forward: Ssend -> Srecv (z-slab -> b-slab)
+        std::vector<void*> s, r;
+        for (Rank& k : ranks) {
+            s.push_back(forward ? k.Ssend : k.Srecv);
+            r.push_back(forward ? k.Srecv : k.Ssend);
+        }
+        if (comm->all_to_all(s, r, sizeof(C) * NK * NB * Nh, stream))
+            return fail(CM_ERR_NCCL, "all_to_all failed");
+        return CM_OK;
+    }
+    int y_pass(bool fwd, bool use_st) {
+        for (Rank& k : ranks) {
+            const int* stop = use_st ? (fwd ? &k.st->done_y : &k.st->done) : nullptr;
+            YParams<R> p{fwd ? k.Snat : k.Ssend, k.twN, nullptr, stop, fwd ? k.Ssend : k.Snat,
+                         fwd ? nat_layout() : dm_layout(), fwd ? dm_layout() : nat_layout()};
+            dim3 grid(Nh / Geo<R, N>::TWY, NK);
+            if (fwd)
+                ypass_kernel<R, N, true, true>
+                    <<<grid, Geo<R, N>::TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);
+            else
+                ypass_kernel<R, N, false, true>
+                    <<<grid, Geo<R, N>::TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);
+            CK(cudaGetLastError());
+        }
+        return CM_OK;
+    }
+    int x_fft(int dir, std::vector<R*> real, bool use_st) {
+        for (size_t v = 0; v < ranks.size(); ++v) {
+            Rank& k = ranks[v];
+            const int* stop = use_st ? (dir == 0 ? &k.st->done : &k.st->done_y) : nullptr;
+            XfParams<R> p{k.Snat, real[v] + NN, k.twN, nullptr, stop, 1.0 / (double)(NN * N),
+                          NK * N};
+            const int grid = std::min(grid_x, (NK * N + XG::LPC - 1) / XG::LPC);
+            if (dir == 0)
+                xfft_kernel<R, N, 0><<<grid, XG::NT, XG::SMEM, stream>>>(p);
+            else
+                xfft_kernel<R, N, 1><<<grid, XG::NT, XG::SMEM, stream>>>(p);
+            CK(cudaGetLastError());
+        }
+        return CM_OK;
+    }
+    int halo(std::vector<R*> x) {
+        std::vector<void*> lo, hi, glo, ghi;
+        for (size_t v = 0; v < ranks.size(); ++v) {
+            lo.push_back(x[v] + NN);
+            hi.push_back(x[v] + (size_t)NK * NN);
+            glo.push_back(x[v]);
+            ghi.push_back(x[v] + (size_t)(NK + 1) * NN);
+        }
+        if (comm->halo(lo, hi, glo, ghi, 4 * NN, stream)) return fail(CM_ERR_NCCL, "halo failed");
+        return CM_OK;
+    }
+    int finalize(const FinParams& base, bool with_part3, int nb3) {
+        for (Rank& k : ranks) {
+            fin_local_kernel<<<1, 256, 0, stream>>>(base.part1 ? k.part1 : nullptr, grid_s2,
+                                                    with_part3 ? k.part3 : nullptr, nb3, k.sums);
+            CK(cudaGetLastError());
+        }
+        std::vector<double*> sums;
+        for (Rank& k : ranks) sums.push_back(k.sums);
+        if (comm->all_reduce_sum(sums, NP1 + NP3, stream))
+            return fail(CM_ERR_NCCL, "all_reduce failed");
+        for (Rank& k : ranks) {
+            FinParams f = base;
+            f.st = k.st;
+            f.trace = base.trace ? k.trace : nullptr;
+            f.sums = k.sums;
+            finalize_kernel<<<1, 256, 0, stream>>>(f);
+            CK(cudaGetLastError());
+        }
+        return CM_OK;
+    }
+
+    // ---- the solver --------------------------------------------------------------------
+    int solve(const cm_reg_config* c, cm_trace_row* trace, int cap, cm_solve_stats* stats) override {
+        CKS(validate(c));
+        if (!acc_set) return fail(CM_ERR_STATE, "accumulator not set");
+        if (!acc_fin || residue > 1e-9)
+            return fail(CM_ERR_NON_HERMITIAN, "accumulator is not Friedel-finalized");
+        if (!vol_set) return fail(CM_ERR_STATE, "volumes not set");
+        const int K = c->inner_iters;
+        const bool lipschitz = c->step_rule == 0, fista = c->momentum == 1;
+        const bool convex = c->convex_mode != 0;
+        const bool want_trace = trace && cap > 0;
+        const bool audit = !fista && (lipschitz || want_trace || c->tol_kind == 1);
+        const bool refresh_inner = c->refresh == 0 && !convex;
+        const bool wfixed = c->refresh == 1 && !convex;
+        if (wfixed && !anchor_is_init)
+            return fail(CM_ERR_UNSUPPORTED, "z-slab solver: per_m_step needs x_init == x_anchor");
+        const double max_wtv = convex ? 1.0 : 1.0 / c->eps_prime;
+        const double lr = lipschitz ? 1.0 / (2.0 * max_weight + 2.0 * c->gamma +
+                                             12.0 * c->beta * max_wtv / c->mu)
+                                    : c->fixed_step;
+        const double slack = c->audit_slack > 0.0 ? c->audit_slack : 1e-6;
+        const int tol_kind = (fista && c->tol_kind == 1) ? 2 : c->tol_kind;
+        const bool need_part1 = audit || tol_kind == 2;
+        const int nb3 = (Nh / ZG::TW) * NB + NB;
+        result_valid = false;
+
+        std::vector<double> th;
+        if (fista) {
+            th.resize(K + 1);
+            double tk = 1.0;
+            for (int q = 0; q <= K; ++q) {
+                const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * tk * tk));
+                th[q] = (tk - 1.0) / tn;
+                tk = tn;
+            }
+        }
+        const bool grow_theta = fista && theta_cap < K + 1;
+        const bool grow_trace = want_trace && trace_cap < K;
+        for (Rank& k : ranks) {
+            if (fista) {
+                for (int q = 0; q < 2; ++q) {
+                    if (!k.XF[q]) CKS(dalloc(&k.XF[q], ghosted()));
+                    if (!k.YF[q]) {
+                        CKS(dalloc(&k.YF[q], ghosted()));
+                        CK(cudaMemsetAsync(k.YF[q], 0, ghosted() * 4, stream));
+                        CKS(map(k.YF[q], NK + 2, SG::XW, SG::XR, &k.tmx[3 + q]));
+                    }
+                }
+                if (grow_theta) CKS(dalloc(&k.theta, (size_t)K + 1));
+                CK(cudaMemcpyAsync(k.theta, th.data(), 8 * (K + 1), cudaMemcpyHostToDevice, stream));
+            }
+            if (grow_trace) CKS(dalloc(&k.trace, (size_t)K * 15));
+            CK(cudaMemcpyAsync(fista ? k.XF[0] : k.X[0], k.x0keep, ghosted() * 4,
+                               cudaMemcpyDeviceToDevice, stream));
+            if (fista)
+                CK(cudaMemcpyAsync(k.YF[0], k.x0keep, ghosted() * 4, cudaMemcpyDeviceToDevice, stream));
+            if (wfixed) {
+                // frozen weights (regularizer.cpp:178-179): w_tv field of x_init once
+                if (!k.wtvf) {
+                    CKS(dalloc(&k.wtvf, ghosted()));
+                    CK(cudaMemsetAsync(k.wtvf, 0, ghosted() * 4, stream));
+                }
+                wtv_field_kernel<<<grid_for((size_t)NK * NN, 256), 256, 0, stream>>>(
+                    k.anchor, N, k.koff, NK, (float)c->eps_prime, k.wtvf);
+                CK(cudaGetLastError());
+            }
+            DevState hs{};
+            hs.max_iters = K;
+            hs.diverged_iter = -1;
+            hs.audit = audit;
+            hs.check_diverge = audit && lipschitz;
+            hs.tol_kind = tol_kind;
+            hs.fista = fista;
+            hs.refresh_inner = refresh_inner;
+            hs.tol = c->tol;
+            hs.audit_slack = slack;
+            hs.step = lr;
+            CK(cudaMemcpyAsync(k.st, &hs, sizeof(hs), cudaMemcpyHostToDevice, stream));
+        }
+        if (grow_theta) theta_cap = K + 1;
+        if (grow_trace) trace_cap = K;
+        if (wfixed) {  // the sweep reads w_tv on the ghost plane above the slab
+            std::vector<R*> wv;
+            for (Rank& k : ranks) wv.push_back(k.wtvf);
+            CKS(halo(wv));
+        }
+
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, stream));
+
+        FinParams fb{};
+        fb.nb1 = grid_s2;
+        fb.nb3 = nb3;
+        fb.alpha = c->alpha;
+        fb.beta = c->beta;
+        fb.gamma = c->gamma;
+        fb.invL = 1.0 / (double)(NN * N);
+        auto stencil = [&](int g, bool obj_only) -> int {
+            for (Rank& k : ranks) {
+                StencilParams<R> p{};
+                p.g = k.g;
+                p.st = obj_only ? nullptr : k.st;
+                p.lr = lr;
+                p.alpha = c->alpha;
+                p.beta = c->beta;
+                p.gamma = c->gamma;
+                p.eps = c->eps;
+                p.eps_prime = c->eps_prime;
+                p.mu = c->mu;
+                p.convex = convex;
+                p.audit = audit || obj_only;
+                p.fista = fista && !obj_only;
+                p.trace_full = want_trace;
+                p.steptol = tol_kind == 2 && !obj_only;
+                p.anchor = k.anchor;
+                p.part = (need_part1 || obj_only) ? k.part1 : nullptr;
+                p.koff = k.koff;
+                p.nk = NK;
+                p.zshift = 1;
+                p.obj_only = obj_only;
+                int xi, pi;
+                if (fista) {
+                    p.xcur = k.YF[g % 2];
+                    p.xold = k.XF[g % 2];
+                    p.xnext = k.XF[(g + 1) % 2];
+                    p.ynext = k.YF[(g + 1) % 2];
+                    p.theta = k.theta;
+                    xi = 3 + g % 2;
+                    pi = 0;
+                } else {
+                    p.xcur = k.X[g % 3];
+                    p.xnext = k.X[(g + 1) % 3];
+                    p.xprev = (p.audit && refresh_inner) ? k.X[(g + 2) % 3] : nullptr;
+                    xi = g % 3;
+                    pi = (g + 2) % 3;
+                }
+                if (wfixed) {
+                    p.wtvf = k.wtvf;
+                    p.wl1src = k.anchor;
+                }
+                stencil2_kernel<N><<<grid_s2, SG::NT, SG::SMEM, stream>>>(p, k.tmx[xi], k.tmp[pi],
+                                                                         k.tmg, k.tma);
+                CK(cudaGetLastError());
+            }
+            return CM_OK;
+        };
+        // the iterate whose spectrum the next z pass needs (FISTA: y_{k+1})
+        auto next_iterate = [&](int g) {
+            std::vector<R*> v;
+            for (Rank& k : ranks) v.push_back(fista ? k.YF[(g + 1) % 2] : k.X[(g + 1) % 3]);
+            return v;
+        };
+        std::vector<R*> gbufs;
+        for (Rank& k : ranks) gbufs.push_back(k.g);
+
+        // spectrum of the starting point
+        {
+            std::vector<R*> x0;
+            for (Rank& k : ranks) x0.push_back(fista ? k.YF[0] : k.X[0]);
+            CKS(x_fft(1, x0, false));
+            CKS(y_pass(true, false));
+            CKS(a2a(true));
+        }
+        int launches = 0;
+        for (int g = 0; g < K; ++g) {
+            CKS(z_pass(false, audit));               // K3 on the b rows (+ Z0 all-gather)
+            CKS(a2a(false));                         // b-slab -> z-slab
+            CKS(y_pass(false, true));                // K4
+            CKS(x_fft(0, gbufs, true));              // K1a: g
+            CKS(stencil(g, false));                  // K1b
+            const std::vector<R*> nx = next_iterate(g);
+            CKS(halo(nx));                           // ghost planes of the new iterate
+            FinParams f = fb;
+            f.part1 = need_part1 ? ranks[0].part1 : nullptr;
+            f.trace = want_trace ? ranks[0].trace : nullptr;
+            CKS(finalize(f, audit, nb3));            // FIN (local -> all-reduce -> audit)
+            CKS(x_fft(1, nx, true));                 // K1c
+            CKS(y_pass(true, true));                 // K2
+            CKS(a2a(true));                          // z-slab -> b-slab
+            launches += 9;
+            // every rank holds identical device state after the all-reduce, so
+            // every rank takes the same decision from its own copy
+            if ((g & 7) == 7 || g == K - 1) {
+                int done = 0;
+                CK(cudaMemcpyAsync(&done, &ranks[0].st->done, 4, cudaMemcpyDeviceToHost, stream));
+                CK(cudaStreamSynchronize(stream));
+                if (done) break;
+            }
+        }
+        DevState rs;
+        CK(cudaMemcpyAsync(&rs, ranks[0].st, sizeof(rs), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (audit && rs.stop_reason == 1) {
+            // close the last trace row (regularizer.cpp:208): fit(x_K) and the
+            // penalties of x_K under the weights of iteration K-1
+            CKS(z_pass(true, true));
+            CKS(stencil(rs.iter, true));
+            FinParams f = fb;
+            f.part1 = ranks[0].part1;
+            f.trace = want_trace ? ranks[0].trace : nullptr;
+            f.epilogue = 1;
+            CKS(finalize(f, true, nb3));
+            launches += 4;
+            CK(cudaMemcpyAsync(&rs, ranks[0].st, sizeof(rs), cudaMemcpyDeviceToHost, stream));
+        }
+        CK(cudaEventRecord(e1, stream));
+        CK(cudaStreamSynchronize(stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const int rows = std::min(rs.rows, want_trace ? cap : 0);
+        if (want_trace && rows > 0) {
+            std::vector<double> tr((size_t)rows * 15);
+            CK(cudaMemcpy(tr.data(), ranks[0].trace, 8 * tr.size(), cudaMemcpyDeviceToHost));
+            for (int r = 0; r < rows; ++r) {
+                std::memcpy(trace[r].before, &tr[15 * r], 56);
+                std::memcpy(trace[r].after, &tr[15 * r + 7], 56);
+                trace[r].step = tr[15 * r + 14];
+            }
+        }
+        last_iter = rs.iter;
+        last_fista = fista;
+        result_valid = rs.stop_reason != 3;
+        if (stats) {
+            stats->iterations = rs.iter;
+            stats->trace_rows = rows;
+            stats->stop_reason = rs.stop_reason;
+            stats->diverged_iter = rs.diverged_iter;
+            stats->last_rel = rs.last_rel;
+            stats->step = lr;
+            stats->solve_ms = ms;
+            stats->kernel_launches = launches * (int)ranks.size();
+        }
+        if (rs.stop_reason == 3)
+            return fail(CM_ERR_STEP_DIVERGED, "m_step: frozen-weight objective increased");
+        return CM_OK;
+    }
+
+    // this process's planes of the result into the full host volume
+    int get_volume(double* out) override {
+        if (!result_valid) return fail(CM_ERR_STATE, "no solver result resident");
+        const size_t L = NN * N;
+        if (!stage) CKS(dalloc(&stage, 3 * L));
+        for (Rank& k : ranks) {
+            const R* src = (last_fista ? k.XF[last_iter % 2] : k.X[last_iter % 3]) + NN;
+            to_double_kernel<R><<<grid_for((size_t)NK * NN, 256), 256, 0, stream>>>(
+                src, stage, (size_t)NK * NN);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(out + (size_t)k.koff * NN, stage, 8 * (size_t)NK * NN,
+                               cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        return CM_OK;
+    }
+};
+
+} // namespace cm

@@ -15,7 +15,29 @@ struct FinParams {
     double* trace;                  // [max_iters][15] or null
     double alpha, beta, gamma, invL;
     int epilogue;                   // 1: close the last row after the loop
+    const double* sums;             // z-slab ranks: globally reduced partials [NP1+NP3]
 };
+
+// z-slab ranks: this rank's partials -> out[NP1 + NP3] (then all-reduced)
+static __global__ void __launch_bounds__(256) fin_local_kernel(const double* part1, int nb1,
+                                                               const double* part3, int nb3,
+                                                               double* out) {
+    __shared__ double red[32 * (NP1 + NP3)];
+    double s[NP1 + NP3];
+#pragma unroll
+    for (int q = 0; q < NP1 + NP3; ++q) s[q] = 0.0;
+    if (part1)
+        for (int b = threadIdx.x; b < nb1; b += blockDim.x)
+#pragma unroll
+            for (int q = 0; q < NP1; ++q) s[q] += part1[(size_t)b * NP1 + q];
+    if (part3)
+        for (int b = threadIdx.x; b < nb3; b += blockDim.x)
+#pragma unroll
+            for (int q = 0; q < NP3; ++q) s[NP1 + q] += part3[(size_t)b * NP3 + q];
+    block_sum<NP1 + NP3>(s, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < NP1 + NP3; ++q) out[q] = s[q];
+}
 
 static __device__ __forceinline__ double surrogate7(const double* o) { return o[0] + o[1] + o[2] + o[4]; }
 
@@ -28,6 +50,10 @@ static __global__ void __launch_bounds__(256) finalize_kernel(FinParams p) {
     double s[NP1 + NP3];
 #pragma unroll
     for (int q = 0; q < NP1 + NP3; ++q) s[q] = 0.0;
+    if (p.sums) {  // already reduced over ranks
+        if (threadIdx.x != 0) return;
+        for (int q = 0; q < NP1 + NP3; ++q) s[q] = p.sums[q];
+    } else {
     // fixed assignment of blocks to threads + fixed tree => deterministic
     if (p.part1)
         for (int b = threadIdx.x; b < p.nb1; b += blockDim.x)
@@ -39,6 +65,7 @@ static __global__ void __launch_bounds__(256) finalize_kernel(FinParams p) {
             for (int q = 0; q < NP3; ++q) s[NP1 + q] += p.part3[(size_t)b * NP3 + q];
     block_sum<NP1 + NP3>(s, red);
     if (threadIdx.x != 0) return;
+    }
 
     const double fit = (s[NP1 + 0] - 2.0 * s[NP1 + 1]) * p.invL;
     const int i = p.epilogue ? st->max_iters : st->iter;

@@ -103,7 +103,8 @@ __global__ void convert_acc_kernel(int n, const double* __restrict__ W,
         const double wp = 0.5 * (w + wmt);
         const double sg = ((a + b + c) & 1) ? -1.0 : 1.0;
         const double pr = sg * 0.5 * (yr + mr), pi = sg * 0.5 * (yi - mi);
-        if (a < nh) {
+        if (!Wm) {  // statistics only (z-slab ranks convert their own rows)
+        } else if (a < nh) {
             const size_t o = ((size_t)c * n + b) * nh + a;
             Wm[o] = R(wp);
             Ym[o] = cx<C>(R(pr), R(pi));
@@ -463,7 +464,9 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
     int launch_y(bool fwd, DevState* s) {
-        YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr};
+        const SpecLayout nat{(long long)N * Nh, 0, N};
+        YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr,
+                     nullptr, nat, nat};
         dim3 grid(Nh / G::TWY, N);
         if (fwd)
             ypass_kernel<R, N, true><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
@@ -475,7 +478,7 @@ struct Impl final : ImplBase {
     // x-line transforms: dir 0 C2R (S -> g * invL), dir 1 R2C (real -> S)
     int launch_xfft(int dir, R* real, const int* stop) {
         using XG = XGeo<R, N>;
-        XfParams<R> p{S, real, twN, dir == 0 ? twI4 : twF4, stop, 1.0 / (double)L};
+        XfParams<R> p{S, real, twN, dir == 0 ? twI4 : twF4, stop, 1.0 / (double)L, N * N};
         const int grid = std::min(XG::NB, xfft_grid);
         if (dir == 0)
             xfft_kernel<R, N, 0><<<grid, XG::NT, XG::SMEM, stream>>>(p);
@@ -489,7 +492,7 @@ struct Impl final : ImplBase {
     template <int MODE>
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
-        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s};
+        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N};
         dim3 grid(Nh / ZG::TW, N);
         zmain_kernel<R, N, MODE><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
         CK(cudaGetLastError());
@@ -700,6 +703,9 @@ struct Impl final : ImplBase {
             p.fista = fista;
             p.trace_full = want_trace;
             p.steptol = hs.tol_kind == 2;
+            p.koff = 0;
+            p.nk = N;
+            p.zshift = 0;
             p.anchor = anchor;
             p.part = need_part1 ? part1 : nullptr;
             const CUtensorMap* tmx = nullptr;

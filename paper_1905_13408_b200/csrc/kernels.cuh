@@ -86,12 +86,27 @@ template <typename R> struct ZParams {
     DevState* st;
 };
 
+// Spectrum layout of a y pass side: element (k, b, h) at
+//   k*kstride + (b / nb)*sstride + (b % nb)*Nh + h
+// natural [k][b][h]: kstride = N*Nh, nb = N, sstride = 0; destination-major
+// [s][k][b_local][h] of a z-slab rank (the all-to-all send/receive layout):
+// kstride = nb*Nh, sstride = NK*nb*Nh.
+struct SpecLayout {
+    long long kstride, sstride;
+    int nb;
+    __device__ __forceinline__ long long at(int k, int b, int h, int Nh) const {
+        return (long long)k * kstride + (long long)(b / nb) * sstride + (long long)(b % nb) * Nh + h;
+    }
+};
+
 template <typename R> struct YParams {
     using C = Cx<R>;
-    C* S;
+    C* S;               // input spectrum
     const C* twN;
     const float4* tw4;  // packed table of the pass direction (fp32)
-    const int* stop; // &st->done (inverse pass) or &st->done_y (forward pass), or null
+    const int* stop;    // &st->done (inverse pass) or &st->done_y (forward pass), or null
+    C* Sout;            // output spectrum (may equal S), or null for in place
+    SpecLayout lin, lout;
 };
 
 template <typename C>
@@ -116,7 +131,7 @@ template <typename R> __host__ __device__ constexpr bool use_packed_tw() { retur
 // ==================================================================================
 // y pass: FFT along j for every (k, h) column. grid = (Nh/TWY, N)
 // ==================================================================================
-template <typename R, int N, bool FWD>
+template <typename R, int N, bool FWD, bool DM = false>
 __global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY)
 ypass_kernel(YParams<R> p) {
     using G = Geo<R, N>;
@@ -132,15 +147,26 @@ ypass_kernel(YParams<R> p) {
     const int t = threadIdx.x / G::TWY;
     const int h = blockIdx.x * G::TWY + col;
     const int k = blockIdx.y;
-    C* base = p.S + (size_t)k * N * G::Nh + h;
     C v[G::EY];
+    if constexpr (!DM) {  // natural layout, in place
+        C* base = p.S + (size_t)k * p.lin.kstride + h;
 #pragma unroll
-    for (int m = 0; m < G::EY; ++m) v[m] = base[(size_t)(t + G::TY * m) * G::Nh];
-    __syncthreads();
-    fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw_src<R, FWD>(tw, tw4),
-                               BlockSync{});
+        for (int m = 0; m < G::EY; ++m) v[m] = base[(size_t)(t + G::TY * m) * G::Nh];
+        __syncthreads();
+        fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw_src<R, FWD>(tw, tw4),
+                                   BlockSync{});
 #pragma unroll
-    for (int m = 0; m < G::EY; ++m) base[(size_t)(t + G::TY * m) * G::Nh] = v[m];
+        for (int m = 0; m < G::EY; ++m) base[(size_t)(t + G::TY * m) * G::Nh] = v[m];
+    } else {  // z-slab rank: natural <-> destination-major (fused all-to-all packing)
+#pragma unroll
+        for (int m = 0; m < G::EY; ++m) v[m] = p.S[p.lin.at(k, t + G::TY * m, h, G::Nh)];
+        __syncthreads();
+        fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw_src<R, FWD>(tw, tw4),
+                                   BlockSync{});
+        C* out = p.Sout ? p.Sout : p.S;
+#pragma unroll
+        for (int m = 0; m < G::EY; ++m) out[p.lout.at(k, t + G::TY * m, h, G::Nh)] = v[m];
+    }
 }
 
 // ==================================================================================

@@ -46,7 +46,7 @@ template <int N> struct S2Geo {
     static constexpr size_t OFF_BAR = OFF_RED + 32 * NP1 * 8;
     static constexpr size_t SMEM = OFF_BAR + NSTAGE * 8;
     static constexpr int NTI = N / CI, NTJ = N / TJ, NTK = N / KC;
-    static constexpr int NTILES = NTI * NTJ * NTK;
+    static constexpr int NTILES = NTI * NTJ * NTK;  // single GPU (nk = N)
 };
 
 template <int N>
@@ -86,23 +86,25 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     for (int q = 0; q < NP1; ++q) acc[q] = 0.0;
 
     uint32_t phase_bits = 0;  // parity of the next wait on each ring slot
-    for (int tile = blockIdx.x; tile < G::NTILES; tile += gridDim.x) {
+    const int koff = p.koff, zs = p.zshift;
+    const int ntiles = G::NTI * G::NTJ * (p.nk / KC);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int i0 = (tile % G::NTI) * CI;
         const int j0 = ((tile / G::NTI) % G::NTJ) * TJ;
         const int k0 = (tile / (G::NTI * G::NTJ)) * KC;
         // plane q (k0-1 .. k0+KC) lives in ring slot (q - k0 + 1) % NSTAGE
         auto slot_of = [&](int q) { return (q - k0 + 1) & (G::NSTAGE - 1); };
         auto stage = [&](int q) { return smem_raw + (size_t)slot_of(q) * G::STAGE; };
-        auto issue = [&](int q) {
-            if (q > k0 + KC || q > N) return;
+        auto issue = [&](int q) {  // q: local plane (ghost planes at -1 and nk)
+            if (q > k0 + KC) return;
             const int sl = slot_of(q);
             unsigned char* st = smem_raw + (size_t)sl * G::STAGE;
             mbar_expect_tx(&bar[sl], G::XB + (with_prev ? G::PB : 0u) + 2 * G::GB);
-            tma_load_3d(st, &tmx, i0 - 4, j0 - 1, q, &bar[sl]);
-            if (with_prev) tma_load_3d(st + G::OFF_P, &tmp, i0 - 4, j0 - 1, q, &bar[sl]);
+            tma_load_3d(st, &tmx, i0 - 4, j0 - 1, q + zs, &bar[sl]);
+            if (with_prev) tma_load_3d(st + G::OFF_P, &tmp, i0 - 4, j0 - 1, q + zs, &bar[sl]);
             // g / anchor rows of planes past the march are never read; out of grid -> 0
-            tma_load_3d(st + G::OFF_G, &tmg, i0, j0, q, &bar[sl]);
-            tma_load_3d(st + G::OFF_A, &tma, i0, j0, q, &bar[sl]);
+            tma_load_3d(st + G::OFF_G, &tmg, i0, j0, q + zs, &bar[sl]);
+            tma_load_3d(st + G::OFF_A, &tma, i0, j0, q + zs, &bar[sl]);
         };
         auto wait = [&](int q) {
             const int sl = slot_of(q);
@@ -137,12 +139,12 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             float xl = __shfl_up_sync(0xffffffffu, c4.w, 1);
             if (lane == 0) xl = xrow(q, w + 1)[-1];
             const float xlv[4] = {xl, c4.x, c4.y, c4.z};
-            const bool qin = q < N && row_in;
+            const bool qin = koff + q < N && row_in;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float d1 = (gi0 + c > 0) ? xq[c] - xlv[c] : 0.f;
                 const float d2 = (gj > 0) ? xq[c] - yv[c] : 0.f;
-                const float d3 = (q > 0) ? xq[c] - zv[c] : 0.f;
+                const float d3 = (koff + q > 0) ? xq[c] - zv[c] : 0.f;
                 const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const float mx = mu > g ? mu : g;
                 const float s = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
@@ -156,7 +158,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 const float xc = r[0];
                 const float d1 = xc - r[-1];
                 const float d2 = gj > 0 ? xc - r[-XW] : 0.f;
-                const float d3 = q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
+                const float d3 = koff + q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
                 const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const float mx = mu > g ? mu : g;
                 s_halo = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
@@ -164,9 +166,9 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         };
         // per_m_step weights come from a frozen field: s uses w_tv from it
         auto apply_wtvf = [&](int q, float (&sv)[4], float (&gn)[4], float& s_halo) {
-            if (!p.wtvf || convex || !(q < N && row_in)) return;
+            if (!p.wtvf || convex || !(koff + q < N && row_in)) return;
             const float4 wv = __ldg(reinterpret_cast<const float4*>(
-                p.wtvf + ((size_t)q * N + gj) * N + gi0));
+                p.wtvf + ((size_t)(q + zs) * N + gj) * N + gi0));
             const float wt[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -174,12 +176,12 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 sv[c] = wt[c] * rcp_(mx);
             }
             if (lane == 31 && i0 + CI < N && has_beta) {
-                const float wh = __ldg(p.wtvf + ((size_t)q * N + gj) * N + i0 + CI);
+                const float wh = __ldg(p.wtvf + ((size_t)(q + zs) * N + gj) * N + i0 + CI);
                 const float* r = xrow(q, w + 1) - ii + CI;
                 const float xc = r[0];
                 const float d1 = xc - r[-1];
                 const float d2 = gj > 0 ? xc - r[-XW] : 0.f;
-                const float d3 = q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
+                const float d3 = koff + q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
                 const float gg = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 s_halo = wh * rcp_(mu > gg ? mu : gg);
             }
@@ -220,7 +222,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             if (!halo && row_in) {
                 // ---- voxel (j, k): update, prox, partials
                 const float* Sc = Sring + (size_t)(k % 3) * (TJ + 1) * SW;
-                const size_t gidx = ((size_t)k * N + gj) * N + gi0;
+                const size_t gidx = ((size_t)(k + zs) * N + gj) * N + gi0;
                 const unsigned char* stk = stage(k);
                 const float4 g4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_G) + w * CI + ii);
                 const float4 a4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_A) + w * CI + ii);
@@ -245,7 +247,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                         float t = s_cur[c] * ds_cur[c];
                         if (gi0 + c < N - 1) t -= sxv[c] * (xn[c] - x_cur[c]);
                         if (gj < N - 1) t -= sy[c] * (yp[c] - x_cur[c]);
-                        if (k < N - 1) t -= s_nx[c] * (x_nx[c] - x_cur[c]);
+                        if (koff + k < N - 1) t -= s_nx[c] * (x_nx[c] - x_cur[c]);
                         tvg[c] = t;
                     }
                 }
@@ -293,8 +295,9 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     }
                     nx[c] = v;
                 }
-                *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
-                if (p.fista) {
+                if (!p.obj_only)
+                    *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+                if (p.fista && !p.obj_only) {
                     float y[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
@@ -323,7 +326,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                         for (int c = 0; c < 4; ++c) {
                             const float e1 = (gi0 + c > 0) ? pc[c] - pl[c] : 0.f;
                             const float e2 = gj > 0 ? pc[c] - py[c] : 0.f;
-                            const float e3 = k > 0 ? pc[c] - xp_prev[c] : 0.f;
+                            const float e3 = koff + k > 0 ? pc[c] - xp_prev[c] : 0.f;
                             const float a = fabsf(pc[c]) + eps;
                             const float b = sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp;
                             const float r = rcp_(a * b);

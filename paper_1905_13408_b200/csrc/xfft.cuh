@@ -44,6 +44,7 @@ template <typename R> struct XfParams {
     const float4* tw4;  // packed table of the transform direction (fp32)
     const int* stop;    // &st->done (C2R) / &st->done_y (R2C) or null
     double scale;
+    int nlines;         // lines to transform (N*N, or NK*N on a z-slab rank)
 };
 
 // DIR 0: C2R (S -> real * scale), DIR 1: R2C (real -> S)
@@ -65,9 +66,10 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT) xfft_kernel(XfParams<R> p) {
     const PadAddr pad{};
     const WarpSync wsync{};
     // persistent: the twiddle table is staged once per CTA
-    for (int grp = blockIdx.x; grp < X::NB; grp += gridDim.x) {
+    const int ngrp = (p.nlines + X::LPC - 1) / X::LPC;
+    for (int grp = blockIdx.x; grp < ngrp; grp += gridDim.x) {
     const int line = grp * X::LPC + lg;
-    const bool valid = (lg < X::LPC) && (line < N * N);
+    const bool valid = (lg < X::LPC) && (line < p.nlines);
     C* Srow = p.S + (size_t)(valid ? line : 0) * Nh;
     R* xrow = p.real + (size_t)(valid ? line : 0) * N;
     C v[E];

@@ -30,6 +30,7 @@ template <typename R> struct ZMParams {
     const float4* twI4;
     double* part;   // [nblocks_main + N/2 + 1][NP3]
     DevState* st;
+    int nrows;      // rows b of the spectrum block (N, or NB on a b-slab rank)
 };
 
 #ifndef CM_Z_E8
@@ -79,8 +80,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     const int col = threadIdx.x % TW;
     const int t = threadIdx.x / TW;
     const int h = blockIdx.x * TW + col;
-    const int b = blockIdx.y;
-    const size_t plane = (size_t)N * Nh;
+    const int b = blockIdx.y;  // local row
+    const size_t plane = (size_t)p.nrows * Nh;
     C* base = p.S + (size_t)b * Nh + h;
     C v[E];
 #pragma unroll
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     if constexpr (PREFETCH) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const size_t gi = ((size_t)(t + T * m) * N + b) * Nh + h;
+            const size_t gi = ((size_t)(t + T * m) * p.nrows + b) * Nh + h;
             w[m] = __ldg(p.W + gi);
             y[m] = __ldg(p.Yh + gi);
         }
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         if constexpr (!PREFETCH) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const size_t gi = ((size_t)(t + T * m) * N + b) * Nh + h;
+                const size_t gi = ((size_t)(t + T * m) * p.nrows + b) * Nh + h;
                 w[m] = __ldg(p.W + gi);
                 y[m] = p.Yh[gi];
             }

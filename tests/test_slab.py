@@ -1,0 +1,266 @@
+"""z-slab decomposition.
+
+CPU (gloo, world_size 2): the exchange pattern of csrc/dist.cuh — the
+destination-major y-pass output, the all-to-all, the z transform on b rows,
+the column-0 all-gather, the reverse transpose and the halo planes —
+executed with numpy FFTs over torch.distributed, against the full-grid
+transform. This pins SlabPlan's layout arithmetic (the same numbers the
+device code uses) without a GPU.
+
+GPU: the device z-slab solver with P ranks emulated on one B200 (exchanges
+become device copies) against the single-GPU solver and the oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1905_13408_b200 as cm
+from paper_1905_13408_b200 import synth
+from paper_1905_13408_b200.slab import SlabPlan
+
+
+# ---------------------------------------------------------------------------------------
+# host-side layout arithmetic
+# ---------------------------------------------------------------------------------------
+def test_plan_arithmetic():
+    p = SlabPlan(512, 4)
+    assert (p.nk, p.nb, p.nh) == (128, 128, 256)
+    assert p.supported()
+    assert not SlabPlan(256, 8).supported()      # 32 planes < one 64-plane march
+    assert not SlabPlan(192, 1).supported()      # 128-wide stencil tiles
+    assert list(p.planes(1)) == list(range(128, 256))
+    g = p.ghosted_planes(0)
+    assert g[0] is None and g[1] == 0 and g[-1] == 128
+    assert p.ghosted_planes(3)[-1] is None
+    assert p.halo_neighbours(0) == (None, 1) and p.halo_neighbours(3) == (2, None)
+    # destination-major: chunk s (rows of rank s) is contiguous and chunk_elems long
+    offs = sorted(p.dm_offset(k, b, h) for k in range(2) for b in range(0, 512, 128)
+                  for h in (0, 255))
+    assert p.dm_offset(0, 128, 0) == p.chunk_elems()
+    assert p.dm_offset(p.nk - 1, p.nb - 1, p.nh - 1) == p.chunk_elems() - 1
+    assert offs[0] == 0
+    with pytest.raises(cm.InvalidArgument):
+        SlabPlan(100, 3)
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _pack_half(F: np.ndarray, n: int) -> np.ndarray:
+    """rfft over x (last axis) -> packed half spectrum: column 0 = X(0) + i X(n/2)."""
+    S = F[..., : n // 2].copy()
+    S[..., 0] = F[..., 0] + 1j * F[..., n // 2]
+    return S
+
+
+def _slab_worker(rank: int, world: int, port: int, n: int, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = SlabPlan(n, world)
+        nk, nb, nh = plan.nk, plan.nb, plan.nh
+        x = np.random.default_rng(7).standard_normal((n, n, n))   # [k][j][i]
+        mine = x[plan.planes(rank)]
+        # x R2C + y forward on my planes, written destination-major
+        Fxy = np.fft.fft(np.fft.rfft(mine, axis=2), axis=1)        # [kl][b][a]
+        S = _pack_half(Fxy, n)                                      # [kl][b][h]
+        send = np.empty(world * plan.chunk_elems(), np.complex128)
+        for kl in range(nk):
+            for b in range(n):
+                o = plan.dm_offset(kl, b, 0)
+                send[o:o + nh] = S[kl, b]
+        # all-to-all: chunk s -> rank s
+        sv = torch.from_numpy(send.view(np.float64).copy())
+        rv = torch.empty_like(sv)
+        dist.all_to_all_single(rv, sv)
+        recv = rv.numpy().view(np.complex128).reshape(world * nk, nb, nh)  # [c][bl][h]
+        # z pass on my b rows
+        Z = np.fft.fft(recv, axis=0)
+        full = _pack_half(np.fft.fftn(x), n)                        # [c][b][h]
+        ok_fwd = np.allclose(Z, full[:, plan.rows(rank), :], atol=1e-9 * n ** 3)
+        # column 0 all-gather: every rank sees Z0[b][c] of the whole grid
+        z0 = torch.from_numpy(np.ascontiguousarray(Z[:, :, 0].T).view(np.float64).copy())
+        z0all = [torch.empty_like(z0) for _ in range(world)]
+        dist.all_gather(z0all, z0)
+        Z0 = np.concatenate([t.numpy().view(np.complex128) for t in z0all], axis=0)  # [b][c]
+        ok_z0 = np.allclose(Z0, full[:, :, 0].T, atol=1e-9 * n ** 3)
+        # Friedel pairing of the packed column: X(0) and X(n/2) planes per (b, c)
+        b = plan.rows(rank)[0]
+        c = np.arange(n)
+        zz, zm = Z0[b, c], Z0[(-b) % n, (-c) % n]
+        f0, fn = 0.5 * (zz + zm.conj()), (zz - zm.conj()) / 2j
+        F = np.fft.fftn(x)
+        ok_pair = np.allclose(f0, F[c, b, 0], atol=1e-9 * n ** 3) and \
+            np.allclose(fn, F[c, b, n // 2], atol=1e-9 * n ** 3)
+        # reverse transpose returns my planes
+        back = torch.empty_like(rv)
+        dist.all_to_all_single(back, rv)
+        ok_back = np.array_equal(back.numpy(), sv.numpy())
+        # halo: my last plane -> next rank's lower ghost, my first -> previous's upper
+        lo_n, hi_n = plan.halo_neighbours(rank)
+        ghost_lo = torch.zeros(n * n, dtype=torch.float64)
+        ghost_hi = torch.zeros(n * n, dtype=torch.float64)
+        reqs = []
+        if hi_n is not None:
+            reqs += [dist.isend(torch.from_numpy(mine[-1].ravel().copy()), hi_n),
+                     dist.irecv(ghost_hi, hi_n)]
+        if lo_n is not None:
+            reqs += [dist.isend(torch.from_numpy(mine[0].ravel().copy()), lo_n),
+                     dist.irecv(ghost_lo, lo_n)]
+        for r in reqs:
+            r.wait()
+        g = plan.ghosted_planes(rank)
+        ok_halo = True
+        if g[0] is not None:
+            ok_halo &= np.array_equal(ghost_lo.numpy(), x[g[0]].ravel())
+        if g[-1] is not None:
+            ok_halo &= np.array_equal(ghost_hi.numpy(), x[g[-1]].ravel())
+        q.put((rank, bool(ok_fwd), bool(ok_z0), bool(ok_pair), bool(ok_back), bool(ok_halo)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [8, 12])
+def test_slab_exchange_pattern_gloo(n):
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert all(r[1:]), r
+
+
+# ---------------------------------------------------------------------------------------
+# device solver, P ranks emulated on one GPU
+# ---------------------------------------------------------------------------------------
+MODES = {
+    "per_inner": dict(),
+    "per_m_step": dict(refresh=1),
+    "convex": dict(convex_mode=1),
+    "fixed": dict(step_rule=1),
+}
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _traces(rows):
+    return np.array([np.r_[r.before.as_array(), r.after.as_array(), r.step] for r in rows])
+
+
+def _problem(n):
+    p = synth.synthetic_problem(n)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    s = cm.scale_data(acc, precision=32)
+    return p, acc, cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,world", [(128, 2), (256, 2), (256, 4)])
+def test_slab_matches_single_gpu(n, world):
+    from paper_1905_13408_b200.slab import SlabContext
+
+    p, acc, base = _problem(n)
+    lr0 = 1.0 / (2.0 * p.weight.max() + 2.0 * base.gamma + 12.0 * base.beta / base.eps_prime / base.mu)
+    sc = SlabContext(n, world)
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0)
+    for name, extra in MODES.items():
+        cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 10, "fixed_step": 2.0 * lr0, **extra})
+        t1, t2 = [], []
+        x1 = cm.m_step(acc, p.x0, p.x0, cfg, t1, precision=32)
+        sc.solve(cfg, t2)
+        x2 = sc.get_volume()
+        a, b = _traces(t2), _traces(t1)
+        assert a.shape == b.shape, name
+        for half in (slice(0, 7), slice(7, 14)):
+            surr = np.abs(b[:, half][:, [0, 1, 2, 4]].sum(axis=1))
+            scale = np.maximum(np.abs(b[:, half]), surr[:, None])
+            assert (np.abs(a[:, half] - b[:, half]) / scale).max() <= 1e-6, name
+        assert _rel(x2, x1) <= 1e-6, (name, _rel(x2, x1))
+    sc.close()
+
+
+@pytest.mark.gpu
+def test_slab_vs_oracle_128():
+    from oracle_lib import Oracle, make_cfg
+
+    n = 128
+    p, acc, base = _problem(n)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 8})
+    trace = []
+    x = cm.slab.m_step_slab(acc, p.x0, p.x0, cfg, world=2, trace=trace)
+    c = make_cfg(alpha=cfg.alpha, beta=cfg.beta, gamma=cfg.gamma, eps=cfg.eps,
+                 eps_prime=cfg.eps_prime, mu=cfg.mu, inner_iters=8)
+    rc, xo, tro = Oracle().m_step(p.weight, p.numerator, p.x0, p.x0, c)
+    assert rc == 0
+    got = _traces(trace)
+    surr = np.abs(tro[:, 0] + tro[:, 1] + tro[:, 2] + tro[:, 4])
+    for half in (slice(0, 7), slice(7, 14)):
+        err = np.abs(got[:, half] - tro[:, half]) / np.maximum(np.abs(tro[:, half]), surr[:, None])
+        assert err.max() <= 1e-5
+    assert _rel(x, xo) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_slab_fista_tolerance_stop_matches_single_gpu():
+    from paper_1905_13408_b200.slab import SlabContext
+
+    n, world = 256, 4
+    p, acc, base = _problem(n)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 400, "momentum": 1, "tol_kind": 2,
+                          "tol": 0.05})
+    st1 = {}
+    x1 = cm.m_step(acc, p.x0, p.x0, cfg, precision=32, stats=st1)
+    sc = SlabContext(n, world)
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0)
+    st2 = sc.solve(cfg)
+    x2 = sc.get_volume()
+    assert st1["stop_reason"] == 2 and st2.stop_reason == 2
+    assert st2.iterations == st1["iterations"]
+    assert _rel(x2, x1) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_slab_errors():
+    from paper_1905_13408_b200.slab import SlabContext
+
+    with pytest.raises(cm.Error):
+        SlabContext(192, 1)            # no 128-wide tiles
+    with pytest.raises(cm.Error):
+        SlabContext(256, 8)            # 32 planes per rank
+    n = 128
+    p, acc, base = _problem(n)
+    sc = SlabContext(n, 2)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 2, "refresh": cm.Refresh.per_m_step})
+    with pytest.raises(cm.Error):
+        sc.solve(cfg)                  # accumulator not set
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0, p.x0 + 1.0)   # anchor differs: frozen weights need x_init == anchor
+    with pytest.raises(cm.Error):
+        sc.solve(cfg)
+    bad = cm.AccumulatorPair(n, p.numerator, p.weight, False)
+    with pytest.raises(cm.NonHermitianAccumulator):
+        sc.set_accumulator(bad)
+        sc.solve(cm.RegConfig(**{**base.__dict__, "inner_iters": 2}))
+    sc.close()
