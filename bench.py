@@ -10,8 +10,12 @@ iteration) over the resident 512^3 synthetic problem (synth.py).
 value = N^3 * iters * steps / device time (CUDA events), inputs resident in HBM.
 e2e   = the same through the C ABI call cm_m_step with pinned HOST buffers
         (full-grid fp64 accumulator + volume H2D, result D2H inside the timing).
-Under torchrun each rank solves its own replica (weak scaling, no data-path
-collective: SURVEY §8(e) config 5 "replicas only").
+Under torchrun (--mode auto) the same 512^3 solve is z-slab decomposed over the
+ranks (NCCL all-to-all transposes + one-plane halos; strong
+scaling); --mode replicas runs independent replicas instead (config 5).
+Every line also carries "big": the 1024^3 z-slab solve (device-rendered timing
+problem) on the same ranks, so the 1024^3 scaling can be
+read across the N=1,2,4,8 lines.
 """
 from __future__ import annotations
 
@@ -50,6 +54,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ttt", type=int, default=1, help="measure time-to-tolerance (0/1)")
     ap.add_argument("--ttt-max-iters", type=int, default=6000)
+    ap.add_argument("--mode", default="auto", choices=["auto", "single", "slab", "replicas"],
+                    help="auto: one context at N=1, z-slab decomposition under torchrun")
+    ap.add_argument("--big-n", type=int, default=1024,
+                    help="side of the device-rendered z-slab scaling run (0: skip)")
+    ap.add_argument("--big-iters", type=int, default=20)
     return ap.parse_args()
 
 
@@ -267,12 +276,188 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------------
+def broadcast_nccl_id(world, rank):
+    if world == 1:
+        return None
+    import torch.distributed as dist
+    from paper_1905_13408_b200.slab import nccl_unique_id
+
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def time_slab_solves(sc, cfg, steps, warmup, world):
+    import torch
+
+    for _ in range(warmup):
+        sc.solve(cfg)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    dev_ms, launches, st = 0.0, 0, None
+    e0.record()
+    for _ in range(steps):
+        st = sc.solve(cfg)
+        dev_ms += st.solve_ms
+        launches += st.kernel_launches
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    return allreduce_max(e0.elapsed_time(e1), world), allreduce_max(dev_ms, world), launches, st
+
+
+def big_slab(args, world, rank, local):
+    """1024^3 z-slab solve on a device-rendered problem (timing only)."""
+    import paper_1905_13408_b200 as cm
+    from paper_1905_13408_b200.slab import SlabContext, SlabPlan
+
+    n = args.big_n
+    plan = SlabPlan(n, world)
+    if not plan.supported():
+        return {"n": n, "skipped": f"{world} ranks do not tile {n}^3 into 64-plane slabs"}
+    sc = SlabContext(n, world, rank, local, broadcast_nccl_id(world, rank))
+    try:
+        sy = sc.set_synthetic(7)
+        cfg = cm.derive_config(sy, 1.5, 0.1, 0.1 / 3)
+        cfg.inner_iters = args.big_iters
+        t_ms, dev_ms, launches, st = time_slab_solves(sc, cfg, 2, 1, world)
+    finally:
+        sc.close()
+    ms_iter = t_ms / (2 * args.big_iters)
+    L = float(n) ** 3
+    hbm, _ = peaks()
+    iter_bytes = sum(kernel_bytes(n, 4, audit_prev=True).values()) / world
+    return {"n": n, "ranks": world, "iters_per_step": args.big_iters, "steps": 2,
+            "value": L * args.big_iters * 2 / (t_ms / 1e3), "unit": "voxel-iterations/s",
+            "ms_per_iter": ms_iter, "stop_reason": st.stop_reason,
+            "hbm_frac_per_gpu": iter_bytes / (ms_iter / 1e3) / 1e9 / hbm,
+            "exchange_bytes_per_rank_per_iter": plan.exchange_bytes_per_iteration(),
+            "data": "device-rendered blob lattice + random symmetric weight (timing only)"}
+
+
+def run_slab(args, world, rank, local):
+    """The 512^3 solve z-slab decomposed over the torchrun ranks (strong scaling)."""
+    import torch
+
+    import paper_1905_13408_b200 as cm
+    from paper_1905_13408_b200.slab import SlabContext, SlabPlan
+
+    n, iters = args.n, args.iters
+    t0 = time.time()
+    p = load_problem(n, rank, world)
+    gen_s = time.time() - t0
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    s = cm.scale_data(acc, precision=32)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = iters
+    plan = SlabPlan(n, world)
+    sc = SlabContext(n, world, rank, local, broadcast_nccl_id(world, rank))
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0)
+    with ClockSampler(local) as clk:
+        t_ms, dev_ms, launches, st = time_slab_solves(sc, cfg, args.steps, args.warmup, world)
+    clocks = clk.summary()
+    value = float(n) ** 3 * iters * args.steps / (t_ms / 1e3)
+    ms_iter = t_ms / (args.steps * iters)
+    hbm, peak_kind = peaks()
+    kb = kernel_bytes(n, 4, audit_prev=True)
+    iter_bytes = sum(kb.values()) / world
+    xb = plan.exchange_bytes_per_iteration()
+    roofline = {
+        "bound": "hbm", "kernel": "iteration (per GPU, z-slab)", "achieved":
+            iter_bytes / (ms_iter / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": iter_bytes / (ms_iter / 1e3) / 1e9 / hbm, "traffic": None,
+            "peak_kind": peak_kind, "algorithmic_bytes_per_iter_per_gpu": iter_bytes,
+            "exchange_bytes_per_iter_per_gpu": xb,
+            "exchange_GBps_per_gpu": xb / (ms_iter / 1e3) / 1e9}
+    # end to end through the C ABI: host accumulator + volume in, this rank's planes out
+    e2e = None
+    if not args.no_e2e:
+        L = n ** 3
+        pin_w = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
+        pin_y = torch.empty(2 * L, dtype=torch.float64, pin_memory=True).numpy()
+        pin_x = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
+        pin_o = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
+        pin_w[...] = p.weight
+        pin_y[...] = p.numerator.view(np.float64).reshape(-1)
+        pin_x[...] = p.x0
+        pacc = cm.AccumulatorPair(n, pin_y.view(np.complex128).reshape(n, n, n), pin_w, True)
+
+        def one():
+            sc.set_accumulator(pacc)
+            sc.set_volumes(pin_x)
+            sc.solve(cfg)
+            sc.get_volume(pin_o)
+
+        one()
+        barrier(world)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            one()
+        f1.record()
+        torch.cuda.synchronize()
+        e_ms = allreduce_max(f0.elapsed_time(f1), world)
+        e2e = {"value": float(n) ** 3 * iters * args.e2e_steps / (e_ms / 1e3),
+               "unit": "voxel-iterations/s", "h2d_bytes_per_step": 32 * L * world,
+               "d2h_bytes_per_step": 8 * L, "steps": args.e2e_steps,
+               "ms_per_step": e_ms / args.e2e_steps,
+               "api": "cm_dctx_set_accumulator/set_volumes/solve/get_volume (every rank uploads "
+                      "the full accumulator, downloads its planes)"}
+    ttt = None
+    if args.ttt:
+        tc = cm.RegConfig(**{**cfg.__dict__, "inner_iters": args.ttt_max_iters,
+                             "refresh": cm.Refresh.per_m_step, "momentum": 1, "tol_kind": 2,
+                             "tol": 0.03})
+        sc.set_accumulator(acc)
+        sc.set_volumes(p.x0)
+        barrier(world)
+        tst = sc.solve(tc)
+        ttt = {"fista": {"iterations": tst.iterations,
+                         "seconds": allreduce_max(tst.solve_ms, world) / 1e3,
+                         "stop_reason": tst.stop_reason,
+                         "criterion": "step norm < 3% of the largest step"}}
+    sc.close()
+    del p, acc
+    big = big_slab(args, world, rank, local) if args.big_n else None
+    if rank == 0:
+        line = {
+            "metric": "solver voxel-iterations/s (512^3 m_step, ISTA, per-inner reweighting, audit)",
+            "value": value, "unit": "voxel-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"m_step {n}^3 synthetic blob phantom, {iters} ISTA iterations "
+                                   f"per step, z-slab decomposed over {world} GPUs",
+                       "side": n, "iters_per_step": iters, "step_rule": "lipschitz",
+                       "refresh": "per_inner", "audit": True,
+                       "l2": "working set larger than the 126 MB L2; no flush needed",
+                       "parallelism": f"zslab{world}"},
+            "device_ms_solver_stream": dev_ms, "gen_seconds": gen_s,
+            "roofline": roofline, "cpu_baseline": None, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches, "time_to_tolerance": ttt, "big": big,
+        }
+        print(json.dumps(line), flush=True)
+
+
 def run_ours(args):
     import torch
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
     import paper_1905_13408_b200 as cm
+
+    mode = args.mode if args.mode != "auto" else ("single" if world == 1 else "slab")
+    if mode == "slab":
+        run_slab(args, world, rank, local)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
 
     n, iters = args.n, args.iters
     t0 = time.time()
@@ -387,6 +572,11 @@ def run_ours(args):
                                        else "frozen-weight surrogate relative decrease < 3e-7"),
                          "refresh": "per_m_step"}
 
+    big = None
+    if args.big_n:
+        del ctx
+        big = big_slab(args, world, rank, local)
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -411,7 +601,7 @@ def run_ours(args):
                        "parallelism": f"replicas{world}"},
             "device_ms_solver_stream": dev_ms, "gen_seconds": gen_s,
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": launches, "time_to_tolerance": ttt,
+            "gpu_launches": launches, "time_to_tolerance": ttt, "big": big,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -182,6 +182,11 @@ int cm_dctx_set_volumes(cm_dctx* d, const double* x_init, const double* x_anchor
 int cm_dctx_solve(cm_dctx* d, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
                   cm_solve_stats* stats);
 int cm_dctx_get_volume(cm_dctx* d, double* x_out);
+/* Timing problem rendered on the device (no host copy of
+ * a 1024^3 accumulator): a blob-lattice volume as x_init = x_anchor, a symmetric
+ * random weight W in [1, 2) and numerator W * fft3(x) (packed column zero).
+ * s_y receives the volume RMS (the derive_config input). */
+int cm_dctx_set_synthetic(cm_dctx* d, unsigned long long seed, double* s_y);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ def load() -> C.CDLL:
         "cm_dctx_set_volumes": [P, P, P],
         "cm_dctx_solve": [P, C.POINTER(cm_reg_config), P, C.c_int, C.POINTER(cm_solve_stats)],
         "cm_dctx_get_volume": [P, P],
+        "cm_dctx_set_synthetic": [P, C.c_ulonglong, _dp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

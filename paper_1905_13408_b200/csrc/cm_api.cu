@@ -348,4 +348,9 @@ int cm_dctx_get_volume(cm_dctx* d, double* x_out) {
     return d->impl->get_volume(x_out);
 }
 
+int cm_dctx_set_synthetic(cm_dctx* d, unsigned long long seed, double* s_y) {
+    DCTX_GUARD(d);
+    return d->impl->set_synthetic(seed, s_y);
+}
+
 } // extern "C"

@@ -136,6 +136,73 @@ __global__ static void wtv_field_kernel(const float* x, int n, int koff, int nk,
     }
 }
 
+// ---- device-rendered timing problem (1024^3 is rendered on
+// the device; the values are a valid Hermitian problem, the cost is data-independent)
+__device__ __forceinline__ double hash_unit(unsigned long long seed, unsigned long long i) {
+    unsigned long long z = seed * 0x9E3779B97F4A7C15ull + i + 0x632BE59BD9B4E019ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// blob lattice (period 24, sigma 3) plus uniform noise; ghost planes included
+__global__ static void synth_volume_kernel(int n, int koff, int nk, unsigned long long seed,
+                                           float* x, double* sumsq) {
+    const size_t NNl = (size_t)n * n;
+    const size_t tot = (size_t)(nk + 2) * NNl;
+    double acc = 0.0;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < tot;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(q % n), j = (int)((q / n) % n), kl = (int)(q / NNl) - 1;
+        const int k = koff + kl;
+        float v = 0.f;
+        if (k >= 0 && k < n) {
+            const float di = (float)((i % 24) - 12), dj = (float)((j % 24) - 12),
+                        dk = (float)((k % 24) - 12);
+            const float r2 = di * di + dj * dj + dk * dk;
+            const double u = hash_unit(seed, ((size_t)k * n + j) * n + i);
+            v = __expf(-r2 / 18.f) + 0.3f * (float)(u - 0.5);
+            if (kl >= 0 && kl < nk) acc += (double)v * v;
+        }
+        x[q] = v;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(sumsq, acc);
+}
+
+// W = 1 + (u(n) + u(-n))/2 on this rank's rows of the packed half spectrum
+__global__ static void synth_weight_kernel(int n, int rb0, int nrows, unsigned long long seed,
+                                           float* Wm, float* Wn) {
+    const int nh = n / 2;
+    const size_t total = (size_t)n * nrows * (nh + 1);
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(q % (nh + 1));
+        const size_t bc = q / (nh + 1);
+        const int bl = (int)(bc % nrows), c = (int)(bc / nrows);
+        const int b = rb0 + bl;
+        const int am = a ? n - a : 0, bm = b ? n - b : 0, cm_ = c ? n - c : 0;
+        const size_t i = ((size_t)c * n + b) * n + a, m = ((size_t)cm_ * n + bm) * n + am;
+        const float w = float(1.0 + 0.5 * (hash_unit(seed ^ 0xABCDull, i) + hash_unit(seed ^ 0xABCDull, m)));
+        if (a < nh) Wm[((size_t)c * nrows + bl) * nh + a] = w;
+        else Wn[(size_t)c * nrows + bl] = w;
+    }
+}
+
+// Yh = W * F (F: the spectrum of the volume, b-slab layout); packed column and
+// Nyquist plane zero (a valid Hermitian choice)
+__global__ static void synth_numerator_kernel(size_t count, int nh, const float* W, const float2* F,
+                                              float2* Yh, float2* Yn, size_t nyq) {
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < count;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const float w = W[q];
+        const float2 f = F[q];
+        Yh[q] = (q % nh) ? make_float2(w * f.x, w * f.y) : make_float2(0.f, 0.f);
+        if (q < nyq) Yn[q] = make_float2(0.f, 0.f);
+    }
+}
+
 struct DistBase {
     virtual ~DistBase() = default;
     virtual int init() = 0;
@@ -143,6 +210,7 @@ struct DistBase {
     virtual int set_volumes(const double* xi, const double* xa) = 0;
     virtual int solve(const cm_reg_config* c, cm_trace_row* tr, int cap, cm_solve_stats* st) = 0;
     virtual int get_volume(double* out) = 0;
+    virtual int set_synthetic(unsigned long long seed, double* s_y) = 0;
     std::unique_ptr<Comm> comm;
     int device = 0;
 };
@@ -256,7 +324,8 @@ struct DistImpl final : DistBase {
             const size_t H = (size_t)NK * N * Nh;
             CKS(dalloc(&k.Snat, H));
             CKS(dalloc(&k.Ssend, H));
-            CKS(dalloc(&k.Srecv, H));
+            if (P > 1) CKS(dalloc(&k.Srecv, H));
+            else k.Srecv = k.Ssend;  // one rank: the transposes are the identity
             CKS(dalloc(&k.W, (size_t)N * NB * Nh));
             CKS(dalloc(&k.Wn, (size_t)N * NB));
             CKS(dalloc(&k.Yh, (size_t)N * NB * Nh));
@@ -291,6 +360,8 @@ struct DistImpl final : DistBase {
         CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FULL>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
         CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FIT>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FWD>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
         int occ = 0, sms = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2_kernel<N>, SG::NT, SG::SMEM));
@@ -401,6 +472,7 @@ struct DistImpl final : DistBase {
         return CM_OK;
     }
     int a2a(bool forward) {  // forward: Ssend -> Srecv (z-slab -> b-slab)
+        if (P == 1) return CM_OK;
         std::vector<void*> s, r;
         for (Rank& k : ranks) {
             s.push_back(forward ? k.Ssend : k.Srecv);
@@ -711,6 +783,51 @@ struct DistImpl final : DistBase {
         }
         if (rs.stop_reason == 3)
             return fail(CM_ERR_STEP_DIVERGED, "m_step: frozen-weight objective increased");
+        return CM_OK;
+    }
+
+    int set_synthetic(unsigned long long seed, double* s_y) override {
+        double* red = nullptr;
+        CKS(dalloc(&red, ranks.size()));
+        CK(cudaMemsetAsync(red, 0, 8 * ranks.size(), stream));
+        std::vector<R*> xs;
+        for (size_t v = 0; v < ranks.size(); ++v) {
+            Rank& k = ranks[v];
+            synth_volume_kernel<<<grid_for(ghosted(), 256), 256, 0, stream>>>(N, k.koff, NK, seed,
+                                                                             k.x0keep, red + v);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(k.anchor, k.x0keep, ghosted() * 4, cudaMemcpyDeviceToDevice, stream));
+            synth_weight_kernel<<<grid_for((size_t)N * NB * (Nh + 1), 256), 256, 0, stream>>>(
+                N, k.rb0, NB, seed, k.W, k.Wn);
+            CK(cudaGetLastError());
+            xs.push_back(k.x0keep);
+        }
+        // F = fft3 of the volume through the solver's own transforms
+        CKS(x_fft(1, xs, false));
+        CKS(y_pass(true, false));
+        CKS(a2a(true));
+        for (Rank& k : ranks) {
+            ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, nullptr, nullptr,
+                          nullptr, nullptr, NB};
+            zmain_kernel<R, N, ZM_FWD><<<dim3(Nh / ZG::TW, NB), ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+            CK(cudaGetLastError());
+            const size_t cnt = (size_t)N * NB * Nh;
+            synth_numerator_kernel<<<grid_for(cnt, 256), 256, 0, stream>>>(
+                cnt, Nh, k.W, k.Srecv, k.Yh, k.Yn, (size_t)N * NB);
+            CK(cudaGetLastError());
+        }
+        std::vector<double*> rv;
+        for (size_t v = 0; v < ranks.size(); ++v) rv.push_back(red + v);
+        if (comm->all_reduce_sum(rv, 1, stream)) return fail(CM_ERR_NCCL, "all_reduce failed");
+        double h = 0.0;
+        CK(cudaMemcpyAsync(&h, red, 8, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        cudaFree(red);
+        allocs.erase(std::find(allocs.begin(), allocs.end(), (void*)red));
+        if (s_y) *s_y = std::sqrt(h / (double)(NN * N));
+        residue = 0.0;
+        max_weight = 2.0;  // bound of the generator (1 + u, u < 1)
+        acc_set = acc_fin = vol_set = anchor_is_init = true;
         return CM_OK;
     }
 

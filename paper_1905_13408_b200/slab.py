@@ -176,6 +176,12 @@ class SlabContext:
         return SolveStats(st.iterations, st.trace_rows, st.stop_reason, st.diverged_iter,
                           st.last_rel, st.step, st.solve_ms, st.kernel_launches)
 
+    def set_synthetic(self, seed: int = 1) -> float:
+        """Device-rendered timing problem (no host accumulator); returns the volume RMS."""
+        sy = C.c_double()
+        _check(self.lib.cm_dctx_set_synthetic(self.ptr, C.c_ulonglong(seed), C.byref(sy)))
+        return sy.value
+
     def get_volume(self, out: np.ndarray | None = None) -> np.ndarray:
         """Full-size array with this process's planes filled (others untouched)."""
         if out is None:

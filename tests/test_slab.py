@@ -167,6 +167,16 @@ def _traces(rows):
     return np.array([np.r_[r.before.as_array(), r.after.as_array(), r.step] for r in rows])
 
 
+def _check_traces(a, b, tol, what=""):
+    """Objective fields relative to max(|field|, |surrogate|) (test_gpu_parity.check_trace)."""
+    assert a.shape == b.shape, what
+    for half in (slice(0, 7), slice(7, 14)):
+        surr = np.abs(b[:, half][:, [0, 1, 2, 4]].sum(axis=1))
+        scale = np.maximum(np.abs(b[:, half]), surr[:, None])
+        assert (np.abs(a[:, half] - b[:, half]) / scale).max() <= tol, what
+    np.testing.assert_allclose(a[:, 14], b[:, 14], rtol=1e-12)
+
+
 def _problem(n):
     p = synth.synthetic_problem(n)
     acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
@@ -190,12 +200,7 @@ def test_slab_matches_single_gpu(n, world):
         x1 = cm.m_step(acc, p.x0, p.x0, cfg, t1, precision=32)
         sc.solve(cfg, t2)
         x2 = sc.get_volume()
-        a, b = _traces(t2), _traces(t1)
-        assert a.shape == b.shape, name
-        for half in (slice(0, 7), slice(7, 14)):
-            surr = np.abs(b[:, half][:, [0, 1, 2, 4]].sum(axis=1))
-            scale = np.maximum(np.abs(b[:, half]), surr[:, None])
-            assert (np.abs(a[:, half] - b[:, half]) / scale).max() <= 1e-6, name
+        _check_traces(_traces(t2), _traces(t1), 1e-6, name)
         assert _rel(x2, x1) <= 1e-6, (name, _rel(x2, x1))
     sc.close()
 
@@ -264,3 +269,46 @@ def test_slab_errors():
         sc.set_accumulator(bad)
         sc.solve(cm.RegConfig(**{**base.__dict__, "inner_iters": 2}))
     sc.close()
+
+
+@pytest.mark.gpu
+def test_slab_nccl_single_rank_matches_single_gpu():
+    """The NCCL communicator (dlopen'd libnccl) at world size 1: init, all-gather,
+    all-reduce on the solver stream."""
+    from paper_1905_13408_b200.slab import SlabContext, nccl_unique_id
+
+    n = 128
+    p, acc, base = _problem(n)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 10})
+    t1, t2 = [], []
+    x1 = cm.m_step(acc, p.x0, p.x0, cfg, t1, precision=32)
+    sc = SlabContext(n, 1, 0, 0, nccl_unique_id())
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0)
+    sc.solve(cfg, t2)
+    x2 = sc.get_volume()
+    sc.close()
+    assert _rel(x2, x1) <= 1e-6
+    _check_traces(_traces(t2), _traces(t1), 1e-6)  # partial sums regrouped per rank
+
+
+@pytest.mark.gpu
+def test_slab_synthetic_problem_is_decomposition_independent():
+    """The device-rendered timing problem (bench 'big' runs) gives the same solve on
+    1 and 4 ranks."""
+    from paper_1905_13408_b200.slab import SlabContext
+
+    n = 256
+    out = []
+    for world in (1, 4):
+        sc = SlabContext(n, world)
+        sy = sc.set_synthetic(7)
+        cfg = cm.derive_config(sy, 1.5, 0.1, 0.1 / 3)
+        cfg.inner_iters = 12
+        st = sc.solve(cfg)
+        assert st.stop_reason == 1 and st.iterations == 12
+        out.append((sy, sc.get_volume()))
+        sc.close()
+    assert abs(out[0][0] - out[1][0]) <= 1e-12 * out[0][0]
+    assert np.isfinite(out[0][1]).all()
+    assert _rel(out[1][1], out[0][1]) <= 1e-6
