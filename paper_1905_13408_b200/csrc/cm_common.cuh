@@ -97,6 +97,17 @@ struct DevState {
     double step_max;    // largest ||x_{k+1} - x_k|| seen (tol_kind 2 normaliser)
 };
 
+// a value the compiler cannot see through (forces recomputation of addresses
+// derived from it instead of keeping them live in registers)
+template <typename T> __device__ __forceinline__ T* opaque(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
+__device__ __forceinline__ size_t opaque(size_t v) {
+    asm volatile("" : "+l"(v));
+    return v;
+}
+
 __device__ __forceinline__ int ld_done(const DevState* st) {
     return *((volatile const int*)&st->done);
 }

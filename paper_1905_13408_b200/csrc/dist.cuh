@@ -357,11 +357,11 @@ struct DistImpl final : DistBase {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(ypass_kernel<R, N, false, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FULL>,
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FULL, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
-        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FIT>,
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FIT, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
-        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FWD>,
+        CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FWD, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
         int occ = 0, sms = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2_kernel<N>, SG::NT, SG::SMEM));
@@ -437,8 +437,8 @@ struct DistImpl final : DistBase {
     }
 
     // ---- per-phase launches on every local rank ---------------------------------------
-    SpecLayout nat_layout() const { return {(long long)N * Nh, 0, N}; }
-    SpecLayout dm_layout() const { return {(long long)NB * Nh, (long long)NK * NB * Nh, NB}; }
+    SpecLayout nat_layout() const { return spec_layout((long long)N * Nh, 0, N); }
+    SpecLayout dm_layout() const { return spec_layout((long long)NB * Nh, (long long)NK * NB * Nh, NB); }
 
     int z_pass(bool fit_only, bool with_part) {
         for (Rank& k : ranks) {
@@ -446,9 +446,9 @@ struct DistImpl final : DistBase {
                           with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB};
             dim3 grid(Nh / ZG::TW, NB);
             if (fit_only)
-                zmain_kernel<R, N, ZM_FIT><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+                zmain_kernel<R, N, ZM_FIT, 0><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
             else
-                zmain_kernel<R, N, ZM_FULL><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+                zmain_kernel<R, N, ZM_FULL, 0><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
             CK(cudaGetLastError());
         }
         std::vector<void*> mine, all;
@@ -809,7 +809,7 @@ struct DistImpl final : DistBase {
         for (Rank& k : ranks) {
             ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, nullptr, nullptr,
                           nullptr, nullptr, NB};
-            zmain_kernel<R, N, ZM_FWD><<<dim3(Nh / ZG::TW, NB), ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+            zmain_kernel<R, N, ZM_FWD, 0><<<dim3(Nh / ZG::TW, NB), ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
             CK(cudaGetLastError());
             const size_t cnt = (size_t)N * NB * Nh;
             synth_numerator_kernel<<<grid_for(cnt, 256), 256, 0, stream>>>(

@@ -464,7 +464,7 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
     int launch_y(bool fwd, DevState* s) {
-        const SpecLayout nat{(long long)N * Nh, 0, N};
+        const SpecLayout nat = spec_layout((long long)N * Nh, 0, N);
         YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr,
                      nullptr, nat, nat};
         dim3 grid(Nh / G::TWY, N);

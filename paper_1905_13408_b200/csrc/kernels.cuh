@@ -94,10 +94,16 @@ template <typename R> struct ZParams {
 struct SpecLayout {
     long long kstride, sstride;
     int nb;
+    float inv_nb;  // 1/nb: b = s nb + b_local without an integer division
     __device__ __forceinline__ long long at(int k, int b, int h, int Nh) const {
-        return (long long)k * kstride + (long long)(b / nb) * sstride + (long long)(b % nb) * Nh + h;
+        // exact: (b + 1/2)/nb is at least 1/(2 nb) away from an integer, b < 2^12
+        const int s = __float2int_rz(((float)b + 0.5f) * inv_nb);
+        return (long long)k * kstride + (long long)s * sstride + (long long)(b - s * nb) * Nh + h;
     }
 };
+inline SpecLayout spec_layout(long long kstride, long long sstride, int nb) {
+    return {kstride, sstride, nb, 1.0f / (float)nb};
+}
 
 template <typename R> struct YParams {
     using C = Cx<R>;

@@ -18,6 +18,9 @@ namespace cm {
 #ifndef CM_XFFT_E16
 #define CM_XFFT_E16 1
 #endif
+#ifndef CM_XFFT_MINB
+#define CM_XFFT_MINB 0
+#endif
 
 // x lines favour fewer, wider stages (radix-16): one exchange for 256 points
 __host__ __device__ constexpr int xelems_for(int LEN) {
@@ -34,6 +37,8 @@ template <typename R, int N> struct XGeo {
     static constexpr int PADX = (Nh + (Nh >> 3) + 2) / 2 * 2;
     static constexpr size_t SMEM = sizeof(Cx<R>) * (N + (size_t)LPCB * PADX) + packed_tw_bytes<R>(N, 1);
     static constexpr int NB = (N * N + LPC - 1) / LPC;
+    // resident CTAs per SM the register budget must allow (>= 24 warps per SM)
+    static constexpr int MINB = (CM_XFFT_MINB > 0) ? CM_XFFT_MINB : (NT <= 256 && sizeof(R) == 4 ? 3 : 1);
 };
 
 template <typename R> struct XfParams {
@@ -49,7 +54,7 @@ template <typename R> struct XfParams {
 
 // DIR 0: C2R (S -> real * scale), DIR 1: R2C (real -> S)
 template <typename R, int N, int DIR>
-__global__ void __launch_bounds__(XGeo<R, N>::NT) xfft_kernel(XfParams<R> p) {
+__global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(XfParams<R> p) {
     using X = XGeo<R, N>;
     using C = Cx<R>;
     constexpr int Nh = X::Nh, E = X::E, T = X::T;

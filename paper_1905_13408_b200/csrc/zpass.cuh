@@ -36,13 +36,20 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_E8
 #define CM_Z_E8 1
 #endif
+#ifndef CM_Z_E16
+#define CM_Z_E16 1
+#endif
 
 template <typename R, int N> struct ZGeo {
     // 8 elements per thread for power-of-two sides >= 256 so that W and Yh of
     // the whole column fit in registers next to it (prefetched before the
     // forward FFT); other sides keep the y-pass plan
     static constexpr bool E8 = CM_Z_E8 && N >= 256 && (N & (N - 1)) == 0 && sizeof(R) == 4;
-    static constexpr int E = E8 ? 8 : Geo<R, N>::EY;
+    // N >= 1024: 16 elements per thread so that a CTA still covers 16 columns
+    // (128-byte row segments); W and Yh are then loaded after the forward FFT
+    static constexpr bool E16 = CM_Z_E16 && E8 && N >= 1024;
+    static constexpr bool PREFETCH = E8 && !E16;
+    static constexpr int E = E16 ? 16 : E8 ? 8 : Geo<R, N>::EY;
     static constexpr int T = N / E;
     static constexpr int TW = E8 ? (16 < 1024 / T ? 16 : 1024 / T) : Geo<R, N>::TWY;
     static constexpr int NT = TW * T;
@@ -55,7 +62,8 @@ template <typename R, int N> struct ZGeo {
         sizeof(Cx<R>) * (N + 5 * (size_t)N) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 1);
 };
 
-template <typename R, int N, int MODE>
+// NR: rows of the spectrum block at compile time (N on one GPU), 0 = p.nrows (b-slab)
+template <typename R, int N, int MODE, int NR = N>
 __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel(ZMParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
@@ -81,7 +89,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     const int t = threadIdx.x / TW;
     const int h = blockIdx.x * TW + col;
     const int b = blockIdx.y;  // local row
-    const size_t plane = (size_t)p.nrows * Nh;
+    const int nrows = NR ? NR : p.nrows;
+    const size_t plane = (size_t)nrows * Nh;
     C* base = p.S + (size_t)b * Nh + h;
     C v[E];
 #pragma unroll
@@ -90,11 +99,11 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     // plan they are loaded now and land while the forward FFT runs
     R w[E];
     C y[E];
-    constexpr bool PREFETCH = ZGeo<R, N>::E8 && MODE != ZM_FWD;
+    constexpr bool PREFETCH = ZGeo<R, N>::PREFETCH && MODE != ZM_FWD;
     if constexpr (PREFETCH) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const size_t gi = ((size_t)(t + T * m) * p.nrows + b) * Nh + h;
+            const size_t gi = ((size_t)(t + T * m) * nrows + b) * Nh + h;
             w[m] = __ldg(p.W + gi);
             y[m] = __ldg(p.Yh + gi);
         }
@@ -102,29 +111,39 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     __syncthreads();
     fft_regs<N, E, N, true>(v, t, buf, ColAddr{TW, col}, tw_src<R, true>(tw, twF), BlockSync{});
     if constexpr (MODE == ZM_FWD) {
+        C* const sbase = opaque(base);
+        const size_t splane = opaque(plane);
 #pragma unroll
-        for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
+        for (int m = 0; m < E; ++m) sbase[(size_t)(t + T * m) * splane] = v[m];
         return;
     }
     R quad = R(0), cross = R(0);
+    const size_t lplane = opaque(plane);
     if (h == 0) {
 #pragma unroll
         for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
     } else {
-        if constexpr (!PREFETCH) {
+        // without the prefetch, W and Yh are consumed in groups of G (a compiler
+        // fence between groups bounds the registers held by loads in flight)
+        constexpr int G = (PREFETCH || E % 8 != 0) ? E : 8;
 #pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const size_t gi = ((size_t)(t + T * m) * p.nrows + b) * Nh + h;
-                w[m] = __ldg(p.W + gi);
-                y[m] = p.Yh[gi];
+        for (int g0 = 0; g0 < E; g0 += G) {
+            if constexpr (!PREFETCH) {
+#pragma unroll
+                for (int m = g0; m < g0 + G; ++m) {
+                    const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * Nh + h;
+                    w[m] = __ldg(p.W + gi);
+                    y[m] = p.Yh[gi];
+                }
             }
-        }
 #pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const C f = v[m];
-            quad += w[m] * (f.x * f.x + f.y * f.y);
-            cross += y[m].x * f.x + y[m].y * f.y;
-            v[m] = cx<C>(w[m] * f.x - y[m].x, w[m] * f.y - y[m].y);
+            for (int m = g0; m < g0 + G; ++m) {
+                const C f = v[m];
+                quad += w[m] * (f.x * f.x + f.y * f.y);
+                cross += y[m].x * f.x + y[m].y * f.y;
+                v[m] = cx<C>(w[m] * f.x - y[m].x, w[m] * f.y - y[m].y);
+            }
+            if constexpr (!PREFETCH) asm volatile("" ::: "memory");
         }
     }
     if (p.part) {
@@ -139,9 +158,13 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     if constexpr (MODE == ZM_FIT) return;
     __syncthreads();
     fft_regs<N, E, N, false>(v, t, buf, ColAddr{TW, col}, tw_src<R, false>(tw, twI), BlockSync{});
+    // recompute the store addresses here instead of holding E 64-bit addresses
+    // live across the transforms (register pressure at 64 registers per thread)
+    C* const sbase = opaque(base);
+    const size_t splane = opaque(plane);
     if (h != 0)
 #pragma unroll
-        for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
+        for (int m = 0; m < E; ++m) sbase[(size_t)(t + T * m) * splane] = v[m];
 }
 
 template <typename R, int N, int MODE>
