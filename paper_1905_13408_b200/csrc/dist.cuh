@@ -347,8 +347,7 @@ struct DistImpl final : DistBase {
             CKS(map(k.g, NK + 2, SG::CI, SG::TJ, &k.tmg));
             CKS(map(k.anchor, NK + 2, SG::CI, SG::TJ, &k.tma));
         }
-        CK(cudaFuncSetAttribute(stencil2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)SG::SMEM));
+        CK(stencil2_prepare<N>());
         CK(cudaFuncSetAttribute(xfft_kernel<R, N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)XG::SMEM));
         CK(cudaFuncSetAttribute(xfft_kernel<R, N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -364,7 +363,7 @@ struct DistImpl final : DistBase {
         CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FWD, 0>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ZG::SMEM_MAIN));
         int occ = 0, sms = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2_kernel<N>, SG::NT, SG::SMEM));
+        CK(stencil2_occupancy<N>(&occ));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         const int ntiles = SG::NTI * SG::NTJ * (NK / SG::KC);
         grid_s2 = std::max(1, std::min(ntiles, sms * std::max(occ, 1)));
@@ -687,9 +686,7 @@ struct DistImpl final : DistBase {
                     p.wtvf = k.wtvf;
                     p.wl1src = k.anchor;
                 }
-                stencil2_kernel<N><<<grid_s2, SG::NT, SG::SMEM, stream>>>(p, k.tmx[xi], k.tmp[pi],
-                                                                         k.tmg, k.tma);
-                CK(cudaGetLastError());
+                CK(stencil2_launch<N>(p, grid_s2, stream, k.tmx[xi], k.tmp[pi], k.tmg, k.tma));
             }
             return CM_OK;
         };

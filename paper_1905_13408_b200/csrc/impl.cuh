@@ -388,11 +388,9 @@ struct Impl final : ImplBase {
             for (int q = 0; q < 3; ++q) CKS(make_maps2(q, X[q]));
             CKS(make_map_box(gbuf, &tm2_g, SG::CI, SG::TJ, 1));
             CKS(make_map_box(anchor, &tm2_a, SG::CI, SG::TJ, 1));
-            CK(cudaFuncSetAttribute(stencil2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)SG::SMEM));
+            CK(stencil2_prepare<N>());
             int occ2 = 0, dev2 = 0, sms2 = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, stencil2_kernel<N>, SG::NT,
-                                                             SG::SMEM));
+            CK(stencil2_occupancy<N>(&occ2));
             CK(cudaGetDevice(&dev2));
             CK(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2));
             s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
@@ -737,8 +735,7 @@ struct Impl final : ImplBase {
                 if (use_s2) {
                     const int xi = fista ? 3 + g % 2 : g % 3;
                     const int pi = fista ? 0 : (g + 2) % 3;
-                    stencil2_kernel<N><<<s2_grid, S2Geo<N>::NT, S2Geo<N>::SMEM, stream>>>(
-                        p, tm2_x[xi], tm2_p[pi], tm2_g, tm2_a);
+                    CK(stencil2_launch<N>(p, s2_grid, stream, tm2_x[xi], tm2_p[pi], tm2_g, tm2_a));
                 }
             }
             if (!use_s2)

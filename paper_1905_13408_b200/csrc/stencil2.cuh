@@ -49,12 +49,32 @@ template <int N> struct S2Geo {
     static constexpr int NTILES = NTI * NTJ * NTK;  // single GPU (nk = N)
 };
 
-template <int N>
-__global__ void __launch_bounds__(S2Geo<N>::NT, 2)
+#ifdef CM_S2_MAXREG
+#define CM_S2_BOUNDS __maxnreg__(CM_S2_MAXREG)
+#else
+#define CM_S2_BOUNDS __launch_bounds__(S2Geo<N>::NT, 2)
+#endif
+
+// compile-time mode of a sweep: dead terms, branches and accumulators vanish
+enum S2Flags { S2_AUDIT = 1, S2_PREV = 2, S2_TRACE = 4, S2_STEP = 8, S2_FISTA = 16 };
+
+// partial-sum slots a mode produces (kernels.cuh NP1 layout)
+__host__ __device__ constexpr unsigned s2_used(int F) {
+    return ((F & S2_AUDIT) ? (1u | 2u | 32u | ((F & S2_PREV) ? 64u | 128u : 0u) |
+                              ((F & S2_TRACE) ? 4u | 8u | 16u | ((F & S2_PREV) ? 256u : 0u) : 0u))
+                           : 0u) |
+           ((F & S2_STEP) ? 512u | 1024u : 0u);
+}
+
+template <int N, int F>
+__global__ void CM_S2_BOUNDS
 stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmg,
                 const __grid_constant__ CUtensorMap tma) {
     using G = S2Geo<N>;
+    constexpr bool AUDIT = F & S2_AUDIT, PREV = AUDIT && (F & S2_PREV);
+    constexpr bool TRACE = AUDIT && (F & S2_TRACE), STEP = F & S2_STEP, FISTA = F & S2_FISTA;
+    constexpr unsigned USED = s2_used(F);
     constexpr int CI = G::CI, TJ = G::TJ, KC = G::KC, XW = G::XW, SW = G::SW;
     if (p.st && ld_done(p.st)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -68,22 +88,22 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     const float lr = float(p.lr), lra = float(p.lr * p.alpha), beta = float(p.beta);
     const float g2 = float(2.0 * p.gamma), inv2mu = float(0.5 / p.mu), hmu = float(0.5 * p.mu);
     const bool has_beta = p.beta > 0.0, has_alpha = p.alpha > 0.0;
-    const bool with_prev = p.audit && p.xprev;
+    constexpr bool with_prev = PREV;
     const bool convex = p.convex != 0;
-    const float theta = (p.fista && p.st) ? float(p.theta[p.st->iter]) : 0.f;
+    const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter]) : 0.f;
 
     if (tid == 0) {
         for (int q = 0; q < G::NSTAGE; ++q) mbar_init(&bar[q], 1);
         mbar_fence_init();
     }
+    // per-warp fp64 partial sums of the CTA's tiles (no fp64 registers held)
+    for (int q = tid; q < 32 * NP1; q += blockDim.x) red[q] = 0.0;
     __syncthreads();
 
-    float fa[NP1];
+    // fp32 partials: fa over 8 planes, fb over the tile, then fp64 per warp
+    float fa[NP1], fb[NP1];
 #pragma unroll
-    for (int q = 0; q < NP1; ++q) fa[q] = 0.f;
-    double acc[NP1];
-#pragma unroll
-    for (int q = 0; q < NP1; ++q) acc[q] = 0.0;
+    for (int q = 0; q < NP1; ++q) fa[q] = fb[q] = 0.f;
 
     uint32_t phase_bits = 0;  // parity of the next wait on each ring slot
     const int koff = p.koff, zs = p.zshift;
@@ -123,6 +143,11 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         const int ii = 4 * lane;
         const int gi0 = i0 + ii;
         const bool row_in = gj < N;
+        // replicate boundary (gradient.cpp:7-24): the backward neighbour of the
+        // first row / column / plane is the voxel itself, so D = 0 there without
+        // a per-voxel test; forward terms vanish because s = 0 outside the grid
+        const int ry = gj > 0 ? w : w + 1;     // slab row of j-1
+        const bool xlo = (i0 == 0);
         // x slab row r (global j0 - 1 + r) of plane q, at this lane's 4 voxels
         auto xrow = [&](int q, int r) -> const float* {
             return reinterpret_cast<const float*>(stage(q)) + r * XW + 4 + ii;
@@ -131,20 +156,19 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         // returns s[4], plus |Dx|, d-sum for the voxels; halo column (i0+CI) via lane 31
         auto s_row = [&](int q, float (&xq)[4], float (&sv)[4], float (&gn)[4], float (&ds)[4],
                          float& s_halo) {
-            const float4 c4 = ld4(xrow(q, w + 1));
-            const float4 y4 = ld4(xrow(q, w));
-            const float4 z4 = ld4(xrow(q - 1, w + 1));
+            const float* xr = xrow(q, w + 1);
+            const float* yr = xrow(q, ry);
+            const float* zr = koff + q > 0 ? xrow(q - 1, w + 1) : xr;
+            const float4 c4 = ld4(xr), y4 = ld4(yr), z4 = ld4(zr);
             xq[0] = c4.x; xq[1] = c4.y; xq[2] = c4.z; xq[3] = c4.w;
             const float yv[4] = {y4.x, y4.y, y4.z, y4.w}, zv[4] = {z4.x, z4.y, z4.z, z4.w};
             float xl = __shfl_up_sync(0xffffffffu, c4.w, 1);
-            if (lane == 0) xl = xrow(q, w + 1)[-1];
+            if (lane == 0) xl = xlo ? c4.x : xr[-1];
             const float xlv[4] = {xl, c4.x, c4.y, c4.z};
             const bool qin = koff + q < N && row_in;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const float d1 = (gi0 + c > 0) ? xq[c] - xlv[c] : 0.f;
-                const float d2 = (gj > 0) ? xq[c] - yv[c] : 0.f;
-                const float d3 = (koff + q > 0) ? xq[c] - zv[c] : 0.f;
+                const float d1 = xq[c] - xlv[c], d2 = xq[c] - yv[c], d3 = xq[c] - zv[c];
                 const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const float mx = mu > g ? mu : g;
                 const float s = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
@@ -154,11 +178,10 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             }
             s_halo = 0.f;
             if (lane == 31 && has_beta && qin && i0 + CI < N) {  // s at x = i0 + CI
-                const float* r = xrow(q, w + 1) - ii + CI;
-                const float xc = r[0];
-                const float d1 = xc - r[-1];
-                const float d2 = gj > 0 ? xc - r[-XW] : 0.f;
-                const float d3 = koff + q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
+                const float xc = xr[CI - ii];
+                const float d1 = xc - xr[CI - ii - 1];
+                const float d2 = xc - yr[CI - ii];
+                const float d3 = xc - zr[CI - ii];
                 const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const float mx = mu > g ? mu : g;
                 s_halo = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
@@ -177,11 +200,13 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             }
             if (lane == 31 && i0 + CI < N && has_beta) {
                 const float wh = __ldg(p.wtvf + ((size_t)(q + zs) * N + gj) * N + i0 + CI);
-                const float* r = xrow(q, w + 1) - ii + CI;
-                const float xc = r[0];
-                const float d1 = xc - r[-1];
-                const float d2 = gj > 0 ? xc - r[-XW] : 0.f;
-                const float d3 = koff + q > 0 ? xc - xrow(q - 1, w + 1)[CI - ii] : 0.f;
+                const float* xr = xrow(q, w + 1);
+                const float* yr = xrow(q, ry);
+                const float* zr = koff + q > 0 ? xrow(q - 1, w + 1) : xr;
+                const float xc = xr[CI - ii];
+                const float d1 = xc - xr[CI - ii - 1];
+                const float d2 = xc - yr[CI - ii];
+                const float d3 = xc - zr[CI - ii];
                 const float gg = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 s_halo = wh * rcp_(mu > gg ? mu : gg);
             }
@@ -199,8 +224,9 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         }
         float xp_prev[4] = {0.f, 0.f, 0.f, 0.f};
         if (with_prev && !halo) {
-            const float4 v = ld4(reinterpret_cast<const float*>(stage(k0 - 1) + G::OFF_P) +
-                                 (w + 1) * XW + 4 + ii);
+            // plane k0-1 of x_prev (the plane itself at the global first plane)
+            const float4 v = ld4(reinterpret_cast<const float*>(stage(koff + k0 > 0 ? k0 - 1 : k0) +
+                                                                G::OFF_P) + (w + 1) * XW + 4 + ii);
             xp_prev[0] = v.x; xp_prev[1] = v.y; xp_prev[2] = v.z; xp_prev[3] = v.w;
         }
         __syncthreads();
@@ -243,13 +269,9 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     const float yp[4] = {yp4.x, yp4.y, yp4.z, yp4.w};
                     const float sy[4] = {sy4.x, sy4.y, sy4.z, sy4.w};
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        float t = s_cur[c] * ds_cur[c];
-                        if (gi0 + c < N - 1) t -= sxv[c] * (xn[c] - x_cur[c]);
-                        if (gj < N - 1) t -= sy[c] * (yp[c] - x_cur[c]);
-                        if (koff + k < N - 1) t -= s_nx[c] * (x_nx[c] - x_cur[c]);
-                        tvg[c] = t;
-                    }
+                    for (int c = 0; c < 4; ++c)
+                        tvg[c] = s_cur[c] * ds_cur[c] - sxv[c] * (xn[c] - x_cur[c]) -
+                                 sy[c] * (yp[c] - x_cur[c]) - s_nx[c] * (x_nx[c] - x_cur[c]);
                 }
                 float wl1[4] = {1.f, 1.f, 1.f, 1.f}, wtv[4] = {1.f, 1.f, 1.f, 1.f};
                 if (!convex) {
@@ -279,7 +301,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     }
                 }
                 float base[4] = {x_cur[0], x_cur[1], x_cur[2], x_cur[3]};
-                if (p.fista) {
+                if (FISTA) {
                     const float4 o4 = __ldg(reinterpret_cast<const float4*>(p.xold + gidx));
                     base[0] = o4.x; base[1] = o4.y; base[2] = o4.z; base[3] = o4.w;
                 }
@@ -297,13 +319,13 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 }
                 if (!p.obj_only)
                     *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
-                if (p.fista && !p.obj_only) {
+                if (FISTA && !p.obj_only) {
                     float y[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
                     *reinterpret_cast<float4*>(p.ynext + gidx) = make_float4(y[0], y[1], y[2], y[3]);
                 }
-                if (p.steptol) {
+                if (STEP) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         const float dx = nx[c] - base[c];
@@ -311,22 +333,20 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                         fa[10] += nx[c] * nx[c];
                     }
                 }
-                if (p.audit) {
+                if (AUDIT) {
                     float pl1[4] = {0.f, 0.f, 0.f, 0.f}, ptv[4] = {0.f, 0.f, 0.f, 0.f};
                     if (with_prev) {
                         const float* P = reinterpret_cast<const float*>(stk + G::OFF_P);
                         const float4 pc4 = ld4(P + (w + 1) * XW + 4 + ii);
-                        const float4 py4 = ld4(P + w * XW + 4 + ii);
+                        const float4 py4 = ld4(P + ry * XW + 4 + ii);
                         float pm = __shfl_up_sync(0xffffffffu, pc4.w, 1);
-                        if (lane == 0) pm = P[(w + 1) * XW + 3];
+                        if (lane == 0) pm = xlo ? pc4.x : P[(w + 1) * XW + 3];
                         const float pc[4] = {pc4.x, pc4.y, pc4.z, pc4.w};
                         const float pl[4] = {pm, pc4.x, pc4.y, pc4.z};
                         const float py[4] = {py4.x, py4.y, py4.z, py4.w};
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            const float e1 = (gi0 + c > 0) ? pc[c] - pl[c] : 0.f;
-                            const float e2 = gj > 0 ? pc[c] - py[c] : 0.f;
-                            const float e3 = koff + k > 0 ? pc[c] - xp_prev[c] : 0.f;
+                            const float e1 = pc[c] - pl[c], e2 = pc[c] - py[c], e3 = pc[c] - xp_prev[c];
                             const float a = fabsf(pc[c]) + eps;
                             const float b = sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp;
                             const float r = rcp_(a * b);
@@ -347,7 +367,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                             fa[6] += pl1[c] * ax;
                             fa[7] += ptv[c] * hb;
                         }
-                        if (p.trace_full) {
+                        if (TRACE) {
                             fa[2] += wtv[c] * g;
                             fa[3] += __logf(ax + eps);
                             fa[4] += __logf(g + epsp);
@@ -364,25 +384,81 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 gn_cur[c] = gn_nx[c];
                 ds_cur[c] = ds_nx[c];
             }
-            if (((k - k0) & 7) == 7) {
+            if (USED && ((k - k0) & 7) == 7) {
 #pragma unroll
-                for (int q = 0; q < NP1; ++q) {
-                    acc[q] += (double)fa[q];
-                    fa[q] = 0.f;
-                }
+                for (int q = 0; q < NP1; ++q)
+                    if (USED & (1u << q)) {
+                        fb[q] += fa[q];
+                        fa[q] = 0.f;
+                    }
             }
+        }
+        // tile partials -> this warp's fp64 slots (lane order fixed: deterministic)
+        if constexpr (USED != 0) {
+#pragma unroll
+            for (int q = 0; q < NP1; ++q)
+                if (USED & (1u << q)) {
+                    const double v = warp_sum((double)fb[q]);
+                    if (lane == 0) red[w * NP1 + q] += v;
+                    fb[q] = 0.f;
+                }
         }
         // every issued plane (k0-1 .. k0+KC) has been waited on
         __syncthreads();
     }
-#pragma unroll
-    for (int q = 0; q < NP1; ++q) acc[q] += (double)fa[q];
-    if (p.part) {
-        block_sum<NP1>(acc, red);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int q = 0; q < NP1; ++q) p.part[(size_t)blockIdx.x * NP1 + q] = acc[q];
+    if (p.part && tid < NP1) {
+        double t = 0.0;
+        for (int v = 0; v < G::NW; ++v) t += red[v * NP1 + tid];
+        p.part[(size_t)blockIdx.x * NP1 + tid] = t;
     }
+}
+
+// host: mode flags of a sweep and the matching instantiation
+inline int s2_flags(const StencilParams<float>& p) {
+    int f = 0;
+    if (p.audit) {
+        f |= S2_AUDIT;
+        if (p.xprev) f |= S2_PREV;
+        if (p.trace_full) f |= S2_TRACE;
+    }
+    if (p.steptol) f |= S2_STEP;
+    if (p.fista) f |= S2_FISTA;
+    return f;
+}
+
+#define CM_S2_MODES(X) X(0) X(8) X(1) X(9) X(3) X(11) X(5) X(13) X(7) X(15) X(16) X(24)
+
+template <int N> inline cudaError_t stencil2_prepare() {
+    cudaError_t e = cudaSuccess;
+#define CM_S2_ATTR(FL)                                                                         \
+    if (e == cudaSuccess)                                                                     \
+        e = cudaFuncSetAttribute(stencil2_kernel<N, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)S2Geo<N>::SMEM);
+    CM_S2_MODES(CM_S2_ATTR)
+#undef CM_S2_ATTR
+    return e;
+}
+
+template <int N>
+inline cudaError_t stencil2_launch(const StencilParams<float>& p, int grid, cudaStream_t s,
+                                   const CUtensorMap& tmx, const CUtensorMap& tmp,
+                                   const CUtensorMap& tmg, const CUtensorMap& tma) {
+    switch (s2_flags(p)) {
+#define CM_S2_CASE(FL)                                                                         \
+    case FL:                                                                                   \
+        stencil2_kernel<N, FL><<<grid, S2Geo<N>::NT, S2Geo<N>::SMEM, s>>>(p, tmx, tmp, tmg, tma); \
+        break;
+        CM_S2_MODES(CM_S2_CASE)
+#undef CM_S2_CASE
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+template <int N> inline cudaError_t stencil2_occupancy(int* occ) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stencil2_kernel<N, S2_AUDIT | S2_PREV>,
+                                                         S2Geo<N>::NT, S2Geo<N>::SMEM);
 }
 
 } // namespace cm
