@@ -525,7 +525,7 @@ struct DistImpl final : DistBase {
     }
     int finalize(const FinParams& base, bool with_part3, int nb3) {
         for (Rank& k : ranks) {
-            fin_local_kernel<<<1, 256, 0, stream>>>(base.part1 ? k.part1 : nullptr, grid_s2,
+            fin_local_kernel<<<1, FIN_THREADS, 0, stream>>>(base.part1 ? k.part1 : nullptr, grid_s2,
                                                     with_part3 ? k.part3 : nullptr, nb3, k.sums);
             CK(cudaGetLastError());
         }
@@ -538,7 +538,7 @@ struct DistImpl final : DistBase {
             f.st = k.st;
             f.trace = base.trace ? k.trace : nullptr;
             f.sums = k.sums;
-            finalize_kernel<<<1, 256, 0, stream>>>(f);
+            finalize_kernel<<<1, FIN_THREADS, 0, stream>>>(f);
             CK(cudaGetLastError());
         }
         return CM_OK;

@@ -18,22 +18,38 @@ struct FinParams {
     const double* sums;             // z-slab ranks: globally reduced partials [NP1+NP3]
 };
 
-// z-slab ranks: this rank's partials -> out[NP1 + NP3] (then all-reduced)
-static __global__ void __launch_bounds__(256) fin_local_kernel(const double* part1, int nb1,
-                                                               const double* part3, int nb3,
-                                                               double* out) {
-    __shared__ double red[32 * (NP1 + NP3)];
-    double s[NP1 + NP3];
+constexpr int FIN_THREADS = 1024;
+
+// thread-strided sums of the block partials; the loads of an unrolled group are
+// independent (a dependent load chain per thread made this latency bound)
+__device__ __forceinline__ void sum_partials(const double* part1, int nb1, const double* part3,
+                                             int nb3, double (&s)[NP1 + NP3]) {
 #pragma unroll
     for (int q = 0; q < NP1 + NP3; ++q) s[q] = 0.0;
     if (part1)
+#pragma unroll 2
         for (int b = threadIdx.x; b < nb1; b += blockDim.x)
 #pragma unroll
-            for (int q = 0; q < NP1; ++q) s[q] += part1[(size_t)b * NP1 + q];
-    if (part3)
-        for (int b = threadIdx.x; b < nb3; b += blockDim.x)
-#pragma unroll
-            for (int q = 0; q < NP3; ++q) s[NP1 + q] += part3[(size_t)b * NP3 + q];
+            for (int q = 0; q < NP1; ++q) s[q] += __ldcg(part1 + (size_t)b * NP1 + q);
+    if (part3) {
+        const double2* p3 = reinterpret_cast<const double2*>(part3);
+        static_assert(NP3 == 2, "z partials are (quad, cross) pairs");
+#pragma unroll 4
+        for (int b = threadIdx.x; b < nb3; b += blockDim.x) {
+            const double2 v = __ldcg(p3 + b);
+            s[NP1] += v.x;
+            s[NP1 + 1] += v.y;
+        }
+    }
+}
+
+// z-slab ranks: this rank's partials -> out[NP1 + NP3] (then all-reduced)
+static __global__ void __launch_bounds__(FIN_THREADS) fin_local_kernel(const double* part1, int nb1,
+                                                                       const double* part3, int nb3,
+                                                                       double* out) {
+    __shared__ double red[32 * (NP1 + NP3)];
+    double s[NP1 + NP3];
+    sum_partials(part1, nb1, part3, nb3, s);
     block_sum<NP1 + NP3>(s, red);
     if (threadIdx.x == 0)
         for (int q = 0; q < NP1 + NP3; ++q) out[q] = s[q];
@@ -41,7 +57,7 @@ static __global__ void __launch_bounds__(256) fin_local_kernel(const double* par
 
 static __device__ __forceinline__ double surrogate7(const double* o) { return o[0] + o[1] + o[2] + o[4]; }
 
-static __global__ void __launch_bounds__(256) finalize_kernel(FinParams p) {
+static __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinParams p) {
     __shared__ double red[32 * (NP1 + NP3)];
     DevState* st = p.st;
     if (!p.epilogue && ld_done(st)) return;
@@ -55,14 +71,7 @@ static __global__ void __launch_bounds__(256) finalize_kernel(FinParams p) {
         for (int q = 0; q < NP1 + NP3; ++q) s[q] = p.sums[q];
     } else {
     // fixed assignment of blocks to threads + fixed tree => deterministic
-    if (p.part1)
-        for (int b = threadIdx.x; b < p.nb1; b += blockDim.x)
-#pragma unroll
-            for (int q = 0; q < NP1; ++q) s[q] += p.part1[(size_t)b * NP1 + q];
-    if (p.part3)
-        for (int b = threadIdx.x; b < p.nb3; b += blockDim.x)
-#pragma unroll
-            for (int q = 0; q < NP3; ++q) s[NP1 + q] += p.part3[(size_t)b * NP3 + q];
+    sum_partials(p.part1, p.nb1, p.part3, p.nb3, s);
     block_sum<NP1 + NP3>(s, red);
     if (threadIdx.x != 0) return;
     }

@@ -756,7 +756,7 @@ struct Impl final : ImplBase {
             f.gamma = c->gamma;
             f.invL = 1.0 / (double)L;
             f.epilogue = 0;
-            finalize_kernel<<<1, 256, 0, stream>>>(f);
+            finalize_kernel<<<1, FIN_THREADS, 0, stream>>>(f);
             CK(cudaGetLastError());
             CKS(mark(5));
             // K1c: x-line R2C of the new iterate (FISTA: of y_{k+1})
@@ -863,7 +863,7 @@ struct Impl final : ImplBase {
             f.gamma = c->gamma;
             f.invL = 1.0 / (double)L;
             f.epilogue = 1;
-            finalize_kernel<<<1, 256, 0, stream>>>(f);
+            finalize_kernel<<<1, FIN_THREADS, 0, stream>>>(f);
             CK(cudaGetLastError());
             launches += 3;
             CK(cudaMemcpyAsync(&rs, st, sizeof(rs), cudaMemcpyDeviceToHost, stream));

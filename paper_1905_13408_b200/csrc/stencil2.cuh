@@ -90,6 +90,8 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     const bool has_beta = p.beta > 0.0, has_alpha = p.alpha > 0.0;
     constexpr bool with_prev = PREV;
     const bool convex = p.convex != 0;
+    // s = 1/((g cg + ce) max(mu, g)): (1, eps') reweighted, (0, 1) convex
+    const float cg = convex ? 0.f : 1.f, ce = convex ? 1.f : epsp;
     const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter]) : 0.f;
 
     if (tid == 0) {
@@ -171,7 +173,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 const float d1 = xq[c] - xlv[c], d2 = xq[c] - yv[c], d3 = xq[c] - zv[c];
                 const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const float mx = mu > g ? mu : g;
-                const float s = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
+                const float s = rcp_(fmaf(g, cg, ce) * mx);  // convex: 1/mx
                 sv[c] = qin ? s : 0.f;
                 gn[c] = g;
                 ds[c] = d1 + d2 + d3;
@@ -184,7 +186,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 const float d3 = xc - zr[CI - ii];
                 const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const float mx = mu > g ? mu : g;
-                s_halo = convex ? rcp_(mx) : rcp_((g + epsp) * mx);
+                s_halo = rcp_(fmaf(g, cg, ce) * mx);
             }
         };
         // per_m_step weights come from a frozen field: s uses w_tv from it
@@ -313,7 +315,8 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     float v = x_cur[c] - lr * gs;
                     if (has_alpha) {
                         const float th = lra * wl1[c];
-                        v = fabsf(v) <= th ? 0.f : v - copysignf(th, v);
+                        // soft threshold, |v| <= th -> 0 (regularizer.cpp:107): v - clamp(v)
+                        v = v - fminf(fmaxf(v, -th), th);
                     }
                     nx[c] = v;
                 }

@@ -39,6 +39,9 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_E16
 #define CM_Z_E16 1
 #endif
+#ifndef CM_Z_TW
+#define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
+#endif
 
 template <typename R, int N> struct ZGeo {
     // 8 elements per thread for power-of-two sides >= 256 so that W and Yh of
@@ -51,7 +54,8 @@ template <typename R, int N> struct ZGeo {
     static constexpr bool PREFETCH = E8 && !E16;
     static constexpr int E = E16 ? 16 : E8 ? 8 : Geo<R, N>::EY;
     static constexpr int T = N / E;
-    static constexpr int TW = E8 ? (16 < 1024 / T ? 16 : 1024 / T) : Geo<R, N>::TWY;
+    static constexpr int TWMAX = CM_Z_TW ? CM_Z_TW : 16;
+    static constexpr int TW = E8 ? (TWMAX < 1024 / T ? TWMAX : 1024 / T) : Geo<R, N>::TWY;
     static constexpr int NT = TW * T;
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
     static constexpr size_t SMEM_MAIN =
