@@ -25,6 +25,7 @@
 #include "stencil.cuh"
 #include "stencil2.cuh"
 #include "xfft.cuh"
+#include "xyfused.cuh"
 #include "zpass.cuh"
 #include "tma.cuh"
 
@@ -248,6 +249,12 @@ struct Impl final : ImplBase {
     int s2_grid = 0;
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
+    // fused y/x plane pairs (xyfused.cuh): fp32 power-of-two sides 256..1024
+    static constexpr bool FUSE = std::is_same<R, float>::value && (N == 256 || N == 512);
+    bool use_fused = false;
+    int fused_grid = 0, fused_lag = 0;
+    int* fcnt = nullptr;       // [2][N] per-plane producer counters
+    CUtensorMap tm_spec{};     // S as [N*N rows][N/2] 8-byte elements (y column tiles)
     C* S = nullptr;
     R* W = nullptr;
     R* Wn = nullptr;
@@ -374,6 +381,39 @@ struct Impl final : ImplBase {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, xfft_kernel<R, N, 0>,
                                                              XGeo<R, N>::NT, XGeo<R, N>::SMEM));
             xfft_grid = sms * std::max(occx, 1);
+            if constexpr (FUSE) {
+                using F = FGeo<N>;
+                // opt-in: measured no faster than the separate passes at 512^3 (the
+                // passes are latency/issue bound, not DRAM bound)
+                use_fused = std::getenv("CM_FUSED") != nullptr;
+                CK(cudaFuncSetAttribute(fused_pair_kernel<N, 0>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM));
+                CK(cudaFuncSetAttribute(fused_pair_kernel<N, 1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM));
+                int occf0 = 0, occf1 = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf0, fused_pair_kernel<N, 0>, F::NT,
+                                                                 F::SMEM));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf1, fused_pair_kernel<N, 1>, F::NT,
+                                                                 F::SMEM));
+                // every CTA must be resident (consumers spin on producers); the lag
+                // keeps an item's producers more than one grid ahead of it (the
+                // prefetch of the next item must never wait on the current one)
+                fused_grid = sms * std::max(1, std::min(occf0, occf1));
+                fused_lag = std::min(N, (5 * fused_grid + 2 * F::PER_PLANE - 1) / (2 * F::PER_PLANE) + 1);
+                if ((long long)(fused_lag - 1) * F::PER_PLANE < fused_grid) use_fused = false;
+                CKS(dalloc(&fcnt, (size_t)2 * N));
+                EncodeTiledFn enc = encode_tiled_fn();
+                if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+                const cuuint64_t dims[2] = {(cuuint64_t)Nh, (cuuint64_t)N * N};
+                const cuuint64_t strides[1] = {(cuuint64_t)Nh * 8};
+                const cuuint32_t box[2] = {(cuuint32_t)F::TWY, (cuuint32_t)F::YBOX};
+                const cuuint32_t es[2] = {1, 1};
+                if (enc(&tm_spec, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, S, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                    return fail(CM_ERR_CUDA, "tensor map encode failed (spectrum)");
+            }
         }
         CKS(dalloc(&gbuf, L));
         CKS(dalloc(&part1, (size_t)std::max(NB1, sweep_grid) * NP1));
@@ -484,6 +524,26 @@ struct Impl final : ImplBase {
             xfft_kernel<R, N, 1><<<grid, XG::NT, XG::SMEM, stream>>>(p);
         CK(cudaGetLastError());
         return CM_OK;
+    }
+
+    // fused plane pairs: dir 0 = y inverse + x C2R (S -> g), dir 1 = x R2C + y forward
+    int launch_fused(int dir, R* real, const int* stop) {
+        if constexpr (FUSE) {
+            using F = FGeo<N>;
+            CK(cudaMemsetAsync(fcnt + (size_t)dir * N, 0, sizeof(int) * N, stream));
+            FusedParams fp{reinterpret_cast<float2*>(S), reinterpret_cast<float*>(real),
+                           reinterpret_cast<const float2*>(twN), stop, fcnt + (size_t)dir * N,
+                           (float)(1.0 / (double)L), fused_lag};
+            if (dir == 0)
+                fused_pair_kernel<N, 0><<<fused_grid, F::NT, F::SMEM, stream>>>(fp, tm_spec);
+            else
+                fused_pair_kernel<N, 1><<<fused_grid, F::NT, F::SMEM, stream>>>(fp, tm_spec);
+            CK(cudaGetLastError());
+            return CM_OK;
+        } else {
+            (void)dir; (void)real; (void)stop;
+            return fail(CM_ERR_UNSUPPORTED, "fused plane pairs: fp32 N in {256, 512} only");
+        }
     }
 
     // K3: z pass (main tiles, then the packed column 0 with its Friedel mates)
@@ -669,9 +729,14 @@ struct Impl final : ImplBase {
         int launches = 0;
 
         // spectrum of the starting point: x R2C, y forward
-        CKS(launch_xfft(1, fista ? YF[0] : X[0], nullptr));
-        CKS(launch_y(true, nullptr));
-        launches += 2;
+        if (use_fused) {
+            CKS(launch_fused(1, fista ? YF[0] : X[0], nullptr));
+            launches += 1;
+        } else {
+            CKS(launch_xfft(1, fista ? YF[0] : X[0], nullptr));
+            CKS(launch_y(true, nullptr));
+            launches += 2;
+        }
 
         cudaEvent_t pev[8] = {};
         if (profiling)
@@ -682,8 +747,9 @@ struct Impl final : ImplBase {
         };
         auto sweep_and_finalize = [&](int g, cudaEvent_t mid) -> int {
             (void)mid;
-            // K1a: x-line C2R -> data gradient (real space, / L)
-            CKS(launch_xfft(0, gbuf, &st->done));
+            // K1a: x-line C2R -> data gradient (real space, / L); fused: the y
+            // inverse of the same planes ran in the same kernel (mark 2 -> 3 is empty)
+            if (!use_fused) CKS(launch_xfft(0, gbuf, &st->done));
             CKS(mark(3));
             // K1b: stencil sweep
             StencilParams<R> p{};
@@ -759,19 +825,22 @@ struct Impl final : ImplBase {
             finalize_kernel<<<1, FIN_THREADS, 0, stream>>>(f);
             CK(cudaGetLastError());
             CKS(mark(5));
-            // K1c: x-line R2C of the new iterate (FISTA: of y_{k+1})
-            CKS(launch_xfft(1, spec_src, &st->done_y));
+            // K1c: x-line R2C of the new iterate (FISTA: of y_{k+1}); fused: + y forward
+            if (use_fused) CKS(launch_fused(1, spec_src, &st->done_y));
+            else CKS(launch_xfft(1, spec_src, &st->done_y));
             CKS(mark(6));
             return CM_OK;
         };
         auto iteration = [&](int g) -> int {
             CKS(launch_z<ZM_FULL>(audit ? part3 : nullptr, st));  // K3
-            CKS(launch_y(false, st));                              // K4
+            if (use_fused) CKS(launch_fused(0, gbuf, &st->done));  // K4 + K1a
+            else CKS(launch_y(false, st));                         // K4
             CKS(sweep_and_finalize(g, nullptr));                   // K1 + FIN
-            CKS(launch_y(true, st));                               // K2
+            if (!use_fused) CKS(launch_y(true, st));               // K2
             return CM_OK;
         };
 
+        const int per_iter = use_fused ? 6 : 8;  // kernels per iteration
         const bool use_graph = std::getenv("CM_NO_GRAPH") == nullptr && !profiling;
         const int chunk = 6;
         const int nchunks = (K + chunk - 1) / chunk;
@@ -783,10 +852,11 @@ struct Impl final : ImplBase {
                 CKS(mark(0));
                 CKS(launch_z<ZM_FULL>(audit ? part3 : nullptr, st));
                 CKS(mark(1));
-                CKS(launch_y(false, st));
+                if (use_fused) CKS(launch_fused(0, gbuf, &st->done));
+                else CKS(launch_y(false, st));
                 CKS(mark(2));
                 CKS(sweep_and_finalize(g, nullptr));
-                CKS(launch_y(true, st));
+                if (!use_fused) CKS(launch_y(true, st));
                 CKS(mark(7));
                 CK(cudaEventSynchronize(pev[7]));
                 for (int q = 0; q < 7; ++q) {
@@ -795,7 +865,7 @@ struct Impl final : ImplBase {
                     prof_ms[q] += m;
                 }
                 ++prof_iters;
-                launches += 8;
+                launches += per_iter;
             }
             for (auto& e : pev) cudaEventDestroy(e);
         } else if (use_graph) {
@@ -816,7 +886,7 @@ struct Impl final : ImplBase {
                     if (flags_h[q % LOOK]) break;
                 }
                 CK(cudaGraphLaunch(exec, stream));
-                launches += 8 * chunk;
+                launches += per_iter * chunk;
                 CK(cudaMemcpyAsync(&flags_h[q % LOOK], &st->done, sizeof(int),
                                    cudaMemcpyDeviceToHost, stream));
                 CK(cudaEventRecord(ev[q % LOOK], stream));
@@ -828,7 +898,7 @@ struct Impl final : ImplBase {
         } else {
             for (int g = 0; g < K; ++g) {
                 CKS(iteration(g % 6));
-                launches += 8;
+                launches += per_iter;
             }
         }
 
