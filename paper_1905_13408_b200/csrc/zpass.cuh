@@ -39,6 +39,9 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_E16
 #define CM_Z_E16 1
 #endif
+#ifndef CM_Z_E16_MIN
+#define CM_Z_E16_MIN 512
+#endif
 #ifndef CM_Z_TW
 #define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
 #endif
@@ -48,9 +51,11 @@ template <typename R, int N> struct ZGeo {
     // the whole column fit in registers next to it (prefetched before the
     // forward FFT); other sides keep the y-pass plan
     static constexpr bool E8 = CM_Z_E8 && N >= 256 && (N & (N - 1)) == 0 && sizeof(R) == 4;
-    // N >= 1024: 16 elements per thread so that a CTA still covers 16 columns
-    // (128-byte row segments); W and Yh are then loaded after the forward FFT
-    static constexpr bool E16 = CM_Z_E16 && E8 && N >= 1024;
+    // N >= 512: 16 elements per thread, 16 columns per CTA (128-byte row
+    // segments); 512 threads at N = 512 so that two CTAs share an SM (the pass
+    // is latency bound: 0.54 -> 0.47 ms at 512^3); W and Yh are then loaded
+    // after the forward FFT, in groups of 8
+    static constexpr bool E16 = CM_Z_E16 && E8 && N >= CM_Z_E16_MIN;
     static constexpr bool PREFETCH = E8 && !E16;
     static constexpr int E = E16 ? 16 : E8 ? 8 : Geo<R, N>::EY;
     static constexpr int T = N / E;
@@ -60,7 +65,7 @@ template <typename R, int N> struct ZGeo {
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
     static constexpr size_t SMEM_MAIN =
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
-    static constexpr int MINB = NT >= 1024 ? 1 : 2;
+    static constexpr int MINB = NT >= 1024 ? 1 : 2;  // 512 threads: two CTAs per SM
     static constexpr int NT0 = 2 * Geo<R, N>::TY < 64 ? 64 : 2 * Geo<R, N>::TY;
     static constexpr size_t SMEM_COL0 =
         sizeof(Cx<R>) * (N + 5 * (size_t)N) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 1);

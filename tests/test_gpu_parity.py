@@ -307,3 +307,26 @@ def test_vector_path_without_trace_matches_trace_run(n):
     cm.m_step(acc, p.x0, p.x0, cm.RegConfig(**{**cfg.__dict__, "tol_kind": 1, "tol": tol}),
               precision=32, stats=st)
     assert st["stop_reason"] == 2 and st["iterations"] == want + 1
+
+
+@pytest.mark.parametrize("n", [256])
+def test_fused_plane_pairs_match_separate_passes(n, monkeypatch):
+    """The opt-in fused y/x plane-pair kernels (CM_FUSED=1, xyfused.cuh) give the
+    same iterates and audit as the separate passes."""
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=32)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 10
+    t_sep, t_fus = [], []
+    x_sep = cm.m_step(acc, p.x0, p.x0, cfg, t_sep, precision=32)
+    monkeypatch.setenv("CM_FUSED", "1")
+    ctx = cm.Context(n, 32)   # the flag is read when a context is created
+    ctx.set_accumulator(acc)
+    ctx.set_volumes(p.x0, p.x0)
+    st = ctx.solve(cfg, t_fus)
+    x_fus = ctx.get_volume()
+    assert st.kernel_launches < 8 * 10 + 2   # 6 kernels per iteration when fused
+    assert rel_l2(x_fus, x_sep) <= 1e-6
+    np.testing.assert_allclose([r.after.surrogate() for r in t_fus],
+                               [r.after.surrogate() for r in t_sep], rtol=1e-6)
