@@ -22,11 +22,18 @@
 #include "stencil.cuh"
 #include "tma.cuh"
 
+#ifndef CM_S2_MINB
+#define CM_S2_MINB 4
+#endif
+#ifndef CM_S2_TJ
+#define CM_S2_TJ 4  // rows per CTA (+1 halo-row warp); 4 CTAs per SM (8: 2 CTAs, 3.5% slower)
+#endif
+
 namespace cm {
 
 template <int N> struct S2Geo {
     static constexpr int CI = 128;
-    static constexpr int TJ = 8;
+    static constexpr int TJ = CM_S2_TJ;
     static constexpr int KC = N < 64 ? N : 64;   // planes per march
     static constexpr int NW = TJ + 1;            // + halo-row warp
     static constexpr int NT = NW * 32;
@@ -52,7 +59,7 @@ template <int N> struct S2Geo {
 #ifdef CM_S2_MAXREG
 #define CM_S2_BOUNDS __maxnreg__(CM_S2_MAXREG)
 #else
-#define CM_S2_BOUNDS __launch_bounds__(S2Geo<N>::NT, 2)
+#define CM_S2_BOUNDS __launch_bounds__(S2Geo<N>::NT, CM_S2_MINB)
 #endif
 
 // compile-time mode of a sweep: dead terms, branches and accumulators vanish
