@@ -91,14 +91,14 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;  // w = row within tile, TJ = halo
     const bool halo = (w == TJ);
-    const float eps = float(p.eps), epsp = float(p.eps_prime), mu = float(p.mu);
-    const float lr = float(p.lr), lra = float(p.lr * p.alpha), beta = float(p.beta);
-    const float g2 = float(2.0 * p.gamma), inv2mu = float(0.5 / p.mu), hmu = float(0.5 * p.mu);
+    // fp32 parameters as references into the (constant-bank) kernel parameters
+    const float &eps = p.f_eps, &epsp = p.f_epsp, &mu = p.f_mu, &lr = p.f_lr, &lra = p.f_lra;
+    const float &beta = p.f_beta, &g2 = p.f_g2, &inv2mu = p.f_inv2mu, &hmu = p.f_hmu;
+    const float &cg = p.f_cg, &ce = p.f_ce;
     const bool has_beta = p.beta > 0.0, has_alpha = p.alpha > 0.0;
     constexpr bool with_prev = PREV;
     const bool convex = p.convex != 0;
-    // s = 1/((g cg + ce) max(mu, g)): (1, eps') reweighted, (0, 1) convex
-    const float cg = convex ? 0.f : 1.f, ce = convex ? 1.f : epsp;
+    // s = 1/((g cg + ce) max(mu, g)): (cg, ce) = (1, eps') reweighted, (0, 1) convex
     const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter]) : 0.f;
 
     if (tid == 0) {
@@ -450,9 +450,20 @@ template <int N> inline cudaError_t stencil2_prepare() {
 }
 
 template <int N>
-inline cudaError_t stencil2_launch(const StencilParams<float>& p, int grid, cudaStream_t s,
+inline cudaError_t stencil2_launch(StencilParams<float> p, int grid, cudaStream_t s,
                                    const CUtensorMap& tmx, const CUtensorMap& tmp,
                                    const CUtensorMap& tmg, const CUtensorMap& tma) {
+    p.f_eps = float(p.eps);
+    p.f_epsp = float(p.eps_prime);
+    p.f_mu = float(p.mu);
+    p.f_lr = float(p.lr);
+    p.f_lra = float(p.lr * p.alpha);
+    p.f_beta = float(p.beta);
+    p.f_g2 = float(2.0 * p.gamma);
+    p.f_inv2mu = float(0.5 / p.mu);
+    p.f_hmu = float(0.5 * p.mu);
+    p.f_cg = p.convex ? 0.f : 1.f;
+    p.f_ce = p.convex ? 1.f : float(p.eps_prime);
     switch (s2_flags(p)) {
 #define CM_S2_CASE(FL)                                                                         \
     case FL:                                                                                   \
