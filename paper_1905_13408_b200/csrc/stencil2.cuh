@@ -163,8 +163,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         };
         // s on row w of plane q from the slabs of q and q-1 (rows w+1, w in slab coords)
         // returns s[4], plus |Dx|, d-sum for the voxels; halo column (i0+CI) via lane 31
-        auto s_row = [&](int q, float (&xq)[4], float (&sv)[4], float (&gn)[4], float (&ds)[4],
-                         float& s_halo) {
+        auto s_row = [&](int q, float (&xq)[4], float (&sv)[4], float (&gn)[4], float (&ds)[4]) {
             const float* xr = xrow(q, w + 1);
             const float* yr = xrow(q, ry);
             const float* zr = koff + q > 0 ? xrow(q - 1, w + 1) : xr;
@@ -185,19 +184,26 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 gn[c] = g;
                 ds[c] = d1 + d2 + d3;
             }
-            s_halo = 0.f;
-            if (lane == 31 && has_beta && qin && i0 + CI < N) {  // s at x = i0 + CI
-                const float xc = xr[CI - ii];
-                const float d1 = xc - xr[CI - ii - 1];
-                const float d2 = xc - yr[CI - ii];
-                const float d3 = xc - zr[CI - ii];
-                const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
-                const float mx = mu > g ? mu : g;
-                s_halo = rcp_(fmaf(g, cg, ce) * mx);
-            }
+        };
+        // s on the column x = i0 + CI of tile row `lane` (0 .. TJ): computed by the
+        // halo-row warp, so the row warps carry no divergent halo-column work
+        auto s_col = [&](int q) -> float {
+            const int r = lane, gjr = j0 + lane;
+            if (r > TJ || koff + q >= N || gjr >= N || i0 + CI >= N) return 0.f;
+            const float* xb = reinterpret_cast<const float*>(stage(q)) + 4 + CI;
+            const float* zb = koff + q > 0 ? reinterpret_cast<const float*>(stage(q - 1)) + 4 + CI : xb;
+            const float xc = xb[(r + 1) * XW];
+            const float d1 = xc - xb[(r + 1) * XW - 1];
+            const float d2 = xc - xb[(gjr > 0 ? r : r + 1) * XW];
+            const float d3 = xc - zb[(r + 1) * XW];
+            const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+            const float mx = fmaxf(mu, g);
+            if (p.wtvf && !convex)
+                return __ldg(p.wtvf + ((size_t)(q + zs) * N + gjr) * N + i0 + CI) * rcp_(mx);
+            return rcp_(fmaf(g, cg, ce) * mx);
         };
         // per_m_step weights come from a frozen field: s uses w_tv from it
-        auto apply_wtvf = [&](int q, float (&sv)[4], float (&gn)[4], float& s_halo) {
+        auto apply_wtvf = [&](int q, float (&sv)[4], float (&gn)[4]) {
             if (!p.wtvf || convex || !(koff + q < N && row_in)) return;
             const float4 wv = __ldg(reinterpret_cast<const float4*>(
                 p.wtvf + ((size_t)(q + zs) * N + gj) * N + gi0));
@@ -207,29 +213,17 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 const float mx = mu > gn[c] ? mu : gn[c];
                 sv[c] = wt[c] * rcp_(mx);
             }
-            if (lane == 31 && i0 + CI < N && has_beta) {
-                const float wh = __ldg(p.wtvf + ((size_t)(q + zs) * N + gj) * N + i0 + CI);
-                const float* xr = xrow(q, w + 1);
-                const float* yr = xrow(q, ry);
-                const float* zr = koff + q > 0 ? xrow(q - 1, w + 1) : xr;
-                const float xc = xr[CI - ii];
-                const float d1 = xc - xr[CI - ii - 1];
-                const float d2 = xc - yr[CI - ii];
-                const float d3 = xc - zr[CI - ii];
-                const float gg = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
-                s_halo = wh * rcp_(mu > gg ? mu : gg);
-            }
         };
 
         // ---- prologue: s(., k0), rolling state of plane k0 and x_prev(k0-1)
-        float x_cur[4], s_cur[4], gn_cur[4], ds_cur[4], sh_cur;
-        s_row(k0, x_cur, s_cur, gn_cur, ds_cur, sh_cur);
-        apply_wtvf(k0, s_cur, gn_cur, sh_cur);
+        float x_cur[4], s_cur[4], gn_cur[4], ds_cur[4];
+        s_row(k0, x_cur, s_cur, gn_cur, ds_cur);
+        apply_wtvf(k0, s_cur, gn_cur);
         float* S0 = Sring + (size_t)((k0) % 3) * (TJ + 1) * SW;
         if (has_beta) {
             *reinterpret_cast<float4*>(S0 + w * SW + ii) =
                 make_float4(s_cur[0], s_cur[1], s_cur[2], s_cur[3]);
-            if (lane == 31) S0[w * SW + CI] = sh_cur;
+            if (halo && lane <= TJ) S0[lane * SW + CI] = s_col(k0);
         }
         float xp_prev[4] = {0.f, 0.f, 0.f, 0.f};
         if (with_prev && !halo) {
@@ -244,14 +238,14 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             if (tid == 0) issue(k + 2);  // slot of plane k-2: released by the previous barrier
             wait(k + 1);
             // ---- s of plane k+1 on this warp's row
-            float x_nx[4], s_nx[4], gn_nx[4], ds_nx[4], sh_nx;
-            s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx, sh_nx);
-            apply_wtvf(k + 1, s_nx, gn_nx, sh_nx);
+            float x_nx[4], s_nx[4], gn_nx[4], ds_nx[4];
+            s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx);
+            apply_wtvf(k + 1, s_nx, gn_nx);
             float* Sn = Sring + (size_t)((k + 1) % 3) * (TJ + 1) * SW;
             if (has_beta) {
                 *reinterpret_cast<float4*>(Sn + w * SW + ii) =
                     make_float4(s_nx[0], s_nx[1], s_nx[2], s_nx[3]);
-                if (lane == 31) Sn[w * SW + CI] = sh_nx;
+                if (halo && lane <= TJ) Sn[lane * SW + CI] = s_col(k + 1);
             }
             __syncthreads();
             if (!halo && row_in) {
