@@ -48,7 +48,8 @@ template <int N> struct S2Geo {
     static constexpr int NSTAGE = 4;
     static constexpr int SW = CI + 4;            // s row (+ halo column at CI)
     static constexpr size_t OFF_S = NSTAGE * STAGE;
-    static constexpr size_t S_BYTES = (size_t)3 * (TJ + 1) * SW * 4;
+    static constexpr size_t SROW3 = (size_t)(TJ + 1) * SW;   // floats per s ring slot
+    static constexpr size_t S_BYTES = 3 * SROW3 * 4;
     static constexpr size_t OFF_RED = al(OFF_S + S_BYTES);
     static constexpr size_t OFF_BAR = OFF_RED + 32 * NP1 * 8;
     static constexpr size_t SMEM = OFF_BAR + NSTAGE * 8;
@@ -88,6 +89,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     float* Sring = reinterpret_cast<float*>(smem_raw + G::OFF_S);   // [3][TJ+1][SW]
     double* red = reinterpret_cast<double*>(smem_raw + G::OFF_RED);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + G::OFF_BAR);
+    const uint32_t smem_s = smem_u32(smem_raw), bar_s = smem_s + (uint32_t)G::OFF_BAR;
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;  // w = row within tile, TJ = halo
     const bool halo = (w == TJ);
@@ -127,17 +129,17 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         auto issue = [&](int q) {  // q: local plane (ghost planes at -1 and nk)
             if (q > k0 + KC) return;
             const int sl = slot_of(q);
-            unsigned char* st = smem_raw + (size_t)sl * G::STAGE;
-            mbar_expect_tx(&bar[sl], G::XB + (with_prev ? G::PB : 0u) + 2 * G::GB);
-            tma_load_3d(st, &tmx, i0 - 4, j0 - 1, q + zs, &bar[sl]);
-            if (with_prev) tma_load_3d(st + G::OFF_P, &tmp, i0 - 4, j0 - 1, q + zs, &bar[sl]);
+            const uint32_t bs = bar_s + 8u * sl, ss = smem_s + (uint32_t)((size_t)sl * G::STAGE);
+            mbar_expect_tx_s(bs, G::XB + (with_prev ? G::PB : 0u) + 2 * G::GB);
+            tma_load_3d_s(ss, &tmx, i0 - 4, j0 - 1, q + zs, bs);
+            if (with_prev) tma_load_3d_s(ss + (uint32_t)G::OFF_P, &tmp, i0 - 4, j0 - 1, q + zs, bs);
             // g / anchor rows of planes past the march are never read; out of grid -> 0
-            tma_load_3d(st + G::OFF_G, &tmg, i0, j0, q + zs, &bar[sl]);
-            tma_load_3d(st + G::OFF_A, &tma, i0, j0, q + zs, &bar[sl]);
+            tma_load_3d_s(ss + (uint32_t)G::OFF_G, &tmg, i0, j0, q + zs, bs);
+            tma_load_3d_s(ss + (uint32_t)G::OFF_A, &tma, i0, j0, q + zs, bs);
         };
         auto wait = [&](int q) {
             const int sl = slot_of(q);
-            mbar_wait(&bar[sl], (phase_bits >> sl) & 1u);
+            mbar_wait_s(bar_s + 8u * sl, (phase_bits >> sl) & 1u);
             phase_bits ^= (1u << sl);
         };
         if (tid == 0) {
@@ -219,7 +221,11 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         float x_cur[4], s_cur[4], gn_cur[4], ds_cur[4];
         s_row(k0, x_cur, s_cur, gn_cur, ds_cur);
         apply_wtvf(k0, s_cur, gn_cur);
-        float* S0 = Sring + (size_t)((k0) % 3) * (TJ + 1) * SW;
+        // s ring: plane k in slot (k - k0) % 3, rotated by pointer
+        float* Sc_ring = Sring;                        // slot of plane k
+        float* Sn_ring = Sring + G::SROW3;             // slot of plane k + 1
+        float* Sx_ring = Sring + 2 * G::SROW3;         // the third slot
+        float* S0 = Sc_ring;
         if (has_beta) {
             *reinterpret_cast<float4*>(S0 + w * SW + ii) =
                 make_float4(s_cur[0], s_cur[1], s_cur[2], s_cur[3]);
@@ -241,7 +247,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             float x_nx[4], s_nx[4], gn_nx[4], ds_nx[4];
             s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx);
             apply_wtvf(k + 1, s_nx, gn_nx);
-            float* Sn = Sring + (size_t)((k + 1) % 3) * (TJ + 1) * SW;
+            float* Sn = Sn_ring;
             if (has_beta) {
                 *reinterpret_cast<float4*>(Sn + w * SW + ii) =
                     make_float4(s_nx[0], s_nx[1], s_nx[2], s_nx[3]);
@@ -250,7 +256,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             __syncthreads();
             if (!halo && row_in) {
                 // ---- voxel (j, k): update, prox, partials
-                const float* Sc = Sring + (size_t)(k % 3) * (TJ + 1) * SW;
+                const float* Sc = Sc_ring;
                 const size_t gidx = ((size_t)(k + zs) * N + gj) * N + gi0;
                 const unsigned char* stk = stage(k);
                 const float4 g4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_G) + w * CI + ii);
@@ -388,6 +394,10 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 gn_cur[c] = gn_nx[c];
                 ds_cur[c] = ds_nx[c];
             }
+            float* const sfree = Sc_ring;
+            Sc_ring = Sn_ring;
+            Sn_ring = Sx_ring;
+            Sx_ring = sfree;
             if (USED && ((k - k0) & 7) == 7) {
 #pragma unroll
                 for (int q = 0; q < NP1; ++q)
