@@ -119,6 +119,35 @@ def random_phantom_spec(n_blobs: int, side_n: int, seed: int) -> list[Blob]:
     return blobs
 
 
+def bond_phantom_spec(n_chains: int, side_n: int, seed: int) -> list[Blob]:
+    """BASELINE config 2: anisotropic, bond-like structure as a plain
+    blob list (phantom.hpp:10-18) - chains of 6-12 blobs spaced 0.75 sigma along a
+    random direction, starts in the same ball as random_phantom_spec."""
+    rng = Rng(seed, 0xB0D5)
+    c = (side_n - 1) / 2.0
+    radius = 0.27 * side_n
+    blobs = []
+    for _ in range(n_chains):
+        while True:
+            x, y, z = rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(-1, 1)
+            if x * x + y * y + z * z <= 1.0:
+                break
+        while True:
+            dx, dy, dz = rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(-1, 1)
+            r = math.sqrt(dx * dx + dy * dy + dz * dz)
+            if 1e-3 < r <= 1.0:
+                break
+        dx, dy, dz = dx / r, dy / r, dz / r
+        sigma = rng.uniform(1.6, 2.8)
+        amp = rng.uniform(0.6, 1.4)
+        length = 6 + int(rng.uniform(0.0, 7.0))  # 6 .. 12 blobs
+        step = 0.75 * sigma
+        for b in range(length):
+            blobs.append(Blob(c + radius * x + b * step * dx, c + radius * y + b * step * dy,
+                              c + radius * z + b * step * dz, amp, sigma))
+    return blobs
+
+
 def generate_phantom(blobs: list[Blob], side_n: int) -> np.ndarray:
     """phantom.cpp:11-38; returns float64 [k][j][i] (x fastest)."""
     n = side_n
@@ -181,10 +210,18 @@ class Problem:
 
 def synthetic_problem(n: int, n_blobs: int | None = None, phantom_seed: int = 77,
                       weight_seed: int = 5, noise_seed: int = 501,
-                      noise_frac: float = 0.5) -> Problem:
+                      noise_frac: float = 0.5, kind: str = "blobs") -> Problem:
+    """kind "blobs": BASELINE configs 1/3 (isotropic blobs); "bonds": config 2
+    (chains, about the same occupancy: n_blobs / 9 chains of ~9 blobs)."""
     if n_blobs is None:
         n_blobs = max(1, n_blobs_for(n))
-    t = generate_phantom(random_phantom_spec(n_blobs, n, phantom_seed), n)
+    if kind == "bonds":
+        spec = bond_phantom_spec(max(1, n_blobs // 9), n, phantom_seed)
+    elif kind == "blobs":
+        spec = random_phantom_spec(n_blobs, n, phantom_seed)
+    else:
+        raise ValueError(f"unknown phantom kind {kind!r}")
+    t = generate_phantom(spec, n)
     w = symmetric_weight(n, weight_seed)
     rms = math.sqrt(float(np.mean(t * t)))
     nu = counter_gaussian(noise_seed, np.arange(n ** 3, dtype=np.uint64)).reshape(n, n, n)

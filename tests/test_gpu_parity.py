@@ -330,3 +330,39 @@ def test_fused_plane_pairs_match_separate_passes(n, monkeypatch):
     assert rel_l2(x_fus, x_sep) <= 1e-6
     np.testing.assert_allclose([r.after.surrogate() for r in t_fus],
                                [r.after.surrogate() for r in t_sep], rtol=1e-6)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_config2_reweighting_loops_vs_oracle(O, prec):
+    """BASELINE config 2 structure: bond-like (chain) phantom, three
+    m_step calls with per_m_step reweighting, x_init <- previous output, anchor
+    fixed at the initial volume (refine.cpp:181 pattern), against the oracle.
+    128^3 and 6 inner iterations per loop keep the oracle within seconds; every
+    loop starts both solvers from the oracle's previous output (per-call parity)
+    and the GPU-only chain is checked at the end."""
+    n, loops, iters = 128, 3, 6
+    p = synth.synthetic_problem(n, kind="bonds")
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = iters
+    cfg.refresh = cm.Refresh.per_m_step
+    c = make_cfg(alpha=cfg.alpha, beta=cfg.beta, gamma=cfg.gamma, eps=cfg.eps,
+                 eps_prime=cfg.eps_prime, mu=cfg.mu, inner_iters=iters, refresh=1)
+    ctx = cm.Context(n, prec)
+    ctx.set_accumulator(acc)
+    x_ref, x_gpu = p.x0, p.x0
+    for _ in range(loops):
+        trace = []
+        ctx.set_volumes(x_ref, p.x0)
+        ctx.solve(cfg, trace)
+        x_step = ctx.get_volume()
+        rc, xo, tro = O.m_step(p.weight, p.numerator, x_ref, p.x0, c)
+        assert rc == 0
+        check_trace(trace, tro, TOL[prec]["obj"])
+        assert rel_l2(x_step, xo) <= TOL[prec]["vol"]
+        ctx.set_volumes(x_gpu, p.x0)
+        ctx.solve(cfg)
+        x_gpu = ctx.get_volume()
+        x_ref = xo
+    assert rel_l2(x_gpu, x_ref) <= 3 * TOL[prec]["vol"]
