@@ -58,6 +58,27 @@ template <typename C, bool FWD> struct TwPlain {
         return FWD ? cmul(u, w) : cmulc(u, w);
     }
 };
+// Same table, but a radix-R stage reads only w^k and forms w^(rk) by complex
+// products (depth <= 6: error ~6 ulp). For the x lines, where the lanes of a
+// warp read 16 different k at stride 2r (up to 16-way bank conflicts), this
+// trades 14 shared loads per 16 elements for FMA work.
+template <typename C, bool FWD> struct TwPow {
+    static constexpr bool kPow = true;
+    const C* tw;
+    __device__ __forceinline__ C get(int q) const {
+        const C w = tw[q];
+        return FWD ? w : cx<C>(w.x, -w.y);
+    }
+    __device__ __forceinline__ C mul(C u, int q) const {
+        const C w = tw[q];
+        return FWD ? cmul(u, w) : cmulc(u, w);
+    }
+};
+template <typename T, typename = void> struct tw_has_pow { static constexpr bool value = false; };
+template <typename T> struct tw_has_pow<T, decltype((void)T::kPow, void())> {
+    static constexpr bool value = T::kPow;
+};
+
 struct TwPacked {
     const float4* tw4;
     __device__ __forceinline__ float2 mul(float2 u, int q) const {

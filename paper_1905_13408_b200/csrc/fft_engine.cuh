@@ -172,8 +172,18 @@ struct FftStage {
 #pragma unroll
             for (int r = 0; r < R; ++r) u[r] = v[q + r * Q];
             if constexpr (NS > 1) {
+                if constexpr (tw_has_pow<Tw>::value && R >= 4) {
+                    C wp[R];
+                    wp[1] = tw.get(k * TWSTEP);
 #pragma unroll
-                for (int r = 1; r < R; ++r) u[r] = tw.mul(u[r], r * k * TWSTEP);
+                    for (int r = 2; r < R; ++r)
+                        wp[r] = (r % 2 == 0) ? cmul(wp[r / 2], wp[r / 2]) : cmul(wp[r - 1], wp[1]);
+#pragma unroll
+                    for (int r = 1; r < R; ++r) u[r] = cmul(u[r], wp[r]);
+                } else {
+#pragma unroll
+                    for (int r = 1; r < R; ++r) u[r] = tw.mul(u[r], r * k * TWSTEP);
+                }
             }
             Dft<R, FWD, C>::run(u);
             if constexpr (LAST) {

@@ -52,6 +52,22 @@ template <typename R> struct XfParams {
     int nlines;         // lines to transform (N*N, or NK*N on a z-slab rank)
 };
 
+#ifndef CM_XFFT_TWPOW
+#define CM_XFFT_TWPOW 1
+#endif
+
+// x-line twiddles: powers of one table entry per stage in fp32 (bank conflicts,
+// cm_common.cuh TwPow), the plain table in fp64
+template <typename R, bool FWD>
+__device__ __forceinline__ auto xline_tw(const Cx<R>* plain, const float4* packed) {
+    if constexpr (sizeof(R) == 4 && CM_XFFT_TWPOW) {
+        (void)packed;
+        return TwPow<Cx<R>, FWD>{plain};
+    } else {
+        return tw_src<R, FWD>(plain, packed);
+    }
+}
+
 // DIR 0: C2R (S -> real * scale), DIR 1: R2C (real -> S)
 template <typename R, int N, int DIR>
 __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(XfParams<R> p) {
@@ -100,7 +116,7 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
             }
         }
         __syncwarp();
-        fft_regs<Nh, E, N, false>(v, t, buf, pad, tw_src<R, false>(tw, tw4), wsync);
+        fft_regs<Nh, E, N, false>(v, t, buf, pad, xline_tw<R, false>(tw, tw4), wsync);
         const R sc = R(p.scale);
         if (valid)
 #pragma unroll
@@ -115,7 +131,7 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
             v[m] = valid ? *reinterpret_cast<const C*>(xrow + 2 * pp) : cx<C>(R(0), R(0));
         }
         __syncwarp();
-        fft_regs<Nh, E, N, true>(v, t, buf, pad, tw_src<R, true>(tw, tw4), wsync);
+        fft_regs<Nh, E, N, true>(v, t, buf, pad, xline_tw<R, true>(tw, tw4), wsync);
         __syncwarp();
 #pragma unroll
         for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];

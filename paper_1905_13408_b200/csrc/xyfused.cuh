@@ -203,7 +203,7 @@ fused_pair_kernel(FusedParams p, const __grid_constant__ CUtensorMap tmS) {
                         v[m] = make_float2(a.x - bb.y, a.y + bb.x);
                     }
                 }
-                fft_regs<Nh, E, N, false>(v, t, lb, pad, TwPlain<float2, false>{tw}, wsync);
+                fft_regs<Nh, E, N, false>(v, t, lb, pad, TwPow<float2, false>{tw}, wsync);
                 float* xrow = p.real + line * N;
                 const float sc = p.scale;
 #pragma unroll
@@ -217,7 +217,7 @@ fused_pair_kernel(FusedParams p, const __grid_constant__ CUtensorMap tmS) {
                 for (int m = 0; m < E; ++m) v[m] = sl[t + T * m];
                 __syncthreads();
                 if (tid == 0 && i + gridDim.x < seq.total) issue(i + gridDim.x);
-                fft_regs<Nh, E, N, true>(v, t, lb, pad, TwPlain<float2, true>{tw}, wsync);
+                fft_regs<Nh, E, N, true>(v, t, lb, pad, TwPow<float2, true>{tw}, wsync);
                 __syncwarp();
 #pragma unroll
                 for (int m = 0; m < E; ++m) lb[pad(t + T * m)] = v[m];
