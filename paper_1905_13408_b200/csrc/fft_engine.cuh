@@ -227,8 +227,13 @@ __host__ __device__ constexpr int elems_for(int LEN) {
            : (LEN >= 512 ? 16 : 8);
 }
 
-struct PadAddr {  // line layout, one pad element every 8 (bank spread)
-    __device__ __forceinline__ int operator()(int p) const { return p + (p >> 3); }
+#ifndef CM_PAD_SHIFT
+#define CM_PAD_SHIFT 4
+#endif
+struct PadAddr {  // line layout, one pad element every CM_PAD_SHIFT^2 (bank spread)
+    // 16: the radix-16 exchange writes positions 16 t + r of 16 lanes -> 17 t + r,
+    // distinct banks for 8-byte elements (every 8 left a 2-way conflict)
+    __device__ __forceinline__ int operator()(int p) const { return p + (p >> CM_PAD_SHIFT); }
 };
 struct ColAddr {  // [position][column] tile layout
     int tw, col;
