@@ -269,6 +269,7 @@ struct DistImpl final : DistBase {
     bool acc_set = false, acc_fin = false, vol_set = false, anchor_is_init = false;
     double residue = 0.0, max_weight = 0.0;
     int grid_s2 = 1, grid_x = 1, last_iter = 0, last_fista = 0;
+    int ygrid = 1, zgrid = 1;
     bool result_valid = false;
     int trace_cap = 0, theta_cap = 0;
 
@@ -370,6 +371,14 @@ struct DistImpl final : DistBase {
         int occx = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, xfft_kernel<R, N, 0>, XG::NT, XG::SMEM));
         grid_x = sms * std::max(occx, 1);
+        int occy = 0, occz = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occy, ypass_kernel<R, N, false, true>,
+                                                         Geo<R, N>::TWY * Geo<R, N>::TY,
+                                                         YSmem<R, N>::bytes));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occz, zmain_kernel<R, N, ZM_FULL, 0>,
+                                                         ZG::NT, ZG::SMEM_MAIN));
+        ygrid = sms * std::max(occy, 1);
+        zgrid = sms * std::max(occz, 1);
         CK(cudaStreamSynchronize(stream));
         return CM_OK;
     }
@@ -485,8 +494,8 @@ struct DistImpl final : DistBase {
         for (Rank& k : ranks) {
             const int* stop = use_st ? (fwd ? &k.st->done_y : &k.st->done) : nullptr;
             YParams<R> p{fwd ? k.Snat : k.Ssend, k.twN, nullptr, stop, fwd ? k.Ssend : k.Snat,
-                         fwd ? nat_layout() : dm_layout(), fwd ? dm_layout() : nat_layout()};
-            dim3 grid(Nh / Geo<R, N>::TWY, NK);
+                         fwd ? nat_layout() : dm_layout(), fwd ? dm_layout() : nat_layout(), NK};
+            const int grid = std::min((Nh / Geo<R, N>::TWY) * NK, ygrid);
             if (fwd)
                 ypass_kernel<R, N, true, true>
                     <<<grid, Geo<R, N>::TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);

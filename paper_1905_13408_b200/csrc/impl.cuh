@@ -249,6 +249,7 @@ struct Impl final : ImplBase {
     int s2_grid = 0;
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
+    int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
     // fused y/x plane pairs (xyfused.cuh): fp32 power-of-two sides 256..1024
     static constexpr bool FUSE = std::is_same<R, float>::value && (N == 256 || N == 512);
     bool use_fused = false;
@@ -381,6 +382,18 @@ struct Impl final : ImplBase {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occx, xfft_kernel<R, N, 0>,
                                                              XGeo<R, N>::NT, XGeo<R, N>::SMEM));
             xfft_grid = sms * std::max(occx, 1);
+            int occy = 0, occz = 0;
+            CK(cudaFuncSetAttribute(ypass_kernel<R, N, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occy, ypass_kernel<R, N, false>,
+                                                             G::TWY * G::TY, YSmem<R, N>::bytes));
+            CK(cudaFuncSetAttribute(zmain_kernel<R, N, ZM_FULL>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ZGeo<R, N>::SMEM_MAIN));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occz, zmain_kernel<R, N, ZM_FULL>,
+                                                             ZGeo<R, N>::NT, ZGeo<R, N>::SMEM_MAIN));
+            ygrid = sms * std::max(occy, 1);
+            zgrid = sms * std::max(occz, 1);
             if constexpr (FUSE) {
                 using F = FGeo<N>;
                 // opt-in: measured no faster than the separate passes at 512^3 (the
@@ -504,8 +517,8 @@ struct Impl final : ImplBase {
     int launch_y(bool fwd, DevState* s) {
         const SpecLayout nat = spec_layout((long long)N * Nh, 0, N);
         YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr,
-                     nullptr, nat, nat};
-        dim3 grid(Nh / G::TWY, N);
+                     nullptr, nat, nat, N};
+        const int grid = std::min((Nh / G::TWY) * N, ygrid);  // persistent
         if (fwd)
             ypass_kernel<R, N, true><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
         else

@@ -113,6 +113,7 @@ template <typename R> struct YParams {
     const int* stop;    // &st->done (inverse pass) or &st->done_y (forward pass), or null
     C* Sout;            // output spectrum (may equal S), or null for in place
     SpecLayout lin, lout;
+    int nplanes;        // planes k (N, or NK on a z-slab rank)
 };
 
 template <typename C>
@@ -138,7 +139,8 @@ template <typename R> __host__ __device__ constexpr bool use_packed_tw() { retur
 // y pass: FFT along j for every (k, h) column. grid = (Nh/TWY, N)
 // ==================================================================================
 template <typename R, int N, bool FWD, bool DM = false>
-__global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY)
+__global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY,
+                                  Geo<R, N>::TWY * Geo<R, N>::TY <= 512 ? 2 : 1)
 ypass_kernel(YParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
@@ -151,8 +153,12 @@ ypass_kernel(YParams<R> p) {
     else stage_table(tw, p.twN, N);
     const int col = threadIdx.x % G::TWY;
     const int t = threadIdx.x / G::TWY;
-    const int h = blockIdx.x * G::TWY + col;
-    const int k = blockIdx.y;
+    // persistent over (column tile, plane): the twiddle table is staged once
+    constexpr int NTX = G::Nh / G::TWY;
+    const int ntiles = NTX * p.nplanes;
+    for (int tile = blockIdx.y * gridDim.x + blockIdx.x; tile < ntiles; tile += gridDim.x * gridDim.y) {
+    const int h = (tile % NTX) * G::TWY + col;
+    const int k = tile / NTX;
     C v[G::EY];
     if constexpr (!DM) {  // natural layout, in place
         C* base = p.S + (size_t)k * p.lin.kstride + h;
@@ -172,6 +178,7 @@ ypass_kernel(YParams<R> p) {
         C* out = p.Sout ? p.Sout : p.S;
 #pragma unroll
         for (int m = 0; m < G::EY; ++m) out[p.lout.at(k, t + G::TY * m, h, G::Nh)] = v[m];
+    }
     }
 }
 

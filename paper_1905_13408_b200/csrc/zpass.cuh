@@ -96,9 +96,14 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     }
     const int col = threadIdx.x % TW;
     const int t = threadIdx.x / TW;
-    const int h = blockIdx.x * TW + col;
-    const int b = blockIdx.y;  // local row
     const int nrows = NR ? NR : p.nrows;
+    // one (column tile, row b) per CTA: a persistent loop here costs registers
+    // (spills at 64 per thread) for less than the twiddle staging it saves
+    constexpr int NTX = Nh / TW;
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    if (tile >= NTX * nrows) return;
+    const int h = (tile % NTX) * TW + col;
+    const int b = tile / NTX;  // local row
     const size_t plane = (size_t)nrows * Nh;
     C* base = p.S + (size_t)b * Nh + h;
     C v[E];
@@ -159,9 +164,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         double acc[2] = {2.0 * (double)quad, 2.0 * (double)cross};  // mates 0 < h < N/2
         block_sum<2>(acc, red);
         if (threadIdx.x == 0) {
-            const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-            p.part[bid * NP3 + 0] = acc[0];
-            p.part[bid * NP3 + 1] = acc[1];
+            p.part[tile * NP3 + 0] = acc[0];
+            p.part[tile * NP3 + 1] = acc[1];
         }
     }
     if constexpr (MODE == ZM_FIT) return;

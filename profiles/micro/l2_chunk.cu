@@ -40,7 +40,7 @@ int main(int argc, char** argv) {
     const SpecLayout nat = spec_layout((long long)N * Nh, 0, N);
     auto run = [&](int B) {
         for (int p0 = 0; p0 < N; p0 += B) {
-            YParams<float> yp{S + (size_t)p0 * N * Nh, tw, nullptr, nullptr, nullptr, nat, nat};
+            YParams<float> yp{S + (size_t)p0 * N * Nh, tw, nullptr, nullptr, nullptr, nat, nat, B};
             ypass_kernel<float, N, false><<<dim3(Nh / G::TWY, B), G::TWY * G::TY, YSmem<float, N>::bytes>>>(yp);
             XfParams<float> xp{S + (size_t)p0 * N * Nh, g + (size_t)p0 * N * N, tw, nullptr, nullptr, 1.0, B * N};
             const int grid = std::min(xgrid, (B * N + XG::LPC - 1) / XG::LPC);
