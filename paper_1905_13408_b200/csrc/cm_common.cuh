@@ -129,6 +129,20 @@ __device__ __forceinline__ size_t opaque(size_t v) {
     return v;
 }
 
+#ifndef CM_PDL_EARLY
+#define CM_PDL_EARLY 0  // trigger at CTA start (measured slower: dependents hold SM slots)
+#endif
+// programmatic dependent launch (PDL): the next kernel in the stream may be
+// scheduled once every CTA of this one has triggered; it must wait for this
+// grid's completion (and memory) before reading anything this grid wrote.
+// Both are no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() {
+#if CM_PDL_EARLY
+    asm volatile("griddepcontrol.launch_dependents;");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ int ld_done(const DevState* st) {
     return *((volatile const int*)&st->done);
 }

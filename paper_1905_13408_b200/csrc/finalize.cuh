@@ -59,6 +59,8 @@ static __device__ __forceinline__ double surrogate7(const double* o) { return o[
 
 static __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinParams p) {
     __shared__ double red[32 * (NP1 + NP3)];
+    pdl_trigger();
+    pdl_wait();
     DevState* st = p.st;
     if (!p.epilogue && ld_done(st)) return;
     if (p.epilogue && !(st->stop_reason == 1 && st->audit)) return;

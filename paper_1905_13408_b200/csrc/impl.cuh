@@ -250,6 +250,11 @@ struct Impl final : ImplBase {
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
+    // programmatic dependent launch between the per-iteration kernels (each
+    // waits on griddepcontrol before touching its predecessor's output); opt-in:
+    // measured neutral (dependents cannot start work before the predecessor
+    // completes) or slower with an early trigger (waiting CTAs hold SM slots)
+    bool use_pdl = std::getenv("CM_PDL") != nullptr;
     // fused y/x plane pairs (xyfused.cuh): fp32 power-of-two sides 256..1024
     static constexpr bool FUSE = std::is_same<R, float>::value && (N == 256 || N == 512);
     bool use_fused = false;
@@ -520,10 +525,11 @@ struct Impl final : ImplBase {
                      nullptr, nat, nat, N};
         const int grid = std::min((Nh / G::TWY) * N, ygrid);  // persistent
         if (fwd)
-            ypass_kernel<R, N, true><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
+            CK(launch_pdl(use_pdl, ypass_kernel<R, N, true>, dim3(grid), dim3(G::TWY * G::TY),
+                          YSmem<R, N>::bytes, stream, p));
         else
-            ypass_kernel<R, N, false><<<grid, G::TWY * G::TY, YSmem<R, N>::bytes, stream>>>(p);
-        CK(cudaGetLastError());
+            CK(launch_pdl(use_pdl, ypass_kernel<R, N, false>, dim3(grid), dim3(G::TWY * G::TY),
+                          YSmem<R, N>::bytes, stream, p));
         return CM_OK;
     }
     // x-line transforms: dir 0 C2R (S -> g * invL), dir 1 R2C (real -> S)
@@ -532,10 +538,9 @@ struct Impl final : ImplBase {
         XfParams<R> p{S, real, twN, dir == 0 ? twI4 : twF4, stop, 1.0 / (double)L, N * N};
         const int grid = std::min(XG::NB, xfft_grid);
         if (dir == 0)
-            xfft_kernel<R, N, 0><<<grid, XG::NT, XG::SMEM, stream>>>(p);
+            CK(launch_pdl(use_pdl, xfft_kernel<R, N, 0>, dim3(grid), dim3(XG::NT), XG::SMEM, stream, p));
         else
-            xfft_kernel<R, N, 1><<<grid, XG::NT, XG::SMEM, stream>>>(p);
-        CK(cudaGetLastError());
+            CK(launch_pdl(use_pdl, xfft_kernel<R, N, 1>, dim3(grid), dim3(XG::NT), XG::SMEM, stream, p));
         return CM_OK;
     }
 
@@ -565,12 +570,10 @@ struct Impl final : ImplBase {
         using ZG = ZGeo<R, N>;
         ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N};
         dim3 grid(Nh / ZG::TW, N);
-        zmain_kernel<R, N, MODE><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
-        CK(cudaGetLastError());
-        if constexpr (MODE != ZM_FWD) {
-            zcol0_kernel<R, N, MODE><<<N / 2 + 1, ZG::NT0, ZG::SMEM_COL0, stream>>>(p);
-            CK(cudaGetLastError());
-        }
+        CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
+        if constexpr (MODE != ZM_FWD)
+            CK(launch_pdl(use_pdl, zcol0_kernel<R, N, MODE>, dim3(N / 2 + 1), dim3(ZG::NT0),
+                          ZG::SMEM_COL0, stream, p));
         return CM_OK;
     }
     int upload_real(const double* host, R* dst) {
@@ -814,7 +817,8 @@ struct Impl final : ImplBase {
                 if (use_s2) {
                     const int xi = fista ? 3 + g % 2 : g % 3;
                     const int pi = fista ? 0 : (g + 2) % 3;
-                    CK(stencil2_launch<N>(p, s2_grid, stream, tm2_x[xi], tm2_p[pi], tm2_g, tm2_a));
+                    CK(stencil2_launch<N>(p, s2_grid, stream, tm2_x[xi], tm2_p[pi], tm2_g, tm2_a,
+                                          use_pdl));
                 }
             }
             if (!use_s2)
@@ -835,8 +839,7 @@ struct Impl final : ImplBase {
             f.gamma = c->gamma;
             f.invL = 1.0 / (double)L;
             f.epilogue = 0;
-            finalize_kernel<<<1, FIN_THREADS, 0, stream>>>(f);
-            CK(cudaGetLastError());
+            CK(launch_pdl(use_pdl, finalize_kernel, dim3(1), dim3(FIN_THREADS), 0, stream, f));
             CKS(mark(5));
             // K1c: x-line R2C of the new iterate (FISTA: of y_{k+1}); fused: + y forward
             if (use_fused) CKS(launch_fused(1, spec_src, &st->done_y));

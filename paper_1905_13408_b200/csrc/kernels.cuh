@@ -144,6 +144,8 @@ __global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY,
 ypass_kernel(YParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
+    pdl_trigger();
+    pdl_wait();
     if (p.stop && *((volatile const int*)p.stop)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);

@@ -22,6 +22,8 @@
 #include "stencil.cuh"
 #include "tma.cuh"
 
+#include <utility>
+
 #ifndef CM_S2_MINB
 #define CM_S2_MINB 4
 #endif
@@ -84,6 +86,8 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     constexpr bool TRACE = AUDIT && (F & S2_TRACE), STEP = F & S2_STEP, FISTA = F & S2_FISTA;
     constexpr unsigned USED = s2_used(F);
     constexpr int CI = G::CI, TJ = G::TJ, KC = G::KC, XW = G::XW, SW = G::SW;
+    pdl_trigger();
+    pdl_wait();
     if (p.st && ld_done(p.st)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* Sring = reinterpret_cast<float*>(smem_raw + G::OFF_S);   // [3][TJ+1][SW]
@@ -453,10 +457,27 @@ template <int N> inline cudaError_t stencil2_prepare() {
     return e;
 }
 
+// launch with the programmatic-dependent-launch attribute (see pdl_wait)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int N>
 inline cudaError_t stencil2_launch(StencilParams<float> p, int grid, cudaStream_t s,
                                    const CUtensorMap& tmx, const CUtensorMap& tmp,
-                                   const CUtensorMap& tmg, const CUtensorMap& tma) {
+                                   const CUtensorMap& tmg, const CUtensorMap& tma, bool pdl = false) {
     p.f_eps = float(p.eps);
     p.f_epsp = float(p.eps_prime);
     p.f_mu = float(p.mu);
@@ -471,8 +492,8 @@ inline cudaError_t stencil2_launch(StencilParams<float> p, int grid, cudaStream_
     switch (s2_flags(p)) {
 #define CM_S2_CASE(FL)                                                                         \
     case FL:                                                                                   \
-        stencil2_kernel<N, FL><<<grid, S2Geo<N>::NT, S2Geo<N>::SMEM, s>>>(p, tmx, tmp, tmg, tma); \
-        break;
+        return launch_pdl(pdl, stencil2_kernel<N, FL>, dim3(grid), dim3(S2Geo<N>::NT),          \
+                          S2Geo<N>::SMEM, s, p, tmx, tmp, tmg, tma);
         CM_S2_MODES(CM_S2_CASE)
 #undef CM_S2_CASE
         default:

@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
     using X = XGeo<R, N>;
     using C = Cx<R>;
     constexpr int Nh = X::Nh, E = X::E, T = X::T;
+    pdl_trigger();
+    pdl_wait();
     if (p.stop && *((volatile const int*)p.stop)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);

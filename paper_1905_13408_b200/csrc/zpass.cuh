@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     using G = Geo<R, N>;
     using C = Cx<R>;
     constexpr int TW = ZGeo<R, N>::TW, T = ZGeo<R, N>::T, E = ZGeo<R, N>::E, Nh = G::Nh;
+    pdl_trigger();
+    pdl_wait();
     if (p.st && ld_done(p.st)) {
         // the y-forward pass of the stopping iteration has run; stop the next one
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) p.st->done_y = 1;
@@ -186,6 +188,8 @@ zcol0_kernel(ZMParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
     constexpr int T = G::TY, E = G::EY, Nh = G::Nh;
+    pdl_trigger();
+    pdl_wait();
     if (p.st && ld_done(p.st)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
