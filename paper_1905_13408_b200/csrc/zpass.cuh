@@ -14,6 +14,7 @@
 #include "cm_common.cuh"
 #include "fft_engine.cuh"
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace cm {
 
@@ -42,6 +43,9 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_E16_MIN
 #define CM_Z_E16_MIN 512
 #endif
+#ifndef CM_Z_WSM
+#define CM_Z_WSM 0  // cp.async staging of W: measured slower (0.46 -> 0.55 ms at 512^3)
+#endif
 #ifndef CM_Z_TW
 #define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
 #endif
@@ -63,8 +67,12 @@ template <typename R, int N> struct ZGeo {
     static constexpr int TW = E8 ? (TWMAX < 1024 / T ? TWMAX : 1024 / T) : Geo<R, N>::TWY;
     static constexpr int NT = TW * T;
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
-    static constexpr size_t SMEM_MAIN =
+    // E16: the W tile is staged into shared memory by cp.async at kernel start
+    // (its latency overlaps the S loads and the forward FFT)
+    static constexpr bool WSM = E16 && CM_Z_WSM;
+    static constexpr size_t OFF_WSM =
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
+    static constexpr size_t SMEM_MAIN = OFF_WSM + (WSM ? sizeof(R) * (size_t)N * TW : 0);
     static constexpr int MINB = NT >= 1024 ? 1 : 2;  // 512 threads: two CTAs per SM
     static constexpr int NT0 = 2 * Geo<R, N>::TY < 64 ? 64 : 2 * Geo<R, N>::TY;
     static constexpr size_t SMEM_COL0 =
@@ -106,6 +114,20 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     if (tile >= NTX * nrows) return;
     const int h = (tile % NTX) * TW + col;
     const int b = tile / NTX;  // local row
+    [[maybe_unused]] R* wsm = reinterpret_cast<R*>(smem_raw + ZGeo<R, N>::OFF_WSM);
+    if constexpr (ZGeo<R, N>::WSM && MODE != ZM_FWD) {
+        constexpr int CH = TW * (int)sizeof(R) / 16;  // 16-byte chunks per row
+        const R* wrow = p.W + (size_t)b * Nh + (tile % NTX) * TW;
+        const size_t wstride = (size_t)nrows * Nh;
+        for (int q = threadIdx.x; q < N * CH; q += blockDim.x) {
+            const int c = q / CH, part = q % CH;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             smem_u32(wsm + c * TW + part * 4)),
+                         "l"(wrow + c * wstride + part * 4)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     const size_t plane = (size_t)nrows * Nh;
     C* base = p.S + (size_t)b * Nh + h;
     C v[E];
@@ -135,6 +157,10 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     }
     R quad = R(0), cross = R(0);
     const size_t lplane = opaque(plane);
+    if constexpr (ZGeo<R, N>::WSM) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
     if (h == 0) {
 #pragma unroll
         for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
@@ -148,7 +174,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
 #pragma unroll
                 for (int m = g0; m < g0 + G; ++m) {
                     const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * Nh + h;
-                    w[m] = __ldg(p.W + gi);
+                    if constexpr (!ZGeo<R, N>::WSM) w[m] = __ldg(p.W + gi);
+                    else w[m] = wsm[(t + T * m) * TW + col];
                     y[m] = p.Yh[gi];
                 }
             }
