@@ -73,7 +73,7 @@ template <typename R, int N> struct ZGeo {
     static constexpr size_t OFF_WSM =
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
     static constexpr size_t SMEM_MAIN = OFF_WSM + (WSM ? sizeof(R) * (size_t)N * TW : 0);
-    static constexpr int MINB = NT >= 1024 ? 1 : 2;  // 512 threads: two CTAs per SM
+    static constexpr int MINB = NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
     static constexpr int NT0 = 2 * Geo<R, N>::TY < 64 ? 64 : 2 * Geo<R, N>::TY;
     static constexpr size_t SMEM_COL0 =
         sizeof(Cx<R>) * (N + 5 * (size_t)N) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 1);
