@@ -46,6 +46,9 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_WSM
 #define CM_Z_WSM 0  // cp.async staging of W: measured slower (0.46 -> 0.55 ms at 512^3)
 #endif
+#ifndef CM_Z_PFW
+#define CM_Z_PFW 0
+#endif
 #ifndef CM_Z_TW
 #define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
 #endif
@@ -138,12 +141,14 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     R w[E];
     C y[E];
     constexpr bool PREFETCH = ZGeo<R, N>::PREFETCH && MODE != ZM_FWD;
-    if constexpr (PREFETCH) {
+    // E16: W alone (one register per element) is prefetched under CM_Z_PFW
+    constexpr bool PFW = !PREFETCH && CM_Z_PFW && ZGeo<R, N>::E16 && MODE != ZM_FWD;
+    if constexpr (PREFETCH || PFW) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const size_t gi = ((size_t)(t + T * m) * nrows + b) * Nh + h;
             w[m] = __ldg(p.W + gi);
-            y[m] = __ldg(p.Yh + gi);
+            if constexpr (PREFETCH) y[m] = __ldg(p.Yh + gi);
         }
     }
     __syncthreads();
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
 #pragma unroll
                 for (int m = g0; m < g0 + G; ++m) {
                     const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * Nh + h;
-                    if constexpr (!ZGeo<R, N>::WSM) w[m] = __ldg(p.W + gi);
-                    else w[m] = wsm[(t + T * m) * TW + col];
+                    if constexpr (ZGeo<R, N>::WSM) w[m] = wsm[(t + T * m) * TW + col];
+                    else if constexpr (!PFW) w[m] = __ldg(p.W + gi);
                     y[m] = p.Yh[gi];
                 }
             }
