@@ -1,0 +1,91 @@
+"""Parity at the BASELINE sizes, where the CPU oracle is too slow to run
+(a 512^3 audited iteration takes ~90 s on one core):
+
+* the fp32 product kernels (the 512-point plans, 16-element z pass, 4-row
+  stencil tiles, x-line twiddle powers) against the fp64 parity mode — which is
+  itself pinned to the reference's golden vectors and oracle at small sizes —
+  per-iteration objective within 1e-5 relative, final volume within 1e-4;
+* the data gradient (the solver's z/y/x transforms) against scipy's fp64 FFT
+  at 512^3 (regularizer.cpp:87-101 restated with numpy);
+* the z-slab decomposition at 512^3 over 8 emulated ranks against one GPU.
+"""
+import numpy as np
+import pytest
+
+import paper_1905_13408_b200 as cm
+from paper_1905_13408_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _traces(rows):
+    return np.array([np.r_[r.before.as_array(), r.after.as_array(), r.step] for r in rows])
+
+
+def _check_traces(a, b, tol):
+    assert a.shape == b.shape
+    for half in (slice(0, 7), slice(7, 14)):
+        surr = np.abs(b[:, half][:, [0, 1, 2, 4]].sum(axis=1))
+        scale = np.maximum(np.abs(b[:, half]), surr[:, None])
+        assert (np.abs(a[:, half] - b[:, half]) / scale).max() <= tol
+    np.testing.assert_allclose(a[:, 14], b[:, 14], rtol=1e-6)
+
+
+@pytest.fixture(scope="module")
+def p512():
+    return synth.synthetic_problem(512)
+
+
+@pytest.mark.parametrize("mode", ["per_inner", "per_m_step", "fista"])
+def test_fp32_kernels_match_fp64_mode_at_512(p512, mode):
+    p = p512
+    acc = cm.AccumulatorPair(512, p.numerator, p.weight, True)
+    s = cm.scale_data(acc, precision=64)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    extra = {"per_inner": {}, "per_m_step": {"refresh": cm.Refresh.per_m_step},
+             "fista": {"momentum": 1, "refresh": cm.Refresh.per_m_step}}[mode]
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 8, **extra})
+    t32, t64 = [], []
+    x32 = cm.m_step(acc, p.x0, p.x0, cfg, t32 if mode != "fista" else None, precision=32)
+    x64 = cm.m_step(acc, p.x0, p.x0, cfg, t64 if mode != "fista" else None, precision=64)
+    if mode != "fista":
+        _check_traces(_traces(t32), _traces(t64), 1e-5)
+    assert _rel(x32, x64) <= 1e-4
+
+
+def test_data_gradient_512_vs_scipy(p512):
+    import scipy.fft
+
+    p = p512
+    acc = cm.AccumulatorPair(512, p.numerator, p.weight, True)
+    x = p.truth
+    g = cm.data_gradient(x, acc, precision=32)
+    # regularizer.cpp:87-101: halfshift3(Re ifft3(W * fft3(halfshift3 x) - Y))
+    F = scipy.fft.fftn(synth.halfshift3(x).astype(np.complex128), workers=-1)
+    R = scipy.fft.ifftn(p.weight * F - p.numerator, workers=-1).real
+    ref = synth.halfshift3(R)
+    assert np.abs(g - ref).max() <= 2e-5 * np.abs(ref).max()
+
+
+def test_slab_8_ranks_at_512(p512):
+    from paper_1905_13408_b200.slab import SlabContext
+
+    p = p512
+    acc = cm.AccumulatorPair(512, p.numerator, p.weight, True)
+    s = cm.scale_data(acc, precision=32)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 8
+    t1, t2 = [], []
+    x1 = cm.m_step(acc, p.x0, p.x0, cfg, t1, precision=32)
+    sc = SlabContext(512, 8)
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0)
+    sc.solve(cfg, t2)
+    x2 = sc.get_volume()
+    sc.close()
+    _check_traces(_traces(t2), _traces(t1), 1e-6)
+    assert _rel(x2, x1) <= 1e-6
