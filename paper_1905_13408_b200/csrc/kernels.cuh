@@ -35,6 +35,10 @@ __host__ __device__ constexpr int pow2_divisor_le(int v, int cap) {
     return t;
 }
 
+#ifndef CM_Y_TWMAX
+#define CM_Y_TWMAX 16  // columns per y tile (128-byte rows in fp32)
+#endif
+
 template <typename R, int N> struct Geo {
     using C = Cx<R>;
     static constexpr int Nh = N / 2;
@@ -48,7 +52,8 @@ template <typename R, int N> struct Geo {
     static constexpr int TY = N / EY;
     static constexpr int SMEM_CAP = 96 * 1024; // per tile buffer budget (bytes)
     static constexpr int TWY_CAP = (SMEM_CAP / (N * (int)sizeof(C))) < 1 ? 1 : (SMEM_CAP / (N * (int)sizeof(C)));
-    static constexpr int TWY = pow2_divisor_le(Nh, (16 < (1024 / TY) ? 16 : (1024 / TY)) < TWY_CAP ? (16 < (1024 / TY) ? 16 : (1024 / TY)) : TWY_CAP);
+    static constexpr int TWY_LIM = (CM_Y_TWMAX < (1024 / TY) ? CM_Y_TWMAX : (1024 / TY));
+    static constexpr int TWY = pow2_divisor_le(Nh, TWY_LIM < TWY_CAP ? TWY_LIM : TWY_CAP);
     static constexpr int TW3_LIM = (512 / TY) < 1 ? 1 : (512 / TY);
     static constexpr int TW3_CAP = TWY_CAP / 2 < 1 ? 1 : TWY_CAP / 2;
     static constexpr int TW3 = pow2_divisor_le(Nh, (16 < TW3_LIM ? 16 : TW3_LIM) < TW3_CAP ? (16 < TW3_LIM ? 16 : TW3_LIM) : TW3_CAP);
