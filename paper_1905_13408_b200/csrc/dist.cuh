@@ -57,10 +57,9 @@ zcol0r_kernel(ZMParams<float> p, const float2* Z0full, int rb0) {
         const C zm = Z0full[(size_t)bm * N + (N - c) % N];
         const C f0 = make_float2(0.5f * (zz.x + zm.x), 0.5f * (zz.y - zm.y));
         const C fn = make_float2(0.5f * (zz.y + zm.y), -0.5f * (zz.x - zm.x));
-        const size_t gi = ((size_t)c * p.nrows + bl) * Nh;
-        const size_t ni = (size_t)c * p.nrows + bl;
-        const float w0 = p.W[gi], wn = p.Wn[ni];
-        const C y0 = p.Yh[gi], yn = p.Yn[ni];
+        const C* q = p.Q0 + ((size_t)bl * N + c) * 3;
+        const C wq = q[0], y0 = q[1], yn = q[2];
+        const float w0 = wq.x, wn = wq.y;
         if (act) {
             quad += (double)w0 * ((double)f0.x * f0.x + (double)f0.y * f0.y) +
                     (double)wn * ((double)fn.x * fn.x + (double)fn.y * fn.y);
@@ -93,7 +92,7 @@ zcol0r_kernel(ZMParams<float> p, const float2* Z0full, int rb0) {
 // are taken once by the owner of the staging copy.
 __global__ static void convert_rows_kernel(int n, int rb0, int nrows, const double* __restrict__ W,
                                            const double* __restrict__ Y, float* Wm, float* Wn,
-                                           float2* Ym, float2* Yn) {
+                                           float2* Ym, float2* Yn, float2* Q0) {
     const int nh = n / 2;
     const size_t total = (size_t)n * nrows * (nh + 1);
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
@@ -116,6 +115,11 @@ __global__ static void convert_rows_kernel(int n, int rb0, int nrows, const doub
             const size_t o = (size_t)c * nrows + bl;
             Wn[o] = float(wp);
             Yn[o] = make_float2(float(pr), float(pi));
+        }
+        if (a == 0 || a == nh) {  // row-major column-0 copy (zcol0r_kernel)
+            float2* q = Q0 + ((size_t)bl * n + c) * 3;
+            reinterpret_cast<float*>(q)[a == 0 ? 0 : 1] = float(wp);
+            q[a == 0 ? 1 : 2] = make_float2(float(pr), float(pi));
         }
     }
 }
@@ -173,7 +177,7 @@ __global__ static void synth_volume_kernel(int n, int koff, int nk, unsigned lon
 
 // W = 1 + (u(n) + u(-n))/2 on this rank's rows of the packed half spectrum
 __global__ static void synth_weight_kernel(int n, int rb0, int nrows, unsigned long long seed,
-                                           float* Wm, float* Wn) {
+                                           float* Wm, float* Wn, float2* Q0) {
     const int nh = n / 2;
     const size_t total = (size_t)n * nrows * (nh + 1);
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
@@ -187,6 +191,7 @@ __global__ static void synth_weight_kernel(int n, int rb0, int nrows, unsigned l
         const float w = float(1.0 + 0.5 * (hash_unit(seed ^ 0xABCDull, i) + hash_unit(seed ^ 0xABCDull, m)));
         if (a < nh) Wm[((size_t)c * nrows + bl) * nh + a] = w;
         else Wn[(size_t)c * nrows + bl] = w;
+        if (a == 0 || a == nh) reinterpret_cast<float*>(Q0 + ((size_t)bl * n + c) * 3)[a == 0 ? 0 : 1] = w;
     }
 }
 
@@ -245,6 +250,7 @@ struct DistImpl final : DistBase {
         R* Wn = nullptr;
         C* Yh = nullptr;
         C* Yn = nullptr;
+        C* Q0 = nullptr;  // [NB][N][3] column-0 inputs, row-major
         C* Z0 = nullptr;
         C* Z0full = nullptr;
         C* twN = nullptr;
@@ -331,6 +337,7 @@ struct DistImpl final : DistBase {
             CKS(dalloc(&k.Wn, (size_t)N * NB));
             CKS(dalloc(&k.Yh, (size_t)N * NB * Nh));
             CKS(dalloc(&k.Yn, (size_t)N * NB));
+            CKS(dalloc(&k.Q0, (size_t)3 * N * NB));
             CKS(dalloc(&k.Z0, (size_t)NB * N));
             CKS(dalloc(&k.Z0full, NN));
             CKS(dalloc(&k.twN, N));
@@ -401,7 +408,7 @@ struct DistImpl final : DistBase {
         CK(cudaGetLastError());
         for (Rank& k : ranks) {
             convert_rows_kernel<<<grid_for(NN * (Nh + 1) / P, 256), 256, 0, stream>>>(
-                N, k.rb0, NB, stage, stage + L, k.W, k.Wn, k.Yh, k.Yn);
+                N, k.rb0, NB, stage, stage + L, k.W, k.Wn, k.Yh, k.Yn, k.Q0);
             CK(cudaGetLastError());
         }
         unsigned long long h[4];
@@ -451,7 +458,7 @@ struct DistImpl final : DistBase {
     int z_pass(bool fit_only, bool with_part) {
         for (Rank& k : ranks) {
             ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, k.twF4, k.twI4,
-                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB};
+                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB, k.Q0};
             dim3 grid(Nh / ZG::TW, NB);
             if (fit_only)
                 zmain_kernel<R, N, ZM_FIT, 0><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
@@ -470,7 +477,7 @@ struct DistImpl final : DistBase {
         const size_t sm = sizeof(C) * 3 * N + 64 * 8;
         for (Rank& k : ranks) {
             ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, k.twF4, k.twI4,
-                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB};
+                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB, k.Q0};
             if (fit_only)
                 zcol0r_kernel<N, ZM_FIT><<<NB, nt, sm, stream>>>(p, k.Z0full, k.rb0);
             else
@@ -803,8 +810,9 @@ struct DistImpl final : DistBase {
                                                                              k.x0keep, red + v);
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(k.anchor, k.x0keep, ghosted() * 4, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemsetAsync(k.Q0, 0, sizeof(C) * 3 * N * NB, stream));  // Y column 0 stays zero
             synth_weight_kernel<<<grid_for((size_t)N * NB * (Nh + 1), 256), 256, 0, stream>>>(
-                N, k.rb0, NB, seed, k.W, k.Wn);
+                N, k.rb0, NB, seed, k.W, k.Wn, k.Q0);
             CK(cudaGetLastError());
             xs.push_back(k.x0keep);
         }

@@ -61,7 +61,8 @@ static __device__ __forceinline__ void atomic_max_pos(unsigned long long* a, dou
 template <typename R>
 __global__ void convert_acc_kernel(int n, const double* __restrict__ W,
                                    const double* __restrict__ Y, R* Wm, R* Wn, Cx<R>* Ym,
-                                   Cx<R>* Yn, double* part, unsigned long long* maxes) {
+                                   Cx<R>* Yn, double* part, unsigned long long* maxes,
+                                   Cx<R>* Q0 = nullptr) {
     using C = Cx<R>;
     const int nh = n / 2;
     const size_t total = (size_t)n * n * (nh + 1);
@@ -113,6 +114,12 @@ __global__ void convert_acc_kernel(int n, const double* __restrict__ W,
             const size_t o = (size_t)c * n + b;
             Wn[o] = R(wp);
             Yn[o] = cx<C>(R(pr), R(pi));
+        }
+        if (Q0 && (a == 0 || a == nh)) {  // row-major column-0 copy (zcol0_kernel)
+            C* q = Q0 + ((size_t)b * n + c) * 3;
+            R* wq = reinterpret_cast<R*>(q);
+            wq[a == 0 ? 0 : 1] = R(wp);
+            q[a == 0 ? 1 : 2] = cx<C>(R(pr), R(pi));
         }
     }
     __shared__ double red[32 * 2];
@@ -266,6 +273,7 @@ struct Impl final : ImplBase {
     R* Wn = nullptr;
     C* Yh = nullptr;
     C* Yn = nullptr;
+    C* Q0 = nullptr;           // [N][N][3] column-0 inputs, row-major
     C* Z0 = nullptr;           // forward-transformed packed column 0 [N][N]
     C* twN = nullptr;
     float4* twF4 = nullptr;    // packed {w, i w} forward / inverse tables (fp32)
@@ -366,6 +374,7 @@ struct Impl final : ImplBase {
         CKS(dalloc(&Wn, NN));
         CKS(dalloc(&Yh, H));
         CKS(dalloc(&Yn, NN));
+        CKS(dalloc(&Q0, 3 * NN));
         CKS(dalloc(&Z0, NN));
         CKS(dalloc(&twN, N));
         CKS(dalloc(&stage, 3 * L));
@@ -568,7 +577,7 @@ struct Impl final : ImplBase {
     template <int MODE>
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
-        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N};
+        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0};
         dim3 grid(Nh / ZG::TW, N);
         CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
         if constexpr (MODE != ZM_FWD)
@@ -597,7 +606,7 @@ struct Impl final : ImplBase {
         CK(cudaMemsetAsync(maxes, 0, sizeof(unsigned long long) * 4, stream));
         const int blocks = grid_for(NN * (Nh + 1), 256);
         convert_acc_kernel<R><<<blocks, 256, 0, stream>>>(N, stage, stage + L, W, Wn, Yh, Yn,
-                                                          part_acc, maxes);
+                                                          part_acc, maxes, Q0);
         CK(cudaGetLastError());
         std::vector<double> parts(2 * (size_t)blocks);
         unsigned long long mx[4];

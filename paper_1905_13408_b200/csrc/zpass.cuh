@@ -32,6 +32,9 @@ template <typename R> struct ZMParams {
     double* part;   // [nblocks_main + N/2 + 1][NP3]
     DevState* st;
     int nrows;      // rows b of the spectrum block (N, or NB on a b-slab rank)
+    // column-0 inputs row-major for the column-0 kernels: Q0[(b*N + c)*3 + j] =
+    // {(W(0), W(N/2)), Yh(0), Y(N/2)} (the h = 0 entries of W/Yh are strided)
+    const Cx<R>* Q0;
 };
 
 #ifndef CM_Z_E8
@@ -77,7 +80,11 @@ template <typename R, int N> struct ZGeo {
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
     static constexpr size_t SMEM_MAIN = OFF_WSM + (WSM ? sizeof(R) * (size_t)N * TW : 0);
     static constexpr int MINB = NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
-    static constexpr int NT0 = 2 * Geo<R, N>::TY < 64 ? 64 : 2 * Geo<R, N>::TY;
+    // column-0 kernel: 8 elements per thread on power-of-two sides >= 256 (more
+    // warps per pair block: the kernel is latency bound with 257 blocks)
+    static constexpr int E0 = (N >= 256 && (N & (N - 1)) == 0) ? 8 : Geo<R, N>::EY;
+    static constexpr int T0 = N / E0;
+    static constexpr int NT0 = 2 * T0 < 64 ? 64 : 2 * T0;
     static constexpr size_t SMEM_COL0 =
         sizeof(Cx<R>) * (N + 5 * (size_t)N) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 1);
 };
@@ -215,11 +222,11 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
 }
 
 template <typename R, int N, int MODE>
-__global__ void __launch_bounds__(2 * Geo<R, N>::TY < 64 ? 64 : 2 * Geo<R, N>::TY)
+__global__ void __launch_bounds__(ZGeo<R, N>::NT0)
 zcol0_kernel(ZMParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
-    constexpr int T = G::TY, E = G::EY, Nh = G::Nh;
+    constexpr int T = ZGeo<R, N>::T0, E = ZGeo<R, N>::E0, Nh = G::Nh;
     pdl_trigger();
     pdl_wait();
     if (p.st && ld_done(p.st)) return;
@@ -255,10 +262,9 @@ zcol0_kernel(ZMParams<R> p) {
         // F0 = (Z + conj Zm)/2, FN = (Z - conj Zm)/(2i)
         const C f0 = cx<C>(R(0.5) * (zz.x + zm.x), R(0.5) * (zz.y - zm.y));
         const C fn = cx<C>(R(0.5) * (zz.y + zm.y), R(-0.5) * (zz.x - zm.x));
-        const size_t gi = ((size_t)c * N + b) * Nh;
-        const size_t ni = (size_t)c * N + b;
-        const R w0 = p.W[gi], wn = p.Wn[ni];
-        const C y0 = p.Yh[gi], yn = p.Yn[ni];
+        const C* q = p.Q0 + ((size_t)b * N + c) * 3;
+        const C wq = q[0], y0 = q[1], yn = q[2];
+        const R w0 = wq.x, wn = wq.y;
         if (active) {
             quad += (double)w0 * ((double)f0.x * f0.x + (double)f0.y * f0.y) +
                     (double)wn * ((double)fn.x * fn.x + (double)fn.y * fn.y);
