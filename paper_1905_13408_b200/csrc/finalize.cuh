@@ -78,72 +78,78 @@ static __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinParams 
     if (threadIdx.x != 0) return;
     }
 
-    const double fit = (s[NP1 + 0] - 2.0 * s[NP1 + 1]) * p.invL;
-    const int i = p.epilogue ? st->max_iters : st->iter;
-    double cur[7] = {fit,
-                     p.alpha * s[0],
-                     p.beta * s[1],
-                     p.beta * s[2],
-                     p.gamma * s[5],
-                     p.alpha * s[3],
-                     p.beta * s[4]};
-    if (st->audit && i > 0) {
-        double after[7];
-        for (int q = 0; q < 7; ++q) after[q] = cur[q];
-        if (st->refresh_inner) { // weights of x_{i-1} at x_i
-            after[1] = p.alpha * s[6];
-            after[2] = p.beta * s[7];
-            after[3] = p.beta * s[8];
+    // work on a register copy of the state: its fields load in one round trip
+    // instead of a chain of dependent global loads by one thread
+    DevState S = *st;
+    [&] {
+        const double fit = (s[NP1 + 0] - 2.0 * s[NP1 + 1]) * p.invL;
+        const int i = p.epilogue ? S.max_iters : S.iter;
+        double cur[7] = {fit,
+                         p.alpha * s[0],
+                         p.beta * s[1],
+                         p.beta * s[2],
+                         p.gamma * s[5],
+                         p.alpha * s[3],
+                         p.beta * s[4]};
+        if (S.audit && i > 0) {
+            double after[7];
+            for (int q = 0; q < 7; ++q) after[q] = cur[q];
+            if (S.refresh_inner) { // weights of x_{i-1} at x_i
+                after[1] = p.alpha * s[6];
+                after[2] = p.beta * s[7];
+                after[3] = p.beta * s[8];
+            }
+            const double sb = surrogate7(S.before);
+            const double sa = surrogate7(after);
+            const double slack = S.audit_slack * fmax(1.0, fabs(sb));
+            if (S.check_diverge && sa > sb + slack) {
+                S.diverged_iter = i - 1;
+                S.stop_reason = 3;
+                S.done = 1;
+                S.rows = i - 1;
+                return;
+            }
+            if (p.trace) {
+                double* row = p.trace + (size_t)(i - 1) * 15;
+                for (int q = 0; q < 7; ++q) row[q] = S.before[q];
+                for (int q = 0; q < 7; ++q) row[7 + q] = after[q];
+                row[14] = S.step;
+            }
+            S.rows = i;
+            if (S.tol_kind == 1) {
+                const double rel = fabs(sb - sa) / fmax(fabs(sb), 1e-300);
+                S.last_rel = rel;
+                if (!p.epilogue && rel < S.tol) {
+                    // stop with x_i as the result
+                    S.stop_reason = 2;
+                    S.done = 1;
+                    S.iter = i;
+                    return;
+                }
+            }
         }
-        const double sb = surrogate7(st->before);
-        const double sa = surrogate7(after);
-        const double slack = st->audit_slack * fmax(1.0, fabs(sb));
-        if (st->check_diverge && sa > sb + slack) {
-            st->diverged_iter = i - 1;
-            st->stop_reason = 3;
-            st->done = 1;
-            st->rows = i - 1;
-            return;
-        }
-        if (p.trace) {
-            double* row = p.trace + (size_t)(i - 1) * 15;
-            for (int q = 0; q < 7; ++q) row[q] = st->before[q];
-            for (int q = 0; q < 7; ++q) row[7 + q] = after[q];
-            row[14] = st->step;
-        }
-        st->rows = i;
-        if (st->tol_kind == 1) {
-            const double rel = fabs(sb - sa) / fmax(fabs(sb), 1e-300);
-            st->last_rel = rel;
-            if (!p.epilogue && rel < st->tol) {
-                // stop with x_i as the result
-                st->stop_reason = 2;
-                st->done = 1;
-                st->iter = i;
+        if (p.epilogue) return;
+        for (int q = 0; q < 7; ++q) S.before[q] = cur[q];
+        S.iter = i + 1;
+        if (S.tol_kind == 2) {
+            // scale-free step rule: ||x_{k+1} - x_k|| relative to the largest step so
+            // far (the first steps are tiny under the Lipschitz step of the TV term)
+            const double dn = sqrt(s[9]);
+            S.step_max = fmax(S.step_max, dn);
+            const double rel = dn / fmax(S.step_max, 1e-300);
+            S.last_rel = rel;
+            if (i >= 1 && rel < S.tol) {
+                S.stop_reason = 2;
+                S.done = 1;
                 return;
             }
         }
-    }
-    if (p.epilogue) return;
-    for (int q = 0; q < 7; ++q) st->before[q] = cur[q];
-    st->iter = i + 1;
-    if (st->tol_kind == 2) {
-        // scale-free step rule: ||x_{k+1} - x_k|| relative to the largest step so
-        // far (the first steps are tiny under the Lipschitz step of the TV term)
-        const double dn = sqrt(s[9]);
-        st->step_max = fmax(st->step_max, dn);
-        const double rel = dn / fmax(st->step_max, 1e-300);
-        st->last_rel = rel;
-        if (i >= 1 && rel < st->tol) {
-            st->stop_reason = 2;
-            st->done = 1;
-            return;
+        if (S.iter >= S.max_iters) {
+            S.stop_reason = 1;
+            S.done = 1;
         }
-    }
-    if (st->iter >= st->max_iters) {
-        st->stop_reason = 1;
-        st->done = 1;
-    }
+    }();
+    *st = S;
 }
 
 } // namespace cm
