@@ -84,7 +84,14 @@ zcol0r_kernel(ZMParams<float> p, const float2* Z0full, int rb0) {
     fft_regs<N, E, N, false>(v, act ? t : 0, buf + (act ? 0 : N), ColAddr{1, 0}, tw, BlockSync{});
     if (act)
 #pragma unroll
-        for (int m = 0; m < E; ++m) p.S[((size_t)(t + T * m) * p.nrows + bl) * Nh] = v[m];
+        for (int m = 0; m < E; ++m) p.S[((size_t)(t + T * m) * p.nrows + bl) * p.hlen] = v[m];
+}
+
+// b-slab layout of the packed half spectrum with split column halves:
+// [half][c][b_local][h - half N/4], each half one all-to-all (see SpecLayout)
+__host__ __device__ inline size_t bslab_index(int n, int nrows, int c, int bl, int a) {
+    const int hh = n / 4, half = a >= hh ? 1 : 0;
+    return (size_t)half * ((size_t)n * nrows * hh) + ((size_t)c * nrows + bl) * hh + (a - half * hh);
 }
 
 // Full-grid fp64 accumulator -> this rank's b rows of the packed half spectrum
@@ -108,7 +115,7 @@ __global__ static void convert_rows_kernel(int n, int rb0, int nrows, const doub
         const double sg = ((a + b + c) & 1) ? -1.0 : 1.0;
         const double pr = sg * 0.5 * (Y[2 * i] + Y[2 * m]), pi = sg * 0.5 * (Y[2 * i + 1] - Y[2 * m + 1]);
         if (a < nh) {
-            const size_t o = ((size_t)c * nrows + bl) * nh + a;
+            const size_t o = bslab_index(n, nrows, c, bl, a);
             Wm[o] = float(wp);
             Ym[o] = make_float2(float(pr), float(pi));
         } else {
@@ -189,7 +196,7 @@ __global__ static void synth_weight_kernel(int n, int rb0, int nrows, unsigned l
         const int am = a ? n - a : 0, bm = b ? n - b : 0, cm_ = c ? n - c : 0;
         const size_t i = ((size_t)c * n + b) * n + a, m = ((size_t)cm_ * n + bm) * n + am;
         const float w = float(1.0 + 0.5 * (hash_unit(seed ^ 0xABCDull, i) + hash_unit(seed ^ 0xABCDull, m)));
-        if (a < nh) Wm[((size_t)c * nrows + bl) * nh + a] = w;
+        if (a < nh) Wm[bslab_index(n, nrows, c, bl, a)] = w;
         else Wn[(size_t)c * nrows + bl] = w;
         if (a == 0 || a == nh) reinterpret_cast<float*>(Q0 + ((size_t)bl * n + c) * 3)[a == 0 ? 0 : 1] = w;
     }
@@ -197,13 +204,14 @@ __global__ static void synth_weight_kernel(int n, int rb0, int nrows, unsigned l
 
 // Yh = W * F (F: the spectrum of the volume, b-slab layout); packed column and
 // Nyquist plane zero (a valid Hermitian choice)
-__global__ static void synth_numerator_kernel(size_t count, int nh, const float* W, const float2* F,
-                                              float2* Yh, float2* Yn, size_t nyq) {
+__global__ static void synth_numerator_kernel(size_t count, int hh, size_t half, const float* W,
+                                              const float2* F, float2* Yh, float2* Yn, size_t nyq) {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < count;
          q += (size_t)gridDim.x * blockDim.x) {
         const float w = W[q];
         const float2 f = F[q];
-        Yh[q] = (q % nh) ? make_float2(w * f.x, w * f.y) : make_float2(0.f, 0.f);
+        const bool col0 = q < half && (q % hh) == 0;  // global column h = 0
+        Yh[q] = col0 ? make_float2(0.f, 0.f) : make_float2(w * f.x, w * f.y);
         if (q < nyq) Yn[q] = make_float2(0.f, 0.f);
     }
 }
@@ -281,6 +289,9 @@ struct DistImpl final : DistBase {
 
     ~DistImpl() override {
         for (void* p : allocs) cudaFree(p);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (cstream) cudaStreamDestroy(cstream);
         if (stream) cudaStreamDestroy(stream);
     }
     template <typename T>
@@ -313,6 +324,10 @@ struct DistImpl final : DistBase {
             return fail(CM_ERR_INVALID_ARGUMENT, "z-slab decomposition needs N/P a multiple of 64");
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (Nh % 2 || Hh % ZG::TW || Hh % Geo<R, N>::TWY)
+            return fail(CM_ERR_UNSUPPORTED, "z-slab solver: column halves do not tile");
         std::vector<C> tw(N);
         for (int q = 0; q < N; ++q) {
             const double a = -2.0 * M_PI * q / N;
@@ -452,32 +467,62 @@ struct DistImpl final : DistBase {
     }
 
     // ---- per-phase launches on every local rank ---------------------------------------
-    SpecLayout nat_layout() const { return spec_layout((long long)N * Nh, 0, N); }
-    SpecLayout dm_layout() const { return spec_layout((long long)NB * Nh, (long long)NK * NB * Nh, NB); }
+    // ---- per-phase launches on every local rank -------------------------------------
+    // The spectrum's columns h are split into two halves (Hh = N/4 columns each)
+    // stored one after the other in the b-slab (Srecv, W, Yh) and the
+    // destination-major (Ssend) layouts, so each half has its own contiguous
+    // all-to-all and the transposes of one half overlap the transforms of the
+    // other (collectives on `cstream`, ordered by events).
+    static constexpr int Hh = Nh / 2;
+    size_t half_elems() const { return (size_t)NK * N * Hh; }  // = N * NB * Hh
+    SpecLayout nat_layout() const { return spec_layout((long long)N * Nh, 0, N, Nh); }
+    SpecLayout dm_layout() const {
+        return spec_layout((long long)NB * Hh, (long long)NK * NB * Hh, NB, Hh, (long long)half_elems());
+    }
+    cudaStream_t cstream = nullptr;  // collectives
+    enum Ev { EV_ZA, EV_AG, EV_ZB, EV_C0, EV_IA, EV_IB, EV_ST, EV_HALO, EV_FL, EV_AR, EV_YA, EV_YB,
+              EV_FA, EV_FB, EV_N };
+    cudaEvent_t ev[EV_N] = {};
+    int record(Ev e, cudaStream_t s) {
+        CK(cudaEventRecord(ev[e], s));
+        return CM_OK;
+    }
+    int wait(Ev e, cudaStream_t s) {
+        CK(cudaStreamWaitEvent(s, ev[e], 0));
+        return CM_OK;
+    }
 
-    int z_pass(bool fit_only, bool with_part) {
+    int zmain_half(int half, bool fit_only, bool with_part) {
         for (Rank& k : ranks) {
-            ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, k.twF4, k.twI4,
-                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB, k.Q0};
-            dim3 grid(Nh / ZG::TW, NB);
+            const size_t off = (size_t)half * half_elems();
+            double* part = with_part ? k.part3 + (size_t)half * (Hh / ZG::TW) * NB * NP3 : nullptr;
+            ZMParams<R> p{k.Srecv + off, k.Z0, k.W + off, k.Wn, k.Yh + off, k.Yn, k.twN, k.twF4,
+                          k.twI4, part, fit_only ? nullptr : k.st, NB, k.Q0, Hh, half * Hh};
+            dim3 grid(Hh / ZG::TW, NB);
             if (fit_only)
                 zmain_kernel<R, N, ZM_FIT, 0><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
             else
                 zmain_kernel<R, N, ZM_FULL, 0><<<grid, ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
             CK(cudaGetLastError());
         }
+        return CM_OK;
+    }
+    int gather_col0() {  // on cstream
         std::vector<void*> mine, all;
         for (Rank& k : ranks) {
             mine.push_back(k.Z0);
             all.push_back(k.Z0full);
         }
-        if (comm->all_gather(mine, all, sizeof(C) * NB * N, stream))
+        if (comm->all_gather(mine, all, sizeof(C) * NB * N, cstream))
             return fail(CM_ERR_NCCL, "all_gather (column 0) failed");
+        return CM_OK;
+    }
+    int zcol0(bool fit_only, bool with_part) {  // column 0 lives in half 0
         const int nt = Geo<R, N>::TY < 32 ? 32 : Geo<R, N>::TY;
         const size_t sm = sizeof(C) * 3 * N + 64 * 8;
         for (Rank& k : ranks) {
             ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, k.twF4, k.twI4,
-                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB, k.Q0};
+                          with_part ? k.part3 : nullptr, fit_only ? nullptr : k.st, NB, k.Q0, Hh, 0};
             if (fit_only)
                 zcol0r_kernel<N, ZM_FIT><<<NB, nt, sm, stream>>>(p, k.Z0full, k.rb0);
             else
@@ -486,31 +531,75 @@ struct DistImpl final : DistBase {
         }
         return CM_OK;
     }
-    int a2a(bool forward) {  // forward: Ssend -> Srecv (z-slab -> b-slab)
+    // all-to-all of one column half on cstream; forward: z-slab -> b-slab
+    int a2a_half(bool forward, int half) {
         if (P == 1) return CM_OK;
         std::vector<void*> s, r;
+        const size_t off = (size_t)half * half_elems();
         for (Rank& k : ranks) {
-            s.push_back(forward ? k.Ssend : k.Srecv);
-            r.push_back(forward ? k.Srecv : k.Ssend);
+            s.push_back((forward ? k.Ssend : k.Srecv) + off);
+            r.push_back((forward ? k.Srecv : k.Ssend) + off);
         }
-        if (comm->all_to_all(s, r, sizeof(C) * NK * NB * Nh, stream))
+        if (comm->all_to_all(s, r, sizeof(C) * NK * NB * Hh, cstream))
             return fail(CM_ERR_NCCL, "all_to_all failed");
         return CM_OK;
     }
-    int y_pass(bool fwd, bool use_st) {
+    int y_half(bool fwd, bool use_st, int half) {
+        constexpr int TWY = Geo<R, N>::TWY;
         for (Rank& k : ranks) {
             const int* stop = use_st ? (fwd ? &k.st->done_y : &k.st->done) : nullptr;
             YParams<R> p{fwd ? k.Snat : k.Ssend, k.twN, nullptr, stop, fwd ? k.Ssend : k.Snat,
-                         fwd ? nat_layout() : dm_layout(), fwd ? dm_layout() : nat_layout(), NK};
-            const int grid = std::min((Nh / Geo<R, N>::TWY) * NK, ygrid);
+                         fwd ? nat_layout() : dm_layout(), fwd ? dm_layout() : nat_layout(), NK,
+                         half * (Hh / TWY), Hh / TWY};
+            const int grid = std::min((Hh / TWY) * NK, ygrid);
             if (fwd)
                 ypass_kernel<R, N, true, true>
-                    <<<grid, Geo<R, N>::TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);
+                    <<<grid, TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);
             else
                 ypass_kernel<R, N, false, true>
-                    <<<grid, Geo<R, N>::TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);
+                    <<<grid, TWY * Geo<R, N>::TY, YSmem<R, N>::bytes, stream>>>(p);
             CK(cudaGetLastError());
         }
+        return CM_OK;
+    }
+    // forward transform of the iterate in Snat... -> b-slab Srecv, halves pipelined
+    int spectrum_forward(bool use_st) {
+        CKS(y_half(true, use_st, 0));
+        CKS(record(EV_YA, stream));
+        CKS(wait(EV_YA, cstream));
+        CKS(a2a_half(true, 0));
+        CKS(record(EV_FA, cstream));
+        CKS(y_half(true, use_st, 1));
+        CKS(record(EV_YB, stream));
+        CKS(wait(EV_YB, cstream));
+        CKS(a2a_half(true, 1));
+        CKS(record(EV_FB, cstream));
+        return CM_OK;
+    }
+    // z pass on both halves + column 0, transposed back to z-slabs, y inverse
+    int spectrum_inverse(bool fit_only, bool with_part, bool use_st) {
+        CKS(wait(EV_FA, stream));
+        CKS(zmain_half(0, fit_only, with_part));
+        CKS(record(EV_ZA, stream));
+        CKS(wait(EV_ZA, cstream));
+        CKS(gather_col0());
+        CKS(record(EV_AG, cstream));
+        CKS(wait(EV_FB, stream));
+        CKS(zmain_half(1, fit_only, with_part));
+        CKS(record(EV_ZB, stream));
+        CKS(wait(EV_AG, stream));
+        CKS(zcol0(fit_only, with_part));
+        if (fit_only) return CM_OK;
+        CKS(record(EV_C0, stream));
+        CKS(wait(EV_C0, cstream));
+        CKS(a2a_half(false, 0));
+        CKS(record(EV_IA, cstream));
+        CKS(a2a_half(false, 1));  // after zmain(B): EV_C0 follows EV_ZB on the compute stream
+        CKS(record(EV_IB, cstream));
+        CKS(wait(EV_IA, stream));
+        CKS(y_half(false, use_st, 0));
+        CKS(wait(EV_IB, stream));
+        CKS(y_half(false, use_st, 1));
         return CM_OK;
     }
     int x_fft(int dir, std::vector<R*> real, bool use_st) {
@@ -528,7 +617,7 @@ struct DistImpl final : DistBase {
         }
         return CM_OK;
     }
-    int halo(std::vector<R*> x) {
+    int halo(std::vector<R*> x) {  // on cstream
         std::vector<void*> lo, hi, glo, ghi;
         for (size_t v = 0; v < ranks.size(); ++v) {
             lo.push_back(x[v] + NN);
@@ -536,7 +625,7 @@ struct DistImpl final : DistBase {
             glo.push_back(x[v]);
             ghi.push_back(x[v] + (size_t)(NK + 1) * NN);
         }
-        if (comm->halo(lo, hi, glo, ghi, 4 * NN, stream)) return fail(CM_ERR_NCCL, "halo failed");
+        if (comm->halo(lo, hi, glo, ghi, 4 * NN, cstream)) return fail(CM_ERR_NCCL, "halo failed");
         return CM_OK;
     }
     int finalize(const FinParams& base, bool with_part3, int nb3) {
@@ -545,10 +634,14 @@ struct DistImpl final : DistBase {
                                                     with_part3 ? k.part3 : nullptr, nb3, k.sums);
             CK(cudaGetLastError());
         }
+        CKS(record(EV_FL, stream));
+        CKS(wait(EV_FL, cstream));
         std::vector<double*> sums;
         for (Rank& k : ranks) sums.push_back(k.sums);
-        if (comm->all_reduce_sum(sums, NP1 + NP3, stream))
+        if (comm->all_reduce_sum(sums, NP1 + NP3, cstream))
             return fail(CM_ERR_NCCL, "all_reduce failed");
+        CKS(record(EV_AR, cstream));
+        CKS(wait(EV_AR, stream));
         for (Rank& k : ranks) {
             FinParams f = base;
             f.st = k.st;
@@ -557,6 +650,12 @@ struct DistImpl final : DistBase {
             finalize_kernel<<<1, FIN_THREADS, 0, stream>>>(f);
             CK(cudaGetLastError());
         }
+        return CM_OK;
+    }
+    // both streams drained (end of a solve / before host reads)
+    int drain() {
+        CK(cudaStreamSynchronize(cstream));
+        CK(cudaStreamSynchronize(stream));
         return CM_OK;
     }
 
@@ -644,7 +743,11 @@ struct DistImpl final : DistBase {
         if (wfixed) {  // the sweep reads w_tv on the ghost plane above the slab
             std::vector<R*> wv;
             for (Rank& k : ranks) wv.push_back(k.wtvf);
+            CKS(record(EV_ST, stream));
+            CKS(wait(EV_ST, cstream));
             CKS(halo(wv));
+            CKS(record(EV_HALO, cstream));
+            CKS(wait(EV_HALO, stream));
         }
 
         cudaEvent_t e0, e1;
@@ -720,26 +823,27 @@ struct DistImpl final : DistBase {
             std::vector<R*> x0;
             for (Rank& k : ranks) x0.push_back(fista ? k.YF[0] : k.X[0]);
             CKS(x_fft(1, x0, false));
-            CKS(y_pass(true, false));
-            CKS(a2a(true));
+            CKS(spectrum_forward(false));
         }
         int launches = 0;
         for (int g = 0; g < K; ++g) {
-            CKS(z_pass(false, audit));               // K3 on the b rows (+ Z0 all-gather)
-            CKS(a2a(false));                         // b-slab -> z-slab
-            CKS(y_pass(false, true));                // K4
+            // K3 (two column halves) + column 0, transposes, K4 (pipelined)
+            CKS(spectrum_inverse(false, audit, true));
             CKS(x_fft(0, gbufs, true));              // K1a: g
             CKS(stencil(g, false));                  // K1b
             const std::vector<R*> nx = next_iterate(g);
-            CKS(halo(nx));                           // ghost planes of the new iterate
+            CKS(record(EV_ST, stream));              // ghost planes of the new iterate
+            CKS(wait(EV_ST, cstream));               // (overlap the finalize)
+            CKS(halo(nx));
+            CKS(record(EV_HALO, cstream));
             FinParams f = fb;
             f.part1 = need_part1 ? ranks[0].part1 : nullptr;
             f.trace = want_trace ? ranks[0].trace : nullptr;
             CKS(finalize(f, audit, nb3));            // FIN (local -> all-reduce -> audit)
+            CKS(wait(EV_HALO, stream));
             CKS(x_fft(1, nx, true));                 // K1c
-            CKS(y_pass(true, true));                 // K2
-            CKS(a2a(true));                          // z-slab -> b-slab
-            launches += 9;
+            CKS(spectrum_forward(true));             // K2 + z-slab -> b-slab (pipelined)
+            launches += 13;
             // every rank holds identical device state after the all-reduce, so
             // every rank takes the same decision from its own copy
             if ((g & 7) == 7 || g == K - 1) {
@@ -749,13 +853,16 @@ struct DistImpl final : DistBase {
                 if (done) break;
             }
         }
+        // the last forward transposes run on cstream
+        CKS(wait(EV_FA, stream));
+        CKS(wait(EV_FB, stream));
         DevState rs;
         CK(cudaMemcpyAsync(&rs, ranks[0].st, sizeof(rs), cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
+        CKS(drain());
         if (audit && rs.stop_reason == 1) {
             // close the last trace row (regularizer.cpp:208): fit(x_K) and the
             // penalties of x_K under the weights of iteration K-1
-            CKS(z_pass(true, true));
+            CKS(spectrum_inverse(true, true, false));
             CKS(stencil(rs.iter, true));
             FinParams f = fb;
             f.part1 = ranks[0].part1;
@@ -766,7 +873,7 @@ struct DistImpl final : DistBase {
             CK(cudaMemcpyAsync(&rs, ranks[0].st, sizeof(rs), cudaMemcpyDeviceToHost, stream));
         }
         CK(cudaEventRecord(e1, stream));
-        CK(cudaStreamSynchronize(stream));
+        CKS(drain());
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, e0, e1));
         cudaEventDestroy(e0);
@@ -818,24 +925,33 @@ struct DistImpl final : DistBase {
         }
         // F = fft3 of the volume through the solver's own transforms
         CKS(x_fft(1, xs, false));
-        CKS(y_pass(true, false));
-        CKS(a2a(true));
+        CKS(spectrum_forward(false));
+        CKS(wait(EV_FA, stream));
+        CKS(wait(EV_FB, stream));
         for (Rank& k : ranks) {
-            ZMParams<R> p{k.Srecv, k.Z0, k.W, k.Wn, k.Yh, k.Yn, k.twN, nullptr, nullptr,
-                          nullptr, nullptr, NB};
-            zmain_kernel<R, N, ZM_FWD, 0><<<dim3(Nh / ZG::TW, NB), ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
-            CK(cudaGetLastError());
+            for (int half = 0; half < 2; ++half) {
+                const size_t off = (size_t)half * half_elems();
+                ZMParams<R> p{k.Srecv + off, k.Z0, k.W + off, k.Wn, k.Yh + off, k.Yn, k.twN,
+                              nullptr, nullptr, nullptr, nullptr, NB, k.Q0, Hh, half * Hh};
+                zmain_kernel<R, N, ZM_FWD, 0>
+                    <<<dim3(Hh / ZG::TW, NB), ZG::NT, ZG::SMEM_MAIN, stream>>>(p);
+                CK(cudaGetLastError());
+            }
             const size_t cnt = (size_t)N * NB * Nh;
             synth_numerator_kernel<<<grid_for(cnt, 256), 256, 0, stream>>>(
-                cnt, Nh, k.W, k.Srecv, k.Yh, k.Yn, (size_t)N * NB);
+                cnt, Hh, half_elems(), k.W, k.Srecv, k.Yh, k.Yn, (size_t)N * NB);
             CK(cudaGetLastError());
         }
         std::vector<double*> rv;
         for (size_t v = 0; v < ranks.size(); ++v) rv.push_back(red + v);
-        if (comm->all_reduce_sum(rv, 1, stream)) return fail(CM_ERR_NCCL, "all_reduce failed");
+        CKS(record(EV_ST, stream));
+        CKS(wait(EV_ST, cstream));
+        if (comm->all_reduce_sum(rv, 1, cstream)) return fail(CM_ERR_NCCL, "all_reduce failed");
+        CKS(record(EV_AR, cstream));
+        CKS(wait(EV_AR, stream));
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, red, 8, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
+        CKS(drain());
         cudaFree(red);
         allocs.erase(std::find(allocs.begin(), allocs.end(), (void*)red));
         if (s_y) *s_y = std::sqrt(h / (double)(NN * N));

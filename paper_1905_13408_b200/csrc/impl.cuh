@@ -529,9 +529,9 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
     int launch_y(bool fwd, DevState* s) {
-        const SpecLayout nat = spec_layout((long long)N * Nh, 0, N);
+        const SpecLayout nat = spec_layout((long long)N * Nh, 0, N, Nh);
         YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr,
-                     nullptr, nat, nat, N};
+                     nullptr, nat, nat, N, 0, Nh / G::TWY};
         const int grid = std::min((Nh / G::TWY) * N, ygrid);  // persistent
         if (fwd)
             CK(launch_pdl(use_pdl, ypass_kernel<R, N, true>, dim3(grid), dim3(G::TWY * G::TY),
@@ -577,7 +577,7 @@ struct Impl final : ImplBase {
     template <int MODE>
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
-        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0};
+        ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
         dim3 grid(Nh / ZG::TW, N);
         CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
         if constexpr (MODE != ZM_FWD)

@@ -96,18 +96,26 @@ template <typename R> struct ZParams {
 // natural [k][b][h]: kstride = N*Nh, nb = N, sstride = 0; destination-major
 // [s][k][b_local][h] of a z-slab rank (the all-to-all send/receive layout):
 // kstride = nb*Nh, sstride = NK*nb*Nh.
+// z-slab ranks may also split the columns h into two halves stored one after
+// the other (hh columns per row, the second half at +hstride) so that each half
+// is transposed by its own all-to-all (comm/compute overlap, dist.cuh).
 struct SpecLayout {
     long long kstride, sstride;
     int nb;
     float inv_nb;  // 1/nb: b = s nb + b_local without an integer division
-    __device__ __forceinline__ long long at(int k, int b, int h, int Nh) const {
+    int hh;        // columns per stored row (Nh, or Nh/2 with split halves)
+    long long hstride;
+    __device__ __forceinline__ long long at(int k, int b, int h, int) const {
         // exact: (b + 1/2)/nb is at least 1/(2 nb) away from an integer, b < 2^12
         const int s = __float2int_rz(((float)b + 0.5f) * inv_nb);
-        return (long long)k * kstride + (long long)s * sstride + (long long)(b - s * nb) * Nh + h;
+        const int hq = h >= hh ? 1 : 0;
+        return (long long)hq * hstride + (long long)k * kstride + (long long)s * sstride +
+               (long long)(b - s * nb) * hh + (h - hq * hh);
     }
 };
-inline SpecLayout spec_layout(long long kstride, long long sstride, int nb) {
-    return {kstride, sstride, nb, 1.0f / (float)nb};
+inline SpecLayout spec_layout(long long kstride, long long sstride, int nb, int hh,
+                              long long hstride = 0) {
+    return {kstride, sstride, nb, 1.0f / (float)nb, hh, hstride};
 }
 
 template <typename R> struct YParams {
@@ -119,6 +127,7 @@ template <typename R> struct YParams {
     C* Sout;            // output spectrum (may equal S), or null for in place
     SpecLayout lin, lout;
     int nplanes;        // planes k (N, or NK on a z-slab rank)
+    int htile0, htiles; // column tiles [htile0, htile0 + htiles) (0, Nh/TWY: all)
 };
 
 template <typename C>
@@ -161,10 +170,10 @@ ypass_kernel(YParams<R> p) {
     const int col = threadIdx.x % G::TWY;
     const int t = threadIdx.x / G::TWY;
     // persistent over (column tile, plane): the twiddle table is staged once
-    constexpr int NTX = G::Nh / G::TWY;
+    const int NTX = p.htiles;
     const int ntiles = NTX * p.nplanes;
     for (int tile = blockIdx.y * gridDim.x + blockIdx.x; tile < ntiles; tile += gridDim.x * gridDim.y) {
-    const int h = (tile % NTX) * G::TWY + col;
+    const int h = (p.htile0 + tile % NTX) * G::TWY + col;
     const int k = tile / NTX;
     C v[G::EY];
     if constexpr (!DM) {  // natural layout, in place

@@ -35,6 +35,9 @@ template <typename R> struct ZMParams {
     // column-0 inputs row-major for the column-0 kernels: Q0[(b*N + c)*3 + j] =
     // {(W(0), W(N/2)), Yh(0), Y(N/2)} (the h = 0 entries of W/Yh are strided)
     const Cx<R>* Q0;
+    // b-slab ranks with split column halves: stored row length and the first
+    // (global) column of this launch; one GPU: N/2 and 0 (compile-time there)
+    int hlen, h0;
 };
 
 #ifndef CM_Z_E8
@@ -117,18 +120,21 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     const int col = threadIdx.x % TW;
     const int t = threadIdx.x / TW;
     const int nrows = NR ? NR : p.nrows;
+    const int hl = NR ? Nh : p.hlen;  // stored row length
+    const int h0 = NR ? 0 : p.h0;     // first global column of this launch
     // one (column tile, row b) per CTA: a persistent loop here costs registers
     // (spills at 64 per thread) for less than the twiddle staging it saves
-    constexpr int NTX = Nh / TW;
+    const int NTX = hl / TW;
     const int tile = blockIdx.y * gridDim.x + blockIdx.x;
     if (tile >= NTX * nrows) return;
-    const int h = (tile % NTX) * TW + col;
+    const int hloc = (tile % NTX) * TW + col;
+    const int h = h0 + hloc;
     const int b = tile / NTX;  // local row
     [[maybe_unused]] R* wsm = reinterpret_cast<R*>(smem_raw + ZGeo<R, N>::OFF_WSM);
     if constexpr (ZGeo<R, N>::WSM && MODE != ZM_FWD) {
         constexpr int CH = TW * (int)sizeof(R) / 16;  // 16-byte chunks per row
-        const R* wrow = p.W + (size_t)b * Nh + (tile % NTX) * TW;
-        const size_t wstride = (size_t)nrows * Nh;
+        const R* wrow = p.W + (size_t)b * hl + (tile % NTX) * TW;
+        const size_t wstride = (size_t)nrows * hl;
         for (int q = threadIdx.x; q < N * CH; q += blockDim.x) {
             const int c = q / CH, part = q % CH;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -138,8 +144,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    const size_t plane = (size_t)nrows * Nh;
-    C* base = p.S + (size_t)b * Nh + h;
+    const size_t plane = (size_t)nrows * hl;
+    C* base = p.S + (size_t)b * hl + hloc;
     C v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = base[(size_t)(t + T * m) * plane];
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     if constexpr (PREFETCH || PFW) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const size_t gi = ((size_t)(t + T * m) * nrows + b) * Nh + h;
+            const size_t gi = ((size_t)(t + T * m) * nrows + b) * hl + hloc;
             w[m] = __ldg(p.W + gi);
             if constexpr (PREFETCH) y[m] = __ldg(p.Yh + gi);
         }
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
             if constexpr (!PREFETCH) {
 #pragma unroll
                 for (int m = g0; m < g0 + G; ++m) {
-                    const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * Nh + h;
+                    const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * hl + hloc;
                     if constexpr (ZGeo<R, N>::WSM) w[m] = wsm[(t + T * m) * TW + col];
                     else if constexpr (!PFW) w[m] = __ldg(p.W + gi);
                     y[m] = p.Yh[gi];

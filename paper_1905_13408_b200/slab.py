@@ -9,8 +9,10 @@ One process per GPU. Rank r of P owns real-space planes k in [r NK, (r+1) NK)
     finalize (local partials -> all-reduce) -> x R2C -> y forward
     all-to-all (z-slab -> b-slab)
 
-The y passes write the all-to-all send layout directly ([s][k][b_local][h],
-``SlabPlan.dm_offset``), so the transposes need no packing kernels.
+The y passes write the all-to-all send layout directly ([half][s][k][b_local][h],
+``SlabPlan.dm_offset``), so the transposes need no packing kernels; the two
+column halves are transposed separately, overlapping the other half's
+transforms (collectives on their own stream).
 
 ``SlabPlan`` is the host-side arithmetic of that decomposition (the same
 numbers dist.cuh uses); ``SlabContext`` drives the device solver. With
@@ -72,14 +74,24 @@ class SlabPlan:
             out.append(k if 0 <= k < self.n else None)
         return out
 
-    # destination-major spectrum layout [s][k_local][b_local][h] (kernels.cuh SpecLayout)
+    @property
+    def hh(self) -> int:  # columns per half: the spectrum's h range is split in two
+        return self.nh // 2
+
+    def half_elems(self) -> int:
+        """Complex elements of one column half of a rank's spectrum block."""
+        return self.nk * self.n * self.hh
+
+    # destination-major spectrum layout with split column halves
+    # [half][s][k_local][b_local][h - half hh] (kernels.cuh SpecLayout)
     def dm_offset(self, k_local: int, b: int, h: int) -> int:
         s, bl = divmod(b, self.nb)
-        return ((s * self.nk + k_local) * self.nb + bl) * self.nh + h
+        half, hl = divmod(h, self.hh)
+        return half * self.half_elems() + ((s * self.nk + k_local) * self.nb + bl) * self.hh + hl
 
     def chunk_elems(self) -> int:
-        """Complex elements each rank sends to each other rank per transpose."""
-        return self.nk * self.nb * self.nh
+        """Complex elements each rank sends to each other rank per half transpose."""
+        return self.nk * self.nb * self.hh
 
     def halo_neighbours(self, rank: int) -> tuple[int | None, int | None]:
         lo = rank - 1 if rank > 0 else None
@@ -87,10 +99,11 @@ class SlabPlan:
         return lo, hi
 
     def exchange_bytes_per_iteration(self) -> int:
-        """Bytes each rank sends per iteration (fp32): two all-to-alls, the
-        column-0 all-gather, two halo planes and the partial-sum all-reduce."""
+        """Bytes each rank sends per iteration (fp32): two transposes of two column
+        halves, the column-0 all-gather, two halo planes and the partial-sum
+        all-reduce."""
         p = self.world
-        a2a = 2 * (p - 1) * self.chunk_elems() * 8
+        a2a = 2 * 2 * (p - 1) * self.chunk_elems() * 8
         z0 = (p - 1) * self.nb * self.n * 8
         halo = 2 * self.n * self.n * 4
         return a2a + z0 + halo + 13 * 8

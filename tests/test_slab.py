@@ -36,11 +36,12 @@ def test_plan_arithmetic():
     assert p.ghosted_planes(3)[-1] is None
     assert p.halo_neighbours(0) == (None, 1) and p.halo_neighbours(3) == (2, None)
     # destination-major: chunk s (rows of rank s) is contiguous and chunk_elems long
-    offs = sorted(p.dm_offset(k, b, h) for k in range(2) for b in range(0, 512, 128)
-                  for h in (0, 255))
+    # destination-major with column halves: (half, peer) chunks are contiguous
+    assert p.hh == 128 and p.chunk_elems() == 128 * 128 * 128
     assert p.dm_offset(0, 128, 0) == p.chunk_elems()
-    assert p.dm_offset(p.nk - 1, p.nb - 1, p.nh - 1) == p.chunk_elems() - 1
-    assert offs[0] == 0
+    assert p.dm_offset(p.nk - 1, p.nb - 1, p.hh - 1) == p.chunk_elems() - 1
+    assert p.dm_offset(0, 0, p.hh) == p.half_elems() == 4 * p.chunk_elems()
+    assert p.dm_offset(p.nk - 1, 511, p.nh - 1) == 2 * p.half_elems() - 1
     with pytest.raises(cm.InvalidArgument):
         SlabPlan(100, 3)
 
@@ -73,16 +74,21 @@ def _slab_worker(rank: int, world: int, port: int, n: int, q):
         # x R2C + y forward on my planes, written destination-major
         Fxy = np.fft.fft(np.fft.rfft(mine, axis=2), axis=1)        # [kl][b][a]
         S = _pack_half(Fxy, n)                                      # [kl][b][h]
-        send = np.empty(world * plan.chunk_elems(), np.complex128)
+        hh = plan.hh
+        send = np.empty(2 * plan.half_elems(), np.complex128)
         for kl in range(nk):
             for b in range(n):
-                o = plan.dm_offset(kl, b, 0)
-                send[o:o + nh] = S[kl, b]
-        # all-to-all: chunk s -> rank s
+                for half in range(2):
+                    o = plan.dm_offset(kl, b, half * hh)
+                    send[o:o + hh] = S[kl, b, half * hh:(half + 1) * hh]
+        # one all-to-all per column half: chunk s -> rank s
         sv = torch.from_numpy(send.view(np.float64).copy())
         rv = torch.empty_like(sv)
-        dist.all_to_all_single(rv, sv)
-        recv = rv.numpy().view(np.complex128).reshape(world * nk, nb, nh)  # [c][bl][h]
+        he = 2 * plan.half_elems()  # float64 words per half
+        for half in range(2):
+            dist.all_to_all_single(rv[half * he:(half + 1) * he], sv[half * he:(half + 1) * he])
+        halves = rv.numpy().view(np.complex128).reshape(2, world * nk, nb, hh)  # [half][c][bl][hh]
+        recv = np.concatenate([halves[0], halves[1]], axis=2)                  # [c][bl][h]
         # z pass on my b rows
         Z = np.fft.fft(recv, axis=0)
         full = _pack_half(np.fft.fftn(x), n)                        # [c][b][h]
@@ -101,9 +107,10 @@ def _slab_worker(rank: int, world: int, port: int, n: int, q):
         F = np.fft.fftn(x)
         ok_pair = np.allclose(f0, F[c, b, 0], atol=1e-9 * n ** 3) and \
             np.allclose(fn, F[c, b, n // 2], atol=1e-9 * n ** 3)
-        # reverse transpose returns my planes
+        # reverse transposes return my planes
         back = torch.empty_like(rv)
-        dist.all_to_all_single(back, rv)
+        for half in range(2):
+            dist.all_to_all_single(back[half * he:(half + 1) * he], rv[half * he:(half + 1) * he])
         ok_back = np.array_equal(back.numpy(), sv.numpy())
         # halo: my last plane -> next rank's lower ghost, my first -> previous's upper
         lo_n, hi_n = plan.halo_neighbours(rank)
