@@ -89,3 +89,40 @@ def test_slab_8_ranks_at_512(p512):
     sc.close()
     _check_traces(_traces(t2), _traces(t1), 1e-6)
     assert _rel(x2, x1) <= 1e-6
+
+
+@pytest.mark.parametrize("n", [384, 768])
+def test_radix3_sides_fp32_vs_fp64(n):
+    """BASELINE config 5 side (384^3; 768^3 likewise): radix-3 plans, 3 x 128
+    stencil tiles; fp32 product kernels against the fp64 parity mode."""
+    p = synth.synthetic_problem(n, n_blobs=2000)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    s = cm.scale_data(acc, precision=64)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 5
+    t32, t64 = [], []
+    x32 = cm.m_step(acc, p.x0, p.x0, cfg, t32, precision=32)
+    x64 = cm.m_step(acc, p.x0, p.x0, cfg, t64, precision=64)
+    _check_traces(_traces(t32), _traces(t64), 1e-5)
+    assert _rel(x32, x64) <= 1e-4
+
+
+def test_slab_3_ranks_at_384():
+    from paper_1905_13408_b200.slab import SlabContext
+
+    n = 384
+    p = synth.synthetic_problem(n, n_blobs=2000)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    s = cm.scale_data(acc, precision=32)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 6
+    t1, t2 = [], []
+    x1 = cm.m_step(acc, p.x0, p.x0, cfg, t1, precision=32)
+    sc = SlabContext(n, 3)
+    sc.set_accumulator(acc)
+    sc.set_volumes(p.x0)
+    sc.solve(cfg, t2)
+    x2 = sc.get_volume()
+    sc.close()
+    _check_traces(_traces(t2), _traces(t1), 1e-6)
+    assert _rel(x2, x1) <= 1e-6
