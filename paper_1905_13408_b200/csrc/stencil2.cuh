@@ -244,11 +244,15 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         }
         __syncthreads();
 
-        for (int k = k0; k < k0 + KC; ++k) {
+        // one plane of the march; the rolling state alternates between two
+        // register sets (the loop is unrolled by two) instead of being copied
+        float x_nb[4], s_nb[4], gn_nb[4], ds_nb[4];
+        auto step = [&](int k, float (&x_cur)[4], float (&s_cur)[4], float (&gn_cur)[4],
+                        float (&ds_cur)[4], float (&x_nx)[4], float (&s_nx)[4],
+                        float (&gn_nx)[4], float (&ds_nx)[4]) {
             if (tid == 0) issue(k + 2);  // slot of plane k-2: released by the previous barrier
             wait(k + 1);
             // ---- s of plane k+1 on this warp's row
-            float x_nx[4], s_nx[4], gn_nx[4], ds_nx[4];
             s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx);
             apply_wtvf(k + 1, s_nx, gn_nx);
             float* Sn = Sn_ring;
@@ -390,19 +394,15 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     }
                 }
             }
-            // roll plane k+1 into place
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                x_cur[c] = x_nx[c];
-                s_cur[c] = s_nx[c];
-                gn_cur[c] = gn_nx[c];
-                ds_cur[c] = ds_nx[c];
-            }
             float* const sfree = Sc_ring;
             Sc_ring = Sn_ring;
             Sn_ring = Sx_ring;
             Sx_ring = sfree;
-            if (USED && ((k - k0) & 7) == 7) {
+        };
+        for (int k = k0; k < k0 + KC; k += 2) {
+            step(k, x_cur, s_cur, gn_cur, ds_cur, x_nb, s_nb, gn_nb, ds_nb);
+            step(k + 1, x_nb, s_nb, gn_nb, ds_nb, x_cur, s_cur, gn_cur, ds_cur);
+            if (USED && ((k + 1 - k0) & 7) == 7) {
 #pragma unroll
                 for (int q = 0; q < NP1; ++q)
                     if (USED & (1u << q)) {
