@@ -115,6 +115,12 @@ int cm_set_volumes(cm_ctx* ctx, const double* x_init, const double* x_anchor);
 int cm_solve(cm_ctx* ctx, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
              cm_solve_stats* stats);
 int cm_get_volume(cm_ctx* ctx, double* x_out);
+/* The spectrum of the resident solve result on the full complex grid (2*L
+ * interleaved doubles): centered=1 gives fft3_centered(x) (fourier.cpp:109),
+ * the V that em_refine computes after every m_step (refine.cpp:182) — here on
+ * the device, from the transforms the solver already owns; centered=0 gives
+ * fft3(x). The result volume stays resident. */
+int cm_get_spectrum(cm_ctx* ctx, int centered, double* out_interleaved);
 
 /* Diagnostics: when on, cm_solve launches every kernel individually between
  * CUDA events on the context stream (no graph) and accumulates per-kernel

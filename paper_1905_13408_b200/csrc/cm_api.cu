@@ -202,6 +202,12 @@ int cm_get_volume(cm_ctx* ctx, double* x_out) {
     return ctx->impl->get_volume(x_out);
 }
 
+int cm_get_spectrum(cm_ctx* ctx, int centered, double* out_interleaved) {
+    CTX_GUARD(ctx);
+    if (!out_interleaved) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    return ctx->impl->result_spectrum(out_interleaved, centered ? 1 : 0);
+}
+
 int cm_m_step(cm_ctx* ctx, const double* weight, const double* numerator, int finalized,
               const double* x_init, const double* x_anchor, const cm_reg_config* cfg,
               double* x_out, cm_trace_row* trace, int trace_cap, cm_solve_stats* stats) {

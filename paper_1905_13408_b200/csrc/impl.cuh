@@ -156,6 +156,45 @@ __global__ void to_double_kernel(const R* __restrict__ in, double* __restrict__ 
         out[q] = double(in[q]);
 }
 
+// Packed half spectrum (after the x R2C and the y, z forward passes: fft3 of
+// the volume) -> full complex fp64 grid, x fastest (fourier.hpp:6-9 layout);
+// centered: times (-1)^(a+b+c), i.e. fft3_centered (fourier.cpp:109)
+template <typename R>
+__global__ void unpack_full_kernel(int n, const Cx<R>* __restrict__ S, double* __restrict__ out,
+                                   int centered) {
+    const int nh = n / 2;
+    const size_t total = (size_t)n * n * n;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(q % n);
+        const size_t bc = q / n;
+        const int b = (int)(bc % n), c = (int)(bc / n);
+        const int bm = b ? n - b : 0, cm_ = c ? n - c : 0;
+        double re, im;
+        if (a > 0 && a < nh) {
+            const Cx<R> z = S[((size_t)c * n + b) * nh + a];
+            re = z.x;
+            im = z.y;
+        } else if (a > nh) {  // Friedel mate of (n - a, -b, -c)
+            const Cx<R> z = S[((size_t)cm_ * n + bm) * nh + (n - a)];
+            re = z.x;
+            im = -(double)z.y;
+        } else {  // column 0 carries F(0) + i F(n/2): separate with the mate
+            const Cx<R> z = S[((size_t)c * n + b) * nh], zm = S[((size_t)cm_ * n + bm) * nh];
+            if (a == 0) {
+                re = 0.5 * ((double)z.x + zm.x);
+                im = 0.5 * ((double)z.y - zm.y);
+            } else {
+                re = 0.5 * ((double)z.y + zm.y);
+                im = -0.5 * ((double)z.x - zm.x);
+            }
+        }
+        const double sg = (centered && ((a + b + c) & 1)) ? -1.0 : 1.0;
+        out[2 * q] = sg * re;
+        out[2 * q + 1] = sg * im;
+    }
+}
+
 // prox_l1 (regularizer.cpp:103-110), elementwise in fp64
 static __global__ void prox_kernel(const double* __restrict__ x, const double* __restrict__ t,
                             double* __restrict__ out, size_t L) {
@@ -212,6 +251,8 @@ struct ImplBase {
     virtual int objective(const double* x, const cm_reg_config* c, const double* anchor,
                           const double* wsrc, double* out7) = 0;
     virtual int fft3(const double* x, double* out) = 0;
+    // fft3_centered of the resident solve result (em_refine, refine.cpp:182)
+    virtual int result_spectrum(double* out, int centered) = 0;
     virtual long long bytes() const = 0;
 
     cudaStream_t stream = nullptr;
@@ -1122,35 +1163,27 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
 
+    // full complex grid of fft3(x) (or fft3_centered) of a device volume -> host
+    int spectrum_to_host(R* x, double* out, int centered) {
+        CKS(spectrum_of(x));
+        CKS(launch_z<ZM_FWD>(nullptr, nullptr));
+        unpack_full_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(N, S, stage, centered);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, stage, sizeof(double) * 2 * L, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return CM_OK;
+    }
+
     int fft3(const double* x, double* out) override {
         result_valid = false;
         CKS(upload_real(x, X[0]));
-        CKS(spectrum_of(X[0]));
-        CKS(launch_z<ZM_FWD>(nullptr, nullptr));
-        std::vector<C> h(H);
-        CK(cudaMemcpyAsync(h.data(), S, sizeof(C) * H, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        // unpack to the full grid: h in (0, Nh) direct + Friedel mate; column 0
-        // carries F(0,b,c) + i F(Nh,b,c)
-        auto put = [&](int a, int b, int c, double re, double im) {
-            const size_t i = ((size_t)c * N + b) * N + a;
-            out[2 * i] = re;
-            out[2 * i + 1] = im;
-        };
-        for (int c = 0; c < N; ++c)
-            for (int b = 0; b < N; ++b) {
-                const int bm = (N - b) % N, cmt = (N - c) % N;
-                for (int a = 1; a < Nh; ++a) {
-                    const C z = h[((size_t)c * N + b) * Nh + a];
-                    put(a, b, c, z.x, z.y);
-                    put(N - a, bm, cmt, z.x, -z.y);
-                }
-                const C z = h[((size_t)c * N + b) * Nh];
-                const C zm = h[((size_t)cmt * N + bm) * Nh];
-                put(0, b, c, 0.5 * ((double)z.x + zm.x), 0.5 * ((double)z.y - zm.y));
-                put(Nh, b, c, 0.5 * ((double)z.y + zm.y), -0.5 * ((double)z.x - zm.x));
-            }
-        return CM_OK;
+        return spectrum_to_host(X[0], out, 0);
+    }
+
+    int result_spectrum(double* out, int centered) override {
+        if (!vol_set || !result_valid) return fail(CM_ERR_STATE, "no solver result resident");
+        R* src = last_fista ? XF[last_iter % 2] : X[last_iter % 3];
+        return spectrum_to_host(src, out, centered);  // the result buffer itself is untouched
     }
 };
 

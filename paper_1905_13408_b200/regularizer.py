@@ -283,6 +283,13 @@ class Context:
         return SolveStats(st.iterations, st.trace_rows, st.stop_reason, st.diverged_iter,
                           st.last_rel, st.step, st.solve_ms, st.kernel_launches)
 
+    def get_spectrum(self, centered: bool = True) -> np.ndarray:
+        """fft3_centered (or fft3) of the resident solve result, complex128 (n, n, n):
+        em_refine's V = fft3_centered(x) after m_step (refine.cpp:182), on the device."""
+        out = np.empty((self.n,) * 3, dtype=np.complex128)
+        _check(self.lib.cm_get_spectrum(self.ptr, int(bool(centered)), out.ctypes.data))
+        return out
+
     def set_profiling(self, on: bool) -> None:
         _check(self.lib.cm_set_profiling(self.ptr, int(bool(on))))
 
@@ -356,6 +363,29 @@ def m_step(acc: AccumulatorPair, x_init, x_anchor, config: RegConfig,
     if stats is not None:
         stats.update(st.__dict__)
     return ctx.get_volume()
+
+
+def em_m_step(acc: AccumulatorPair, x, eps: float, eps_prime: float,
+              mult: Multipliers | None = None, inner_iters: int = 24,
+              refresh: Refresh = Refresh.per_inner, convex_mode: bool = False,
+              precision: int | None = None, extra: dict | None = None):
+    """em_refine's regularized M-step block (refine.cpp:175-183) on one resident
+    context: scale_data -> derive_config -> m_step(acc, x, x) -> V =
+    fft3_centered(x). Returns (x_new, V); `extra` sets RegConfig extensions
+    (momentum, tol_kind, tol). The data scales and V are computed on the device
+    (no host FFT; the reference does two full-grid FFTs here per half-map)."""
+    ctx = context(acc.side_n, precision)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    cfg = derive_config(s.s_y, s.s_n, eps, eps_prime, mult)
+    cfg.inner_iters = inner_iters
+    cfg.refresh = refresh
+    cfg.convex_mode = convex_mode
+    for k, v in (extra or {}).items():
+        setattr(cfg, k, v)
+    ctx.set_volumes(x, x)
+    ctx.solve(cfg)
+    return ctx.get_volume(), ctx.get_spectrum(centered=True)
 
 
 def data_gradient(x, acc: AccumulatorPair, precision: int | None = None) -> np.ndarray:

@@ -366,3 +366,20 @@ def test_config2_reweighting_loops_vs_oracle(O, prec):
         x_gpu = ctx.get_volume()
         x_ref = xo
     assert rel_l2(x_gpu, x_ref) <= 3 * TOL[prec]["vol"]
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_em_m_step_block_returns_centered_spectrum(prec):
+    """refine.cpp:175-183: scale_data -> derive_config -> m_step -> V =
+    fft3_centered(x), with V from the device (cm_get_spectrum) against numpy."""
+    n = 64
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    x, V = cm.em_m_step(acc, p.x0, p.eps, p.eps_prime, inner_iters=6, precision=prec)
+    s = cm.scale_data(acc, precision=prec)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 6
+    np.testing.assert_array_equal(x, cm.m_step(acc, p.x0, p.x0, cfg, precision=prec))
+    want = np.fft.fftn(synth.halfshift3(x))
+    tol = 1e-12 if prec == 64 else 2e-6
+    assert np.abs(V - want).max() <= tol * np.abs(want).max()
