@@ -128,6 +128,10 @@ __device__ __forceinline__ size_t opaque(size_t v) {
     asm volatile("" : "+l"(v));
     return v;
 }
+__device__ __forceinline__ int opaque(int v) {
+    asm volatile("" : "+r"(v));
+    return v;
+}
 
 #ifndef CM_PDL_EARLY
 #define CM_PDL_EARLY 0  // trigger at CTA start (measured slower: dependents hold SM slots)

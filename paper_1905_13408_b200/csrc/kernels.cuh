@@ -152,9 +152,16 @@ template <typename R> __host__ __device__ constexpr bool use_packed_tw() { retur
 // ==================================================================================
 // y pass: FFT along j for every (k, h) column. grid = (Nh/TWY, N)
 // ==================================================================================
+#ifndef CM_Y_PIPE
+#define CM_Y_PIPE 1  // load the next tile while transforming this one (one CTA per SM)
+#endif
+
+// power-of-two sides >= 256 (16 elements per thread); radix-3 plans hold 24
+template <int N> __host__ __device__ constexpr bool y_pipe() { return CM_Y_PIPE && N >= 256 && (N & (N - 1)) == 0; }
+
 template <typename R, int N, bool FWD, bool DM = false>
 __global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY,
-                                  Geo<R, N>::TWY * Geo<R, N>::TY <= 512 ? 2 : 1)
+                                  (Geo<R, N>::TWY * Geo<R, N>::TY <= 512 && !y_pipe<N>()) ? 2 : 1)
 ypass_kernel(YParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
@@ -172,6 +179,45 @@ ypass_kernel(YParams<R> p) {
     // persistent over (column tile, plane): the twiddle table is staged once
     const int NTX = p.htiles;
     const int ntiles = NTX * p.nplanes;
+    if constexpr (y_pipe<N>()) {
+        // software pipeline: the loads of the next tile are in flight during
+        // this tile's transform (registers for both: one CTA per SM)
+        const int stride = gridDim.x * gridDim.y;
+        int tile = blockIdx.y * gridDim.x + blockIdx.x;
+        auto load = [&](int tl, C (&dst)[G::EY]) {
+            const int hh = (p.htile0 + tl % NTX) * G::TWY + col, kk = tl / NTX;
+            if constexpr (!DM) {
+                const C* b0 = p.S + (size_t)kk * p.lin.kstride + hh;
+#pragma unroll
+                for (int m = 0; m < G::EY; ++m) dst[m] = b0[(size_t)(t + G::TY * m) * G::Nh];
+            } else {
+#pragma unroll
+                for (int m = 0; m < G::EY; ++m) dst[m] = p.S[p.lin.at(kk, t + G::TY * m, hh, G::Nh)];
+            }
+        };
+        C vn[G::EY];
+        if (tile < ntiles) load(tile, vn);
+        for (; tile < ntiles; tile += stride) {
+            C v[G::EY];
+#pragma unroll
+            for (int m = 0; m < G::EY; ++m) v[m] = vn[m];
+            if (tile + stride < ntiles) load(tile + stride, vn);
+            __syncthreads();
+            fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw_src<R, FWD>(tw, tw4),
+                                       BlockSync{});
+            const int hh = (p.htile0 + tile % NTX) * G::TWY + col, kk = tile / NTX;
+            if constexpr (!DM) {
+                C* base = p.S + (size_t)kk * p.lin.kstride + hh;
+#pragma unroll
+                for (int m = 0; m < G::EY; ++m) base[(size_t)(t + G::TY * m) * G::Nh] = v[m];
+            } else {
+                C* out = p.Sout ? p.Sout : p.S;
+#pragma unroll
+                for (int m = 0; m < G::EY; ++m) out[p.lout.at(kk, t + G::TY * m, hh, G::Nh)] = v[m];
+            }
+        }
+        return;
+    }
     for (int tile = blockIdx.y * gridDim.x + blockIdx.x; tile < ntiles; tile += gridDim.x * gridDim.y) {
     const int h = (p.htile0 + tile % NTX) * G::TWY + col;
     const int k = tile / NTX;
@@ -191,9 +237,11 @@ ypass_kernel(YParams<R> p) {
         __syncthreads();
         fft_regs<N, G::EY, N, FWD>(v, t, buf, ColAddr{G::TWY, col}, tw_src<R, FWD>(tw, tw4),
                                    BlockSync{});
-        C* out = p.Sout ? p.Sout : p.S;
+        // store offsets computed here, not held live across the transform
+        C* out = opaque(p.Sout ? p.Sout : p.S);
+        const int ko = opaque(k), to = opaque(t), ho = opaque(h);
 #pragma unroll
-        for (int m = 0; m < G::EY; ++m) out[p.lout.at(k, t + G::TY * m, h, G::Nh)] = v[m];
+        for (int m = 0; m < G::EY; ++m) out[p.lout.at(ko, to + G::TY * m, ho, G::Nh)] = v[m];
     }
     }
 }
