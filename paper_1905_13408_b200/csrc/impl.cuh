@@ -298,7 +298,6 @@ struct Impl final : ImplBase {
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
-    int zpipe_grid = 1;        // persistent pipelined z pass (fp32 512^3)
     // programmatic dependent launch between the per-iteration kernels (each
     // waits on griddepcontrol before touching its predecessor's output); opt-in:
     // measured neutral (dependents cannot start work before the predecessor
@@ -450,16 +449,7 @@ struct Impl final : ImplBase {
                                                              ZGeo<R, N>::NT, ZGeo<R, N>::SMEM_MAIN));
             ygrid = sms * std::max(occy, 1);
             zgrid = sms * std::max(occz, 1);
-            if constexpr (z_pipe<R, N>()) {
-                int occp = 0;
-                for (auto fn : {zmain_pipe_kernel<R, N, ZM_FULL>, zmain_pipe_kernel<R, N, ZM_FIT>,
-                                zmain_pipe_kernel<R, N, ZM_FWD>})
-                    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)ZGeo<R, N>::SMEM_MAIN));
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, zmain_pipe_kernel<R, N, ZM_FULL>,
-                                                                 ZGeo<R, N>::NT, ZGeo<R, N>::SMEM_MAIN));
-                zpipe_grid = sms * std::max(occp, 1);
-            }
+
             if constexpr (FUSE) {
                 using F = FGeo<N>;
                 // opt-in: measured no faster than the separate passes at 512^3 (the
@@ -631,11 +621,7 @@ struct Impl final : ImplBase {
         using ZG = ZGeo<R, N>;
         ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
         dim3 grid(Nh / ZG::TW, N);
-        if constexpr (z_pipe<R, N>())
-            CK(launch_pdl(use_pdl, zmain_pipe_kernel<R, N, MODE>, dim3(zpipe_grid), dim3(ZG::NT),
-                          ZG::SMEM_MAIN, stream, p));
-        else
-            CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
+        CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
         if constexpr (MODE != ZM_FWD)
             CK(launch_pdl(use_pdl, zcol0_kernel<R, N, MODE>, dim3(N / 2 + 1), dim3(ZG::NT0),
                           ZG::SMEM_COL0, stream, p));

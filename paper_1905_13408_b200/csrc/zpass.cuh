@@ -49,15 +49,6 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_E16_MIN
 #define CM_Z_E16_MIN 512
 #endif
-#ifndef CM_Z_PIPE
-#define CM_Z_PIPE 0  // persistent pipelined z pass: measured slower (0.43 -> 0.54 ms)
-#endif
-#ifndef CM_Z_WSM
-#define CM_Z_WSM 0  // cp.async staging of W: measured slower (0.46 -> 0.55 ms at 512^3)
-#endif
-#ifndef CM_Z_PFW
-#define CM_Z_PFW 0
-#endif
 #ifndef CM_Z_TW
 #define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
 #endif
@@ -79,12 +70,8 @@ template <typename R, int N> struct ZGeo {
     static constexpr int TW = E8 ? (TWMAX < 1024 / T ? TWMAX : 1024 / T) : Geo<R, N>::TWY;
     static constexpr int NT = TW * T;
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
-    // E16: the W tile is staged into shared memory by cp.async at kernel start
-    // (its latency overlaps the S loads and the forward FFT)
-    static constexpr bool WSM = E16 && CM_Z_WSM;
-    static constexpr size_t OFF_WSM =
+    static constexpr size_t SMEM_MAIN =
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
-    static constexpr size_t SMEM_MAIN = OFF_WSM + (WSM ? sizeof(R) * (size_t)N * TW : 0);
     static constexpr int MINB = NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
     // column-0 kernel: 8 elements per thread on power-of-two sides >= 256 (more
     // warps per pair block: the kernel is latency bound with 257 blocks)
@@ -133,20 +120,6 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     const int hloc = (tile % NTX) * TW + col;
     const int h = h0 + hloc;
     const int b = tile / NTX;  // local row
-    [[maybe_unused]] R* wsm = reinterpret_cast<R*>(smem_raw + ZGeo<R, N>::OFF_WSM);
-    if constexpr (ZGeo<R, N>::WSM && MODE != ZM_FWD) {
-        constexpr int CH = TW * (int)sizeof(R) / 16;  // 16-byte chunks per row
-        const R* wrow = p.W + (size_t)b * hl + (tile % NTX) * TW;
-        const size_t wstride = (size_t)nrows * hl;
-        for (int q = threadIdx.x; q < N * CH; q += blockDim.x) {
-            const int c = q / CH, part = q % CH;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                             smem_u32(wsm + c * TW + part * 4)),
-                         "l"(wrow + c * wstride + part * 4)
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
     const size_t plane = (size_t)nrows * hl;
     C* base = p.S + (size_t)b * hl + hloc;
     C v[E];
@@ -157,14 +130,12 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     R w[E];
     C y[E];
     constexpr bool PREFETCH = ZGeo<R, N>::PREFETCH && MODE != ZM_FWD;
-    // E16: W alone (one register per element) is prefetched under CM_Z_PFW
-    constexpr bool PFW = !PREFETCH && CM_Z_PFW && ZGeo<R, N>::E16 && MODE != ZM_FWD;
-    if constexpr (PREFETCH || PFW) {
+    if constexpr (PREFETCH) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const size_t gi = ((size_t)(t + T * m) * nrows + b) * hl + hloc;
             w[m] = __ldg(p.W + gi);
-            if constexpr (PREFETCH) y[m] = __ldg(p.Yh + gi);
+            y[m] = __ldg(p.Yh + gi);
         }
     }
     __syncthreads();
@@ -178,10 +149,6 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     }
     R quad = R(0), cross = R(0);
     const size_t lplane = opaque(plane);
-    if constexpr (ZGeo<R, N>::WSM) {
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
-    }
     if (h == 0) {
 #pragma unroll
         for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
@@ -195,8 +162,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
 #pragma unroll
                 for (int m = g0; m < g0 + G; ++m) {
                     const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * hl + hloc;
-                    if constexpr (ZGeo<R, N>::WSM) w[m] = wsm[(t + T * m) * TW + col];
-                    else if constexpr (!PFW) w[m] = __ldg(p.W + gi);
+                    w[m] = __ldg(p.W + gi);
                     y[m] = p.Yh[gi];
                 }
             }
@@ -228,97 +194,6 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     if (h != 0)
 #pragma unroll
         for (int m = 0; m < E; ++m) sbase[(size_t)(t + T * m) * splane] = v[m];
-}
-
-// One GPU, 512-thread tiles (fp32 N = 512): persistent CTAs with the next
-// tile's spectrum loads in flight during this tile's transforms and multiply
-// (registers for both: one CTA per SM). Same arithmetic as zmain_kernel.
-template <typename R, int N> __host__ __device__ constexpr bool z_pipe() {
-    return CM_Z_PIPE && sizeof(R) == 4 && ZGeo<R, N>::E16 && ZGeo<R, N>::NT <= 512;
-}
-
-template <typename R, int N, int MODE>
-__global__ void __launch_bounds__(ZGeo<R, N>::NT, 1) zmain_pipe_kernel(ZMParams<R> p) {
-    using G = Geo<R, N>;
-    using C = Cx<R>;
-    constexpr int TW = ZGeo<R, N>::TW, T = ZGeo<R, N>::T, E = ZGeo<R, N>::E, Nh = G::Nh;
-    constexpr int NTX = Nh / TW, NTILES = NTX * N;
-    pdl_trigger();
-    pdl_wait();
-    if (p.st && ld_done(p.st)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) p.st->done_y = 1;
-        return;
-    }
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C* tw = reinterpret_cast<C*>(smem_raw);
-    C* buf = tw + N;
-    double* red = reinterpret_cast<double*>(buf + N * TW);
-    stage_table(tw, p.twN, N);
-    const int col = threadIdx.x % TW;
-    const int t = threadIdx.x / TW;
-    constexpr size_t plane = (size_t)N * Nh;
-    auto load = [&](int tl, C (&dst)[E]) {
-        const C* b0 = p.S + (size_t)(tl / NTX) * Nh + (tl % NTX) * TW + col;
-#pragma unroll
-        for (int m = 0; m < E; ++m) dst[m] = b0[(size_t)(t + T * m) * plane];
-    };
-    int tile = blockIdx.x;
-    C vn[E];
-    if (tile < NTILES) load(tile, vn);
-    for (; tile < NTILES; tile += gridDim.x) {
-        const int hloc = (tile % NTX) * TW + col, h = hloc;
-        const int b = tile / NTX;
-        C v[E];
-#pragma unroll
-        for (int m = 0; m < E; ++m) v[m] = vn[m];
-        if (tile + (int)gridDim.x < NTILES) load(tile + gridDim.x, vn);
-        __syncthreads();
-        fft_regs<N, E, N, true>(v, t, buf, ColAddr{TW, col}, TwPlain<C, true>{tw}, BlockSync{});
-        C* const base = opaque(p.S + (size_t)b * Nh + hloc);
-        if constexpr (MODE == ZM_FWD) {
-#pragma unroll
-            for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
-            continue;
-        }
-        R quad = R(0), cross = R(0);
-        if (h == 0) {
-#pragma unroll
-            for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
-        } else {
-#pragma unroll
-            for (int g0 = 0; g0 < E; g0 += 8) {
-                R w[8];
-                C y[8];
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const size_t gi = (size_t)(t + T * (g0 + m)) * plane + (size_t)b * Nh + hloc;
-                    w[m] = __ldg(p.W + gi);
-                    y[m] = p.Yh[gi];
-                }
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const C f = v[g0 + m];
-                    quad += w[m] * (f.x * f.x + f.y * f.y);
-                    cross += y[m].x * f.x + y[m].y * f.y;
-                    v[g0 + m] = cx<C>(w[m] * f.x - y[m].x, w[m] * f.y - y[m].y);
-                }
-            }
-        }
-        if (p.part) {
-            double acc[2] = {2.0 * (double)quad, 2.0 * (double)cross};  // mates 0 < h < N/2
-            block_sum<2>(acc, red);
-            if (threadIdx.x == 0) {
-                p.part[tile * NP3 + 0] = acc[0];
-                p.part[tile * NP3 + 1] = acc[1];
-            }
-        }
-        if constexpr (MODE == ZM_FIT) continue;
-        __syncthreads();
-        fft_regs<N, E, N, false>(v, t, buf, ColAddr{TW, col}, TwPlain<C, false>{tw}, BlockSync{});
-        if (h != 0)
-#pragma unroll
-            for (int m = 0; m < E; ++m) base[(size_t)(t + T * m) * plane] = v[m];
-    }
 }
 
 template <typename R, int N, int MODE>
