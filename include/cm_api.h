@@ -121,6 +121,11 @@ int cm_get_volume(cm_ctx* ctx, double* x_out);
  * the device, from the transforms the solver already owns; centered=0 gives
  * fft3(x). The result volume stays resident. */
 int cm_get_spectrum(cm_ctx* ctx, int centered, double* out_interleaved);
+/* FSC (fsc.cpp:10-42) between the resident results of two contexts on the same
+ * device (the two half-maps of em_refine, refine.cpp:194: fsc(V_a, V_b) with
+ * V = fft3_centered(x)); curve receives n/2 + 1 shell values (cap >= n/2 + 1).
+ * Both results stay resident. */
+int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap);
 
 /* Diagnostics: when on, cm_solve launches every kernel individually between
  * CUDA events on the context stream (no graph) and accumulates per-kernel

@@ -14,6 +14,7 @@
 //   scale_data/derive_config  params.hpp:22, 39-41
 //   fft3 / ifft3_complex      fourier.hpp:11-18
 //   accumulator_symmetry_residue backproject.hpp:35
+//   fsc of fft3_centered volumes fsc.hpp:21 (em_refine, refine.cpp:194)
 // Errors are mapped to the same status codes as include/cm_api.h.
 #include <chrono>
 #include <complex>
@@ -24,6 +25,7 @@
 
 #include "cryomap/backproject.hpp"
 #include "cryomap/fourier.hpp"
+#include "cryomap/fsc.hpp"
 #include "cryomap/gradient.hpp"
 #include "cryomap/params.hpp"
 #include "cryomap/phantom.hpp"
@@ -281,6 +283,14 @@ int ref_phantom(int n, int n_blobs, unsigned long long seed, double* out) {
     return guard([&] {
         Volume3D v = generate_phantom(random_phantom_spec(n_blobs, n, seed), n, 1.0);
         std::memcpy(out, v.data.data(), sizeof(double) * v.data.size());
+    });
+}
+
+// FSC of two real volumes as em_refine forms it: fsc(fft3_centered(a), fft3_centered(b))
+int ref_fsc_volumes(int n, const double* a, const double* b, double* curve) {
+    return guard([&] {
+        FSCCurve c = fsc(fft3_centered(to_vol(n, a)), fft3_centered(to_vol(n, b)));
+        std::memcpy(curve, c.value.data(), sizeof(double) * c.value.size());
     });
 }
 

@@ -73,6 +73,7 @@ def load() -> C.CDLL:
         "cm_solve": [P, C.POINTER(cm_reg_config), P, C.c_int, C.POINTER(cm_solve_stats)],
         "cm_get_volume": [P, P],
         "cm_get_spectrum": [P, C.c_int, P],
+        "cm_fsc": [P, P, P, C.c_int],
         "cm_set_profiling": [P, C.c_int],
         "cm_get_profile": [P, _dp, _ip],
         "cm_m_step": [P, P, P, C.c_int, P, P, C.POINTER(cm_reg_config), P, P, C.c_int,

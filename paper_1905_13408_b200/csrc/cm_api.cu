@@ -208,6 +208,16 @@ int cm_get_spectrum(cm_ctx* ctx, int centered, double* out_interleaved) {
     return ctx->impl->result_spectrum(out_interleaved, centered ? 1 : 0);
 }
 
+int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap) {
+    CTX_GUARD(a);
+    if (!b || !b->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
+    if (!curve) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+    if (a->n != b->n) return fail(CM_ERR_GRID_MISMATCH, "fsc: side_n differs");
+    if (a->device != b->device) return fail(CM_ERR_INVALID_ARGUMENT, "fsc: contexts on different devices");
+    if (cap < a->n / 2 + 1) return fail(CM_ERR_INVALID_ARGUMENT, "fsc: curve needs n/2 + 1 entries");
+    return a->impl->fsc_with(b->impl.get(), curve);
+}
+
 int cm_m_step(cm_ctx* ctx, const double* weight, const double* numerator, int finalized,
               const double* x_init, const double* x_anchor, const cm_reg_config* cfg,
               double* x_out, cm_trace_row* trace, int trace_cap, cm_solve_stats* stats) {

@@ -195,6 +195,61 @@ __global__ void unpack_full_kernel(int n, const Cx<R>* __restrict__ S, double* _
     }
 }
 
+// FSC shell sums (fsc.cpp:10-42) of two packed half spectra of real volumes:
+// per shell r = round(|(h, k, l)|) <= n/2: Re sum x conj(y), sum |x|^2, sum |y|^2
+// over the full grid (columns 0 < h < n/2 stand for their Friedel mates too,
+// weight 2; the packed column 0 is split into h = 0 and h = n/2). The centring
+// sign of fft3_centered cancels in every sum. Per-block shared histograms
+// (fp64 shared atomics), then a fixed-order sum over blocks.
+template <typename R>
+__global__ void fsc_shell_kernel(int n, const Cx<R>* __restrict__ Sa, const Cx<R>* __restrict__ Sb,
+                                 double* __restrict__ part) {
+    extern __shared__ double hist[];  // [n/2 + 1][3]
+    const int nh = n / 2, ns = nh + 1;
+    for (int q = threadIdx.x; q < 3 * ns; q += blockDim.x) hist[q] = 0.0;
+    __syncthreads();
+    const size_t total = (size_t)n * n * nh;
+    auto add = [&](int h, int k, int l, double xr, double xi, double yr, double yi, double wgt) {
+        const int r = (int)lround(sqrt((double)h * h + (double)k * k + (double)l * l));
+        if (r > nh) return;
+        atomicAdd(&hist[3 * r + 0], wgt * (xr * yr + xi * yi));
+        atomicAdd(&hist[3 * r + 1], wgt * (xr * xr + xi * xi));
+        atomicAdd(&hist[3 * r + 2], wgt * (yr * yr + yi * yi));
+    };
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const int a = (int)(q % nh);
+        const size_t bc = q / nh;
+        const int b = (int)(bc % n), c = (int)(bc / n);
+        const int k = b < nh ? b : b - n, l = c < nh ? c : c - n;
+        const Cx<R> x = Sa[q], y = Sb[q];
+        if (a > 0) {
+            add(a, k, l, x.x, x.y, y.x, y.y, 2.0);
+        } else {
+            const int bm = b ? n - b : 0, cm_ = c ? n - c : 0;
+            const size_t m = ((size_t)cm_ * n + bm) * nh;
+            const Cx<R> xm = Sa[m], ym = Sb[m];
+            // F(0) = (z + conj zm)/2, F(n/2) = (z - conj zm)/(2i)
+            add(0, k, l, 0.5 * ((double)x.x + xm.x), 0.5 * ((double)x.y - xm.y),
+                0.5 * ((double)y.x + ym.x), 0.5 * ((double)y.y - ym.y), 1.0);
+            add(nh, k, l, 0.5 * ((double)x.y + xm.y), -0.5 * ((double)x.x - xm.x),
+                0.5 * ((double)y.y + ym.y), -0.5 * ((double)y.x - ym.x), 1.0);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < 3 * ns; q += blockDim.x)
+        part[(size_t)blockIdx.x * 3 * ns + q] = hist[q];
+}
+
+__global__ static void fsc_reduce_kernel(const double* __restrict__ part, int nblocks, int len,
+                                         double* __restrict__ out) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < len; q += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nblocks; ++b) s += part[(size_t)b * len + q];  // fixed order
+        out[q] = s;
+    }
+}
+
 // prox_l1 (regularizer.cpp:103-110), elementwise in fp64
 static __global__ void prox_kernel(const double* __restrict__ x, const double* __restrict__ t,
                             double* __restrict__ out, size_t L) {
@@ -253,6 +308,9 @@ struct ImplBase {
     virtual int fft3(const double* x, double* out) = 0;
     // fft3_centered of the resident solve result (em_refine, refine.cpp:182)
     virtual int result_spectrum(double* out, int centered) = 0;
+    // FSC of this context's and another's resident results (refine.cpp:194)
+    virtual int fsc_with(ImplBase* other, double* curve) = 0;
+    virtual int result_to_spectrum() = 0;  // S <- fft3 of the resident result
     virtual long long bytes() const = 0;
 
     cudaStream_t stream = nullptr;
@@ -1179,6 +1237,38 @@ struct Impl final : ImplBase {
         result_valid = false;
         CKS(upload_real(x, X[0]));
         return spectrum_to_host(X[0], out, 0);
+    }
+
+    int result_to_spectrum() override {
+        if (!vol_set || !result_valid) return fail(CM_ERR_STATE, "no solver result resident");
+        R* src = last_fista ? XF[last_iter % 2] : X[last_iter % 3];
+        CKS(spectrum_of(src));
+        CKS(launch_z<ZM_FWD>(nullptr, nullptr));
+        return CM_OK;
+    }
+
+    int fsc_with(ImplBase* other_base, double* curve) override {
+        auto* other = dynamic_cast<Impl*>(other_base);
+        if (!other) return fail(CM_ERR_GRID_MISMATCH, "fsc: contexts differ in side or precision");
+        CKS(other->result_to_spectrum());
+        CK(cudaStreamSynchronize(other->stream));
+        CKS(result_to_spectrum());
+        const int ns = Nh + 1;
+        const int blocks = 148 * 2;
+        double* part = stage;                     // [blocks][ns][3] (stage holds >= 3L doubles)
+        double* sums = stage + (size_t)blocks * 3 * ns;
+        fsc_shell_kernel<R><<<blocks, 256, sizeof(double) * 3 * ns, stream>>>(N, S, other->S, part);
+        CK(cudaGetLastError());
+        fsc_reduce_kernel<<<grid_for((size_t)3 * ns, 256), 256, 0, stream>>>(part, blocks, 3 * ns, sums);
+        CK(cudaGetLastError());
+        std::vector<double> h((size_t)3 * ns);
+        CK(cudaMemcpyAsync(h.data(), sums, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        for (int r = 0; r < ns; ++r) {
+            const double den = std::sqrt(h[3 * r + 1] * h[3 * r + 2]);
+            curve[r] = den > 0.0 ? h[3 * r] / den : 0.0;  // fsc.cpp:36-39
+        }
+        return CM_OK;
     }
 
     int result_spectrum(double* out, int centered) override {

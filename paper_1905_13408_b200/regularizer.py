@@ -290,6 +290,13 @@ class Context:
         _check(self.lib.cm_get_spectrum(self.ptr, int(bool(centered)), out.ctypes.data))
         return out
 
+    def fsc(self, other: "Context") -> np.ndarray:
+        """FSC curve (n/2 + 1 shells, fsc.cpp) between this context's resident result
+        and another's (same device): em_refine's fsc(V_a, V_b), refine.cpp:194."""
+        out = np.empty(self.n // 2 + 1, dtype=np.float64)
+        _check(self.lib.cm_fsc(self.ptr, other.ptr, out.ctypes.data, out.size))
+        return out
+
     def set_profiling(self, on: bool) -> None:
         _check(self.lib.cm_set_profiling(self.ptr, int(bool(on))))
 

@@ -245,6 +245,15 @@ class Reference(_Lib):
         self.f("fft3_centered")(x.shape[0], _d(x), _d(out))
         return out
 
+    def fsc_volumes(self, a, b):
+        """fsc(fft3_centered(a), fft3_centered(b)) by the reference (fsc.cpp)."""
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.empty(a.shape[0] // 2 + 1)
+        rc = self.f("fsc_volumes")(a.shape[0], _d(a), _d(b), _d(out))
+        assert rc == 0, self.last_error()
+        return out
+
     def symmetry_residue(self, w, y):
         out = C.c_double()
         self.f("symmetry_residue")(w.shape[0], _d(w), _d(y), C.byref(out))

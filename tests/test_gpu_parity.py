@@ -383,3 +383,32 @@ def test_em_m_step_block_returns_centered_spectrum(prec):
     want = np.fft.fftn(synth.halfshift3(x))
     tol = 1e-12 if prec == 64 else 2e-6
     assert np.abs(V - want).max() <= tol * np.abs(want).max()
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_fsc_of_two_resident_half_maps_vs_reference(prec):
+    """em_refine's FSC between the two half-map results (refine.cpp:194,
+    fsc.cpp:10-42) computed on the device from two resident contexts, against the
+    unmodified reference (fsc of fft3_centered volumes)."""
+    from oracle_lib import Reference, have_reference
+
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    n = 48
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 4
+    ctxs = []
+    for x0 in (p.x0, p.x0 + 0.2 * random_volume(n, 5)):
+        c = cm.Context(n, prec)
+        c.set_accumulator(acc)
+        c.set_volumes(x0, x0)
+        c.solve(cfg)
+        ctxs.append(c)
+    got = ctxs[0].fsc(ctxs[1])
+    want = Reference().fsc_volumes(ctxs[0].get_volume(), ctxs[1].get_volume())
+    tol = 1e-12 if prec == 64 else 1e-5
+    np.testing.assert_allclose(got, want, atol=tol, rtol=tol)
+    assert got[0] > 0.99 and got.shape == (n // 2 + 1,)
