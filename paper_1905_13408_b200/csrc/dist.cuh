@@ -274,6 +274,9 @@ struct DistImpl final : DistBase {
     };
 
     int P = 1, NK = N, NB = N;
+    // CM_SLAB_FORCE_COMM=1: run the transposes even on one rank (self send/recv
+    // through the communicator; exercises the NCCL all-to-all path on one GPU)
+    const bool force_comm = std::getenv("CM_SLAB_FORCE_COMM") != nullptr;
     std::vector<Rank> ranks;
     cudaStream_t stream = nullptr;
     std::vector<void*> allocs;
@@ -346,7 +349,7 @@ struct DistImpl final : DistBase {
             const size_t H = (size_t)NK * N * Nh;
             CKS(dalloc(&k.Snat, H));
             CKS(dalloc(&k.Ssend, H));
-            if (P > 1) CKS(dalloc(&k.Srecv, H));
+            if (P > 1 || force_comm) CKS(dalloc(&k.Srecv, H));
             else k.Srecv = k.Ssend;  // one rank: the transposes are the identity
             CKS(dalloc(&k.W, (size_t)N * NB * Nh));
             CKS(dalloc(&k.Wn, (size_t)N * NB));
@@ -533,7 +536,7 @@ struct DistImpl final : DistBase {
     }
     // all-to-all of one column half on cstream; forward: z-slab -> b-slab
     int a2a_half(bool forward, int half) {
-        if (P == 1) return CM_OK;
+        if (P == 1 && !force_comm) return CM_OK;
         std::vector<void*> s, r;
         const size_t off = (size_t)half * half_elems();
         for (Rank& k : ranks) {

@@ -300,6 +300,27 @@ def test_slab_nccl_single_rank_matches_single_gpu():
 
 
 @pytest.mark.gpu
+def test_slab_nccl_all_to_all_path_single_rank(monkeypatch):
+    """The grouped ncclSend/ncclRecv transposes (self send/recv at world size 1,
+    CM_SLAB_FORCE_COMM) on the collectives stream: same solve as one GPU."""
+    from paper_1905_13408_b200.slab import SlabContext, nccl_unique_id
+
+    monkeypatch.setenv("CM_SLAB_FORCE_COMM", "1")
+    n = 128
+    p, acc, base = _problem(n)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 8})
+    x1 = cm.m_step(acc, p.x0, p.x0, cfg, precision=32)
+    for nid in (nccl_unique_id(), None):   # NCCL, then the emulated communicator
+        sc = SlabContext(n, 1, 0, 0, nid)
+        sc.set_accumulator(acc)
+        sc.set_volumes(p.x0)
+        sc.solve(cfg)
+        x2 = sc.get_volume()
+        sc.close()
+        assert _rel(x2, x1) <= 1e-6
+
+
+@pytest.mark.gpu
 def test_slab_synthetic_problem_is_decomposition_independent():
     """The device-rendered timing problem (bench 'big' runs) gives the same solve on
     1 and 4 ranks."""
