@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--big-n", type=int, default=1024,
                     help="side of the device-rendered z-slab scaling run (0: skip)")
     ap.add_argument("--big-iters", type=int, default=20)
+    ap.add_argument("--em", type=int, default=1, help="time the EM-block extras (V, FSC)")
     return ap.parse_args()
 
 
@@ -595,6 +596,29 @@ def run_ours(args):
                                        else "frozen-weight surrogate relative decrease < 3e-7"),
                          "refresh": "per_m_step"}
 
+    # ---- EM M-step block extras: V = fft3_centered of the
+    # resident result and the FSC of two resident half-map results, on the device
+    em = None
+    if args.em and world == 1:
+        ctx.solve(cfg)
+        ctx2 = cm.Context(n, args.precision, device=local)
+        ctx2.set_accumulator(acc)
+        ctx2.set_volumes(p.x0 * 0.98, p.x0 * 0.98)
+        ctx2.solve(cm.RegConfig(**{**cfg.__dict__, "inner_iters": 10}))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        V = ctx.get_spectrum(centered=True)
+        t_spec = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        curve = ctx.fsc(ctx2)
+        t_fsc = time.perf_counter() - t0
+        em = {"n": n, "spectrum_centered_s": t_spec, "fsc_s": t_fsc,
+              "spectrum_bytes_to_host": int(V.nbytes), "fsc_shells": int(curve.size),
+              "note": "fft3_centered of the resident m_step result (full complex128 grid to "
+                      "the host) and the FSC of two resident results; the reference does both "
+                      "on the host (full-grid FFTW transforms + shell loop, refine.cpp:182,194)"}
+        del V, ctx2
+
     big = None
     if args.big_n:
         del ctx
@@ -625,7 +649,7 @@ def run_ours(args):
                        "parallelism": f"replicas{world}"},
             "device_ms_solver_stream": dev_ms, "gen_seconds": gen_s,
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": launches, "time_to_tolerance": ttt, "big": big,
+            "gpu_launches": launches, "time_to_tolerance": ttt, "big": big, "em_block": em,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
