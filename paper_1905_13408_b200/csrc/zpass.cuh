@@ -49,6 +49,9 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_E16_MIN
 #define CM_Z_E16_MIN 512
 #endif
+#ifndef CM_Z_E32_MIN
+#define CM_Z_E32_MIN 1024  // 1024^3: z pass 5.5 -> 4.2 ms per iteration
+#endif
 #ifndef CM_Z_TW
 #define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
 #endif
@@ -64,7 +67,10 @@ template <typename R, int N> struct ZGeo {
     // after the forward FFT, in groups of 8
     static constexpr bool E16 = CM_Z_E16 && E8 && N >= CM_Z_E16_MIN;
     static constexpr bool PREFETCH = E8 && !E16;
-    static constexpr int E = E16 ? 16 : E8 ? 8 : Geo<R, N>::EY;
+    // N >= CM_Z_E32_MIN: 32 elements per thread (one warp per column, 512-thread
+    // CTAs, up to 128 registers)
+    static constexpr bool E32 = E16 && N >= CM_Z_E32_MIN;
+    static constexpr int E = E32 ? 32 : E16 ? 16 : E8 ? 8 : Geo<R, N>::EY;
     static constexpr int T = N / E;
     static constexpr int TWMAX = CM_Z_TW ? CM_Z_TW : 16;
     static constexpr int TW = E8 ? (TWMAX < 1024 / T ? TWMAX : 1024 / T) : Geo<R, N>::TWY;
@@ -72,7 +78,7 @@ template <typename R, int N> struct ZGeo {
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
     static constexpr size_t SMEM_MAIN =
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
-    static constexpr int MINB = NT >= 1024 ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
+    static constexpr int MINB = (NT >= 1024 || E32) ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
     // column-0 kernel: 8 elements per thread on power-of-two sides >= 256 (more
     // warps per pair block: the kernel is latency bound with 257 blocks)
     static constexpr int E0 = (N >= 256 && (N & (N - 1)) == 0) ? 8 : Geo<R, N>::EY;

@@ -351,6 +351,15 @@ def context(n: int, precision: int | None = None, device: int = 0) -> Context:
     return cache[key]
 
 
+def release_contexts() -> None:
+    """Free this thread's cached contexts (their device memory)."""
+    cache = getattr(_tls, "ctx", None)
+    if cache:
+        for c in cache.values():
+            c.close()
+        cache.clear()
+
+
 def _side(x) -> int:
     return int(np.shape(_arr(x))[0])
 

@@ -18,6 +18,16 @@ from paper_1905_13408_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _free_device_memory():
+    """Each case here holds tens of GB of device memory; release between cases."""
+    yield
+    import gc
+
+    cm.regularizer.release_contexts()
+    gc.collect()
+
+
 def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
