@@ -35,6 +35,9 @@ __host__ __device__ constexpr int pow2_divisor_le(int v, int cap) {
     return t;
 }
 
+#ifndef CM_Y_SMEM_CAP_KB
+#define CM_Y_SMEM_CAP_KB 96
+#endif
 #ifndef CM_Y_TWMAX
 #define CM_Y_TWMAX 16  // columns per y tile (128-byte rows in fp32)
 #endif
@@ -50,7 +53,7 @@ template <typename R, int N> struct Geo {
     // y / z columns: transform length N
     static constexpr int EY = elems_for(N);
     static constexpr int TY = N / EY;
-    static constexpr int SMEM_CAP = 96 * 1024; // per tile buffer budget (bytes)
+    static constexpr int SMEM_CAP = CM_Y_SMEM_CAP_KB * 1024; // per tile buffer budget (bytes)
     static constexpr int TWY_CAP = (SMEM_CAP / (N * (int)sizeof(C))) < 1 ? 1 : (SMEM_CAP / (N * (int)sizeof(C)));
     static constexpr int TWY_LIM = (CM_Y_TWMAX < (1024 / TY) ? CM_Y_TWMAX : (1024 / TY));
     static constexpr int TWY = pow2_divisor_le(Nh, TWY_LIM < TWY_CAP ? TWY_LIM : TWY_CAP);
@@ -157,7 +160,10 @@ template <typename R> __host__ __device__ constexpr bool use_packed_tw() { retur
 #endif
 
 // power-of-two sides >= 256 (16 elements per thread); radix-3 plans hold 24
-template <int N> __host__ __device__ constexpr bool y_pipe() { return CM_Y_PIPE && N >= 256 && (N & (N - 1)) == 0; }
+template <int N> __host__ __device__ constexpr bool y_pipe() {
+    return CM_Y_PIPE && N >= 256 && (N & (N - 1)) == 0 &&
+           Geo<float, N>::TWY * Geo<float, N>::TY <= 512;  // two tiles in registers
+}
 
 template <typename R, int N, bool FWD, bool DM = false>
 __global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY,
