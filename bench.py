@@ -595,6 +595,17 @@ def run_ours(args):
                          "criterion": ("step norm < 3% of the largest step" if name == "fista"
                                        else "frozen-weight surrogate relative decrease < 3e-7"),
                          "refresh": "per_m_step"}
+            if e2e is not None and name == "fista":
+                # the same solve through cm_m_step on pinned host buffers: fp64 full-grid
+                # accumulator + volume H2D, result D2H ("including H2D")
+                torch.cuda.synchronize()
+                g0 = torch.cuda.Event(enable_timing=True)
+                g1 = torch.cuda.Event(enable_timing=True)
+                g0.record()
+                ctx.m_step_host(pacc, pin_x, pin_x, tc, pin_o)
+                g1.record()
+                torch.cuda.synchronize()
+                ttt[name]["seconds_incl_transfers"] = g0.elapsed_time(g1) / 1e3
 
     # ---- EM M-step block extras: V = fft3_centered of the
     # resident result and the FSC of two resident half-map results, on the device
