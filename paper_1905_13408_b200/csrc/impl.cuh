@@ -361,6 +361,8 @@ struct Impl final : ImplBase {
     // measured neutral (dependents cannot start work before the predecessor
     // completes) or slower with an early trigger (waiting CTAs hold SM slots)
     bool use_pdl = std::getenv("CM_PDL") != nullptr;
+    cudaGraphExec_t gexec = nullptr;  // instantiated 6-iteration chunk (reused while gkey holds)
+    std::vector<uint64_t> gkey;
     // fused y/x plane pairs (xyfused.cuh): fp32 power-of-two sides 256..1024
     static constexpr bool FUSE = std::is_same<R, float>::value && (N == 256 || N == 512);
     bool use_fused = false;
@@ -399,9 +401,10 @@ struct Impl final : ImplBase {
     }
 
     ~Impl() override {
+        if (gexec) cudaGraphExecDestroy(gexec);
         void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, gbuf, S, W,
                       Wn, Yh, Yn, Z0, twN, twF4, twI4, stage, part1, part3, part_acc, maxes, st, trace_d,
-                      theta_d};
+                      theta_d, Q0, fcnt};
         for (void* p : ps)
             if (p) cudaFree(p);
         if (flags_h) cudaFreeHost(flags_h);
@@ -994,15 +997,40 @@ struct Impl final : ImplBase {
             }
             for (auto& e : pev) cudaEventDestroy(e);
         } else if (use_graph) {
-            cudaGraph_t graph;
-            cudaGraphExec_t exec;
-            CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-            int rc = CM_OK;
-            for (int g = 0; g < chunk && rc == CM_OK; ++g) rc = iteration(g);
-            cudaError_t ce = cudaStreamEndCapture(stream, &graph);
-            if (rc != CM_OK) return rc;
-            CK(ce);
-            CK(cudaGraphInstantiate(&exec, graph, 0));
+            // the captured chunk depends only on the values baked into its kernel
+            // parameters: reuse the instantiated graph while they are unchanged
+            std::vector<uint64_t> key;
+            auto put = [&](double v) {
+                uint64_t u;
+                std::memcpy(&u, &v, 8);
+                key.push_back(u);
+            };
+            for (double v : {c->alpha, c->beta, c->gamma, c->eps, c->eps_prime, c->mu, c->fixed_step,
+                             lr, slack})
+                put(v);
+            for (long long v : {(long long)c->step_rule, (long long)c->refresh, (long long)c->convex_mode,
+                                (long long)c->momentum, (long long)hs.tol_kind, (long long)want_trace,
+                                (long long)audit, (long long)use_fused, (long long)use_pdl,
+                                (long long)(std::getenv("CM_STENCIL1") != nullptr),
+                                (long long)(uintptr_t)trace_d, (long long)(uintptr_t)theta_d,
+                                (long long)(uintptr_t)wfixed})
+                key.push_back((uint64_t)v);
+            if (!(gexec && key == gkey)) {
+                if (gexec) cudaGraphExecDestroy(gexec);
+                gexec = nullptr;
+                cudaGraph_t graph;
+                CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+                int rc = CM_OK;
+                for (int g = 0; g < chunk && rc == CM_OK; ++g) rc = iteration(g);
+                cudaError_t ce = cudaStreamEndCapture(stream, &graph);
+                if (rc != CM_OK) return rc;
+                CK(ce);
+                const cudaError_t ie = cudaGraphInstantiate(&gexec, graph, 0);
+                cudaGraphDestroy(graph);
+                CK(ie);
+                gkey = key;
+            }
+            cudaGraphExec_t exec = gexec;
             std::vector<cudaEvent_t> ev(LOOK);
             for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             for (int q = 0; q < nchunks; ++q) {
@@ -1018,8 +1046,6 @@ struct Impl final : ImplBase {
             }
             CK(cudaStreamSynchronize(stream));
             for (auto& e : ev) cudaEventDestroy(e);
-            cudaGraphExecDestroy(exec);
-            cudaGraphDestroy(graph);
         } else {
             for (int g = 0; g < K; ++g) {
                 CKS(iteration(g % 6));
