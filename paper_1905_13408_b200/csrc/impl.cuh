@@ -592,12 +592,6 @@ struct Impl final : ImplBase {
             CK(cudaMemcpy(twF4, f.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
             CK(cudaMemcpy(twI4, iv.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
         }
-        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_OBJ>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_TVGRAD>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
-        CK(cudaFuncSetAttribute(xline_kernel<R, N, XM_WEIGHTS>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(ypass_kernel<R, N, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YSmem<R, N>::bytes));
         CK(cudaFuncSetAttribute(ypass_kernel<R, N, false>,
@@ -627,7 +621,7 @@ struct Impl final : ImplBase {
     }
     template <int MODE>
     int launch_x(const XParams<R>& p) {
-        xline_kernel<R, N, MODE><<<NB1, G::LPC * G::TX, XSmem<R, N>::bytes, stream>>>(p);
+        xline_kernel<R, N, MODE><<<NB1, G::LPC * G::TX, 0, stream>>>(p);
         CK(cudaGetLastError());
         return CM_OK;
     }

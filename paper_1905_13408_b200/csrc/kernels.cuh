@@ -22,7 +22,9 @@
 
 namespace cm {
 
-enum XMode { XM_INIT = 0, XM_SWEEP = 1, XM_OBJ = 2, XM_DGRAD = 3, XM_TVGRAD = 4, XM_WEIGHTS = 5 };
+// line-kernel modes of the component entry points and the audit epilogue (the
+// solver's per-iteration sweep is stencil2/stencil; transforms are xfft/ypass/zpass)
+enum XMode { XM_OBJ = 2, XM_TVGRAD = 4, XM_WEIGHTS = 5 };
 enum ZMode { ZM_FULL = 0, ZM_FIT = 1, ZM_FWD = 2 };
 
 constexpr int NP1 = 11; // xline partial slots
@@ -284,14 +286,9 @@ __global__ void __launch_bounds__(Geo<R, N>::LPC * Geo<R, N>::TX)
 xline_kernel(XParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;
-    constexpr int Nh = G::Nh, E = G::EX, T = G::TX, LPC = G::LPC, PADX = G::PADX;
+    constexpr int T = G::TX, LPC = G::LPC;
     if (p.st && ld_done(p.st)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C* tw = reinterpret_cast<C*>(smem_raw);
-    C* lines = tw + N;                                   // [LPC][PADX]
-    double* red = reinterpret_cast<double*>(lines + LPC * PADX);
-    stage_table(tw, p.twN, N);
-    __syncthreads();
+    __shared__ double red[32 * NP1];
 
     const int lg = threadIdx.x / T;  // line within CTA
     const int t = threadIdx.x % T;
@@ -299,70 +296,18 @@ xline_kernel(XParams<R> p) {
     const bool valid = line < N * N;
     const int j = valid ? line % N : 0;
     const int k = valid ? line / N : 0;
-    C* buf = lines + lg * PADX;     // exchange buffer (padded layout)
-    R* rl = reinterpret_cast<R*>(buf); // real line view (linear), aliases buf
-    C* Srow = p.S + (size_t)line * Nh;
-    const PadAddr pad{};
-    // Lines of one group never straddle warps (T | 32); __syncwarp is the barrier.
-    const WarpSync wsync{};
-
-    C v[E];
-    if constexpr (MODE == XM_SWEEP || MODE == XM_DGRAD) {
-        // ---- C2R: Q(h) for h = t + T m -> Z(h) = A + i B, inverse FFT_Nh
-#pragma unroll
-        for (int m = 0; m < E; ++m) v[m] = valid ? Srow[t + T * m] : cx<C>(R(0), R(0));
-#pragma unroll
-        for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int hh = t + T * m;
-            const C q = v[m];
-            if (hh == 0) {
-                v[m] = cx<C>(q.x + q.y, q.x - q.y);
-            } else {
-                const C qm = buf[pad(Nh - hh)];
-                const C a = cx<C>(q.x + qm.x, q.y - qm.y);      // Q + conj(Qm)
-                const C d = cx<C>(q.x - qm.x, q.y + qm.y);      // Q - conj(Qm)
-                const C bb = cmulc(d, tw[hh]);                  // * exp(+2 pi i h/N)
-                v[m] = cx<C>(a.x - bb.y, a.y + bb.x);           // A + i B
-            }
-        }
-        __syncwarp();
-        fft_regs<Nh, E, N, false>(v, t, buf, pad, tw, wsync);
-        __syncwarp();
-        // z(p) = g(2p) + i g(2p+1), unnormalised
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int pp = t + T * m;
-            rl[2 * pp] = v[m].x;
-            rl[2 * pp + 1] = v[m].y;
-        }
-        __syncwarp();
-    }
-
-    if constexpr (MODE == XM_DGRAD) {
-        if (valid)
-            for (int i = t; i < N; i += T)
-                p.xnext[(size_t)line * N + i] = rl[i] * R(p.invL);
-        return;
-    }
 
     double acc[NP1];
 #pragma unroll
     for (int q = 0; q < NP1; ++q) acc[q] = 0.0;
 
-    if constexpr (MODE == XM_SWEEP || MODE == XM_OBJ || MODE == XM_TVGRAD ||
-                  MODE == XM_WEIGHTS) {
+    {
         const Vox<R> X{p.xcur, N};
         const Vox<R> Wv{p.wsrc, N};
         const bool same_w = (p.wsrc == p.xcur);
         const R eps = R(p.eps), epsp = R(p.eps_prime), mu = R(p.mu);
-        const R lr = R(p.lr), alpha = R(p.alpha), beta = R(p.beta), gamma = R(p.gamma);
-        const bool want_tv = (MODE == XM_TVGRAD) || (MODE == XM_SWEEP && p.beta > 0.0);
-        const bool audit = (MODE == XM_OBJ) || (MODE == XM_SWEEP && p.audit);
-        R theta = R(0);
-        if (MODE == XM_SWEEP && p.fista) theta = R(p.theta[p.st ? p.st->iter : 0]);
+        const bool want_tv = (MODE == XM_TVGRAD);
+        const bool audit = (MODE == XM_OBJ);
         // w_tv at a voxel whose own gradient norm is qn (regularizer.cpp:44-59)
         auto wtv_at = [&](int ii, int jj, int kk, R qn) -> R {
             if (p.convex) return R(1);
@@ -434,71 +379,11 @@ xline_kernel(XParams<R> p) {
                         acc[8] += ptv * (double)gn;
                     }
                 }
-                if constexpr (MODE == XM_SWEEP) {
-                    // update + prox (regularizer.cpp:193-205, 103-110)
-                    const R g = rl[i] * R(p.invL);
-                    R gs = R(2) * g + R(2) * gamma * (xc - av);
-                    if (p.beta > 0.0) gs += beta * tvg;
-                    R nx = xc - lr * gs;
-                    if (p.alpha > 0.0) {
-                        const R th = lr * alpha * wl1;
-                        nx = fabs(nx) <= th ? R(0) : nx - copysign(th, nx);
-                    }
-                    R base = xc;
-                    if (p.fista) base = __ldg(p.xold + gi);
-                    const double dx = (double)nx - (double)base;
-                    acc[9] += dx * dx;
-                    acc[10] += (double)nx * (double)nx;
-                    p.xnext[gi] = nx;
-                    R spec = nx;
-                    if (p.fista) {
-                        spec = nx + theta * (nx - base);
-                        p.ynext[gi] = spec;
-                    }
-                    rl[i] = spec; // the new spectrum is taken of x_{i+1} (or y_{k+1})
-                }
             }
         }
     }
 
-    if constexpr (MODE == XM_INIT) {
-        if (valid)
-            for (int i = t; i < N; i += T) rl[i] = __ldg(p.xcur + (size_t)line * N + i);
-    }
-
-    if constexpr (MODE == XM_SWEEP || MODE == XM_INIT) {
-        __syncwarp();
-        // ---- R2C: z(p) = x(2p) + i x(2p+1) -> FFT_Nh -> split into X(h), pack
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int pp = t + T * m;
-            v[m] = cx<C>(rl[2 * pp], rl[2 * pp + 1]);
-        }
-        __syncwarp();
-        fft_regs<Nh, E, N, true>(v, t, buf, pad, tw, wsync);
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int hh = t + T * m;
-            const C z = v[m];
-            C out;
-            if (hh == 0) {
-                out = cx<C>(z.x + z.y, z.x - z.y); // X(0) + i X(Nh)
-            } else {
-                const C zm = buf[pad(Nh - hh)];
-                const C e = cx<C>(R(0.5) * (z.x + zm.x), R(0.5) * (z.y - zm.y)); // (Z + conj Zm)/2
-                // O = (Z - conj Zm)/(2i): d = Z - conj Zm ; O = (d.y/2, -d.x/2)
-                const C o = cx<C>(R(0.5) * (z.y + zm.y), R(-0.5) * (z.x - zm.x));
-                out = cadd(e, cmul(o, tw[hh]));
-            }
-            if (valid) Srow[hh] = out;
-        }
-    }
-
-    if constexpr (MODE == XM_SWEEP || MODE == XM_OBJ) {
+    if constexpr (MODE == XM_OBJ) {
         if (p.part) {
             block_sum<NP1>(acc, red);
             if (threadIdx.x == 0)
@@ -508,10 +393,6 @@ xline_kernel(XParams<R> p) {
     }
 }
 
-template <typename R, int N> struct XSmem {
-    static constexpr size_t bytes =
-        sizeof(Cx<R>) * (N + Geo<R, N>::LPC * Geo<R, N>::PADX) + sizeof(double) * 32 * NP1;
-};
 template <typename R, int N> struct YSmem {
     static constexpr size_t bytes =
         sizeof(Cx<R>) * (N + (size_t)N * Geo<R, N>::TWY) + packed_tw_bytes<R>(N, 1);
