@@ -40,7 +40,11 @@ typedef enum {
     CM_ERR_NON_POSITIVE_SCALE = 7, /* cryomap::NonPositiveScale  (params.cpp:48-50) */
     CM_ERR_NON_HERMITIAN_INPUT = 8,/* cryomap::NonHermitianInput (fourier.cpp:80-82) */
     CM_ERR_UNSUPPORTED = 9,        /* side length without a compiled radix plan */
-    CM_ERR_STATE = 10              /* call order (e.g. solve before set_accumulator) */
+    CM_ERR_STATE = 10,             /* call order (e.g. solve before set_accumulator) */
+    CM_ERR_IO = 11,                /* cryomap::IoError           (mrc.cpp:125, 159) */
+    CM_ERR_TRUNCATED_FILE = 12,    /* cryomap::TruncatedFile     (mrc.cpp:163, 184) */
+    CM_ERR_BAD_MAGIC = 13,         /* cryomap::BadMagic          (mrc.cpp:166) */
+    CM_ERR_UNSUPPORTED_MODE = 14   /* cryomap::UnsupportedMode   (mrc.cpp:169) */
 } cm_status;
 
 typedef struct cm_ctx cm_ctx;
@@ -121,6 +125,15 @@ int cm_get_volume(cm_ctx* ctx, double* x_out);
  * the device, from the transforms the solver already owns; centered=0 gives
  * fft3(x). The result volume stays resident. */
 int cm_get_spectrum(cm_ctx* ctx, int centered, double* out_interleaved);
+/* MRC volume I/O on the resident volumes (mrc.hpp:28-41):
+ * mode-2 float32 x-fastest payloads are the device layout, so the files are
+ * read into pinned memory and copied to the device without an fp64 detour.
+ * cm_set_volumes_mrc: x_init (and x_anchor; NULL or the same path: one object)
+ * from files written by write_mrc (or any conforming subset file), with the
+ * reference reader's checks and error types. cm_write_volume_mrc: the resident
+ * solve result, byte-identical to write_mrc(path, Volume3D(result, voxel_size)). */
+int cm_set_volumes_mrc(cm_ctx* ctx, const char* path_init, const char* path_anchor);
+int cm_write_volume_mrc(cm_ctx* ctx, const char* path, double voxel_size);
 /* FSC (fsc.cpp:10-42) between the resident results of two contexts on the same
  * device (the two half-maps of em_refine, refine.cpp:194: fsc(V_a, V_b) with
  * V = fft3_centered(x)); curve receives n/2 + 1 shell values (cap >= n/2 + 1).

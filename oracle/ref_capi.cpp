@@ -27,6 +27,7 @@
 #include "cryomap/fourier.hpp"
 #include "cryomap/fsc.hpp"
 #include "cryomap/gradient.hpp"
+#include "cryomap/mrc.hpp"
 #include "cryomap/params.hpp"
 #include "cryomap/phantom.hpp"
 #include "cryomap/regularizer.hpp"
@@ -45,6 +46,10 @@ enum {
     REF_ERR_STEP_DIVERGED = 4,
     REF_ERR_NON_POSITIVE_SCALE = 7,
     REF_ERR_NON_HERMITIAN_INPUT = 8,
+    REF_ERR_IO = 11,
+    REF_ERR_TRUNCATED_FILE = 12,
+    REF_ERR_BAD_MAGIC = 13,
+    REF_ERR_UNSUPPORTED_MODE = 14,
     REF_ERR_OTHER = 99,
 };
 
@@ -71,6 +76,18 @@ int guard(F&& f) {
     } catch (const NonHermitianInput& e) {
         g_err = e.what();
         return REF_ERR_NON_HERMITIAN_INPUT;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return REF_ERR_IO;
+    } catch (const TruncatedFile& e) {
+        g_err = e.what();
+        return REF_ERR_TRUNCATED_FILE;
+    } catch (const BadMagic& e) {
+        g_err = e.what();
+        return REF_ERR_BAD_MAGIC;
+    } catch (const UnsupportedMode& e) {
+        g_err = e.what();
+        return REF_ERR_UNSUPPORTED_MODE;
     } catch (const std::exception& e) {
         g_err = e.what();
         return REF_ERR_OTHER;
@@ -291,6 +308,24 @@ int ref_fsc_volumes(int n, const double* a, const double* b, double* curve) {
     return guard([&] {
         FSCCurve c = fsc(fft3_centered(to_vol(n, a)), fft3_centered(to_vol(n, b)));
         std::memcpy(curve, c.value.data(), sizeof(double) * c.value.size());
+    });
+}
+
+// write_mrc(path, Volume3D) / read_mrc_volume(path) (mrc.cpp:134, 219)
+int ref_write_mrc_volume(const char* path, int n, double voxel_size, const double* x) {
+    return guard([&] {
+        Volume3D v = to_vol(n, x);
+        v.voxel_size = voxel_size;
+        write_mrc(path, v);
+    });
+}
+
+int ref_read_mrc_volume(const char* path, int n, double* x, double* voxel_size) {
+    return guard([&] {
+        Volume3D v = read_mrc_volume(path);
+        if (v.side_n != n) throw GridMismatch("ref_read_mrc_volume: side differs");
+        std::memcpy(x, v.data.data(), sizeof(double) * v.data.size());
+        if (voxel_size) *voxel_size = v.voxel_size;
     });
 }
 

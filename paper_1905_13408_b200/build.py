@@ -71,7 +71,7 @@ def build(sides: list[int] | None = None, jobs: int | None = None, force: bool =
             f.result()
     objs = [str(o) for _, o, _ in units]
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs,
-           "-o", str(lib), "-lcudart", "-ldl"]
+           "-o", str(lib), "-lcudart", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

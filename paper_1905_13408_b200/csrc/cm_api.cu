@@ -8,6 +8,7 @@
 #include "../../include/cm_api.h"
 #include "dist.cuh"
 #include "impl.cuh"
+#include "mrc_io.h"
 
 namespace cm {
 
@@ -55,6 +56,7 @@ struct cm_ctx {
     int n = 0;
     int precision = 32;
     int device = 0;
+    std::unique_ptr<MrcRing> mrc;  // pinned MRC staging, on first use
 };
 
 #define CTX_GUARD(ctx)                                                         \
@@ -206,6 +208,43 @@ int cm_get_spectrum(cm_ctx* ctx, int centered, double* out_interleaved) {
     CTX_GUARD(ctx);
     if (!out_interleaved) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
     return ctx->impl->result_spectrum(out_interleaved, centered ? 1 : 0);
+}
+
+int cm_set_volumes_mrc(cm_ctx* ctx, const char* path_init, const char* path_anchor) {
+    CTX_GUARD(ctx);
+    if (!path_init) return fail(CM_ERR_INVALID_ARGUMENT, "null path");
+    const bool same = !path_anchor || std::strcmp(path_init, path_anchor) == 0;
+    // validate both headers before touching the resident volumes
+    MrcFile fi, fa;
+    size_t oi = 0, oa = 0;
+    CKS(mrc_open_volume(path_init, ctx->n, fi, &oi));
+    if (!same) CKS(mrc_open_volume(path_anchor, ctx->n, fa, &oa));
+    if (!ctx->mrc) ctx->mrc.reset(new MrcRing());
+    CKS(ctx->mrc->ensure());
+    ImplBase* im = ctx->impl.get();
+    const size_t L = (size_t)ctx->n * ctx->n * ctx->n;
+    im->vol_set = false;  // a failed read leaves no half-set state behind
+    CKS(mrc_read_payload(fi, oi, im->mrc_landing(0), L, *ctx->mrc, im->stream));
+    CKS(im->mrc_commit(0));
+    if (!same) {
+        CKS(mrc_read_payload(fa, oa, im->mrc_landing(1), L, *ctx->mrc, im->stream));
+        CKS(im->mrc_commit(1));
+    } else {
+        CKS(im->mrc_commit(2));
+    }
+    if (cudaStreamSynchronize(im->stream) != cudaSuccess)
+        return fail(CM_ERR_CUDA, "mrc: upload failed");
+    return CM_OK;
+}
+
+int cm_write_volume_mrc(cm_ctx* ctx, const char* path, double voxel_size) {
+    CTX_GUARD(ctx);
+    if (!path) return fail(CM_ERR_INVALID_ARGUMENT, "null path");
+    const float* src = ctx->impl->mrc_result_f32();
+    if (!src) return fail(CM_ERR_STATE, "no solver result resident");
+    if (!ctx->mrc) ctx->mrc.reset(new MrcRing());
+    CKS(ctx->mrc->ensure());
+    return mrc_write_volume(path, ctx->n, voxel_size, src, *ctx->mrc, ctx->impl->stream);
 }
 
 int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap) {

@@ -149,6 +149,20 @@ __global__ void to_real_kernel(const double* __restrict__ in, R* __restrict__ ou
         out[q] = R(in[q]);
 }
 
+// MRC payloads (mode 2 float32) <-> the working precision
+template <typename R>
+__global__ void f32_to_real_kernel(const float* __restrict__ in, R* __restrict__ out, size_t L) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < L;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = (R)in[i];
+}
+template <typename R>
+__global__ void real_to_f32_kernel(const R* __restrict__ in, float* __restrict__ out, size_t L) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < L;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];  // round to nearest, as float(double) in write_mrc
+}
+
 template <typename R>
 __global__ void to_double_kernel(const R* __restrict__ in, double* __restrict__ out, size_t L) {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < L;
@@ -312,6 +326,13 @@ struct ImplBase {
     virtual int fsc_with(ImplBase* other, double* curve) = 0;
     virtual int result_to_spectrum() = 0;  // S <- fft3 of the resident result
     virtual long long bytes() const = 0;
+    // MRC I/O (cm_api.cu): float32 payload landing zone of volume `which`
+    // (0 init, 1 anchor) -- the volume itself in fp32, a staging area in fp64 --
+    // then mrc_commit(which) (stream-ordered conversion; which 2: anchor = init)
+    virtual float* mrc_landing(int which) = 0;
+    virtual int mrc_commit(int which) = 0;
+    // the resident result as float32 on the device (stream-ordered), or null
+    virtual const float* mrc_result_f32() = 0;
 
     cudaStream_t stream = nullptr;
     int n = 0;
@@ -1116,6 +1137,40 @@ struct Impl final : ImplBase {
         if (rs.stop_reason == 3)
             return fail(CM_ERR_STEP_DIVERGED, "m_step: frozen-weight objective increased");
         return CM_OK;
+    }
+
+    float* mrc_landing(int which) override {
+        if constexpr (sizeof(R) == 4)
+            return reinterpret_cast<float*>(which == 0 ? x0keep : anchor);
+        else
+            return reinterpret_cast<float*>(stage);
+    }
+    int mrc_commit(int which) override {
+        if constexpr (sizeof(R) == 8) {
+            if (which < 2) {
+                f32_to_real_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(
+                    reinterpret_cast<const float*>(stage), which == 0 ? x0keep : anchor, L);
+                CK(cudaGetLastError());
+            }
+        }
+        if (which == 2)
+            CK(cudaMemcpyAsync(anchor, x0keep, sizeof(R) * L, cudaMemcpyDeviceToDevice, stream));
+        if (which != 0) {
+            anchor_is_init = which == 2;
+            vol_set = true;
+        }
+        return CM_OK;
+    }
+    const float* mrc_result_f32() override {
+        if (!vol_set || !result_valid) return nullptr;
+        const R* src = last_fista ? XF[last_iter % 2] : X[last_iter % 3];
+        if constexpr (sizeof(R) == 4) {
+            return reinterpret_cast<const float*>(src);
+        } else {
+            float* dst = reinterpret_cast<float*>(stage);
+            real_to_f32_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(src, dst, L);
+            return cudaGetLastError() == cudaSuccess ? dst : nullptr;
+        }
     }
 
     int get_volume(double* out) override {

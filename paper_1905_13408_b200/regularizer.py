@@ -62,7 +62,7 @@ class DeviceError(Error):
 _CODES = {
     1: InvalidArgument, 2: GridMismatch, 3: NonHermitianAccumulator, 4: StepDiverged,
     5: DeviceError, 6: DeviceError, 7: NonPositiveScale, 8: NonHermitianInput,
-    9: InvalidArgument, 10: Error,
+    9: InvalidArgument, 10: Error, 11: OSError, 12: OSError, 13: OSError, 14: OSError,
 }
 
 
@@ -330,6 +330,18 @@ class Context:
         out = np.empty((self.n,) * 3, np.float64)
         _check(self.lib.cm_get_volume(self.ptr, out.ctypes.data))
         return out
+
+    def set_volumes_mrc(self, path_init, path_anchor=None) -> None:
+        """x_init (and x_anchor; None: the same object) from MRC files, read
+        into pinned chunks and copied straight to the device (mrc.cpp:156
+        checks and errors; cm_set_volumes_mrc)."""
+        pa = None if path_anchor is None else os.fsencode(path_anchor)
+        _check(self.lib.cm_set_volumes_mrc(self.ptr, os.fsencode(path_init), pa))
+
+    def write_volume_mrc(self, path, voxel_size: float = 1.0) -> None:
+        """The resident solve result as write_mrc(path, Volume3D(x, voxel_size))
+        writes it, byte for byte (mrc.cpp:134; cm_write_volume_mrc)."""
+        _check(self.lib.cm_write_volume_mrc(self.ptr, os.fsencode(path), float(voxel_size)))
 
     def scale_data(self) -> DataScales:
         a, b = C.c_double(), C.c_double()

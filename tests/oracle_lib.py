@@ -254,6 +254,19 @@ class Reference(_Lib):
         assert rc == 0, self.last_error()
         return out
 
+    def write_mrc_volume(self, path, x, voxel_size=1.0):
+        """write_mrc(path, Volume3D) by the reference (mrc.cpp:134)."""
+        x = np.ascontiguousarray(x, np.float64)
+        return self.f("write_mrc_volume")(os.fsencode(str(path)), x.shape[0],
+                                          C.c_double(voxel_size), _d(x))
+
+    def read_mrc_volume(self, path, n):
+        """read_mrc_volume(path) by the reference -> (status, volume, voxel size)."""
+        out = np.zeros((n, n, n))
+        vs = C.c_double(0.0)
+        rc = self.f("read_mrc_volume")(os.fsencode(str(path)), n, _d(out), C.byref(vs))
+        return rc, out, vs.value
+
     def symmetry_residue(self, w, y):
         out = C.c_double()
         self.f("symmetry_residue")(w.shape[0], _d(w), _d(y), C.byref(out))
