@@ -140,6 +140,34 @@ int cm_write_volume_mrc(cm_ctx* ctx, const char* path, double voxel_size);
  * Both results stay resident. */
 int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap);
 
+/* Backprojection: backproject_accumulate
+ * (backproject.hpp:26-30, backproject.cpp:12-101) on the device, Friedel
+ * finalize included, straight into the context's resident accumulator (as if
+ * cm_set_accumulator(weight, numerator, finalized=1) had been called), so the
+ * M-step that follows needs no upload. weight_out / numerator_out (L doubles /
+ * L complex interleaved, AccumulatorPair layout) receive a copy when non-NULL.
+ * The flat input mirrors ParticleSet, the PosteriorRow list and
+ * OrientationGrid: */
+typedef struct {
+    int n_images;
+    const double* images;   /* [n_images][n*n] complex interleaved: ParticleImage::f */
+    const double* image_params; /* [n_images][6]: voltage_kv, defocus_A, cs_mm,
+                                   amplitude_contrast, identity_flag (0/1), voxel_size */
+    int n_poses;
+    const double* poses;    /* [n_poses][3]: rot, tilt, psi (degrees), pose.hpp:10 */
+    int n_shifts;
+    const int* shifts;      /* [n_shifts][2]: dx, dy (orientation.hpp:17) */
+    long long n_entries;    /* the rows' (candidate, posterior) entries, flattened */
+    const long long* entry_particle;
+    const unsigned* entry_candidate; /* pose * n_shifts + shift */
+    const double* entry_posterior;   /* entries <= 0 are skipped (backproject.cpp:43) */
+    int kernel_kind;        /* KernelKind: 0 gaussian, 1 trilinear (kernel.hpp:6) */
+    double bandwidth;       /* gaussian only; must be > 0 (kernel.cpp:7-10) */
+    double radius_cutoff;   /* < 0: the full plane (backproject.cpp:20) */
+} cm_bp_input;
+int cm_backproject(cm_ctx* ctx, const cm_bp_input* in, double* weight_out,
+                   double* numerator_out);
+
 /* Diagnostics: when on, cm_solve launches every kernel individually between
  * CUDA events on the context stream (no graph) and accumulates per-kernel
  * device time, ms7 = {z pass (tile + column-0 kernels), y inverse, x C2R,

@@ -28,6 +28,7 @@
 #include "cryomap/fsc.hpp"
 #include "cryomap/gradient.hpp"
 #include "cryomap/mrc.hpp"
+#include "cryomap/orientation.hpp"
 #include "cryomap/params.hpp"
 #include "cryomap/phantom.hpp"
 #include "cryomap/regularizer.hpp"
@@ -308,6 +309,55 @@ int ref_fsc_volumes(int n, const double* a, const double* b, double* curve) {
     return guard([&] {
         FSCCurve c = fsc(fft3_centered(to_vol(n, a)), fft3_centered(to_vol(n, b)));
         std::memcpy(curve, c.value.data(), sizeof(double) * c.value.size());
+    });
+}
+
+// backproject_accumulate (backproject.cpp:12-101) over the flat cm_bp_input
+// layout (include/cm_api.h): consecutive entries of one particle form a row.
+int ref_backproject(int n, int n_images, const double* images, const double* image_params,
+                    int n_poses, const double* poses, int n_shifts, const int* shifts,
+                    long long n_entries, const long long* entry_particle,
+                    const unsigned* entry_candidate, const double* entry_posterior,
+                    int kernel_kind, double bandwidth, double radius_cutoff, int threads,
+                    double* weight_out, double* numerator_out) {
+    return guard([&] {
+        ParticleSet parts;
+        parts.side_n = n;
+        parts.voxel_size = n_images > 0 ? image_params[5] : 1.0;
+        const size_t plane = size_t(n) * n;
+        for (int i = 0; i < n_images; ++i) {
+            ParticleImage img;
+            img.side_n = n;
+            const double* ip = image_params + 6 * size_t(i);
+            img.ctf.voltage_kv = ip[0];
+            img.ctf.defocus_A = ip[1];
+            img.ctf.cs_mm = ip[2];
+            img.ctf.amplitude_contrast = ip[3];
+            img.ctf.identity_flag = ip[4] != 0.0;
+            img.voxel_size = ip[5];
+            img.f.resize(plane);
+            std::memcpy(img.f.data(), images + 2 * plane * size_t(i), sizeof(double) * 2 * plane);
+            img.id = i;
+            parts.items.push_back(std::move(img));
+        }
+        OrientationGrid grid;
+        grid.side_n = n;
+        for (int q = 0; q < n_poses; ++q)
+            grid.poses.push_back(Pose{poses[3 * q], poses[3 * q + 1], poses[3 * q + 2], 0.0, 0.0});
+        for (int q = 0; q < n_shifts; ++q) grid.shifts.emplace_back(shifts[2 * q], shifts[2 * q + 1]);
+        std::vector<PosteriorRow> rows;
+        for (long long e = 0; e < n_entries; ++e) {
+            if (rows.empty() || rows.back().particle != size_t(entry_particle[e])) {
+                rows.emplace_back();
+                rows.back().particle = size_t(entry_particle[e]);
+            }
+            rows.back().entries.emplace_back(entry_candidate[e], entry_posterior[e]);
+        }
+        const KernelSpec kernel{kernel_kind == 0 ? KernelKind::gaussian : KernelKind::trilinear,
+                                bandwidth};
+        AccumulatorPair acc = backproject_accumulate(parts, rows, kernel, grid, radius_cutoff, threads);
+        std::memcpy(weight_out, acc.weight.data(), sizeof(double) * acc.weight.size());
+        std::memcpy(numerator_out, acc.numerator.data(), sizeof(double) * 2 * acc.numerator.size());
     });
 }
 

@@ -14,6 +14,7 @@ from .regularizer import (  # noqa: F401
 )
 
 from . import slab  # noqa: F401,E402
+from .backproject import BackprojectInput, backproject_accumulate, backproject_into  # noqa: F401,E402
 from .slab import SlabContext, SlabPlan  # noqa: F401,E402
 
 __version__ = "0.1.0"

@@ -1,0 +1,112 @@
+"""Device backprojection: backproject_accumulate (backproject.hpp:26-30,
+backproject.cpp:12-101) through cm_backproject, SURVEY §8(f) rank 2.
+
+The inputs are the reference's ParticleSet, PosteriorRow list and
+OrientationGrid in flat arrays (include/cm_api.h, cm_bp_input). The
+accumulator is produced on the device, Friedel-finalized, and left resident in
+the context as its M-step accumulator; the host copy is optional.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from .regularizer import AccumulatorPair, Context, _check
+
+
+class cm_bp_input(C.Structure):
+    _fields_ = [
+        ("n_images", C.c_int),
+        ("images", C.c_void_p),
+        ("image_params", C.c_void_p),
+        ("n_poses", C.c_int),
+        ("poses", C.c_void_p),
+        ("n_shifts", C.c_int),
+        ("shifts", C.c_void_p),
+        ("n_entries", C.c_longlong),
+        ("entry_particle", C.c_void_p),
+        ("entry_candidate", C.c_void_p),
+        ("entry_posterior", C.c_void_p),
+        ("kernel_kind", C.c_int),
+        ("bandwidth", C.c_double),
+        ("radius_cutoff", C.c_double),
+    ]
+
+
+GAUSSIAN, TRILINEAR = 0, 1  # KernelKind order, kernel.hpp:6
+
+
+@dataclass
+class BackprojectInput:
+    """ParticleSet + posterior rows + OrientationGrid, flattened.
+
+    images:          complex128 (m, n, n), ParticleImage::f (row l, column k,
+                     storage indices)
+    image_params:    float64 (m, 6): voltage_kv, defocus_A, cs_mm,
+                     amplitude_contrast, identity_flag, voxel_size
+    poses:           float64 (p, 3): rot, tilt, psi in degrees
+    shifts:          int32 (s, 2): dx, dy
+    entry_particle / entry_candidate / entry_posterior: one per (row, entry),
+                     candidate = pose * s + shift (orientation.hpp:19-21)
+    """
+    images: np.ndarray
+    image_params: np.ndarray
+    poses: np.ndarray
+    shifts: np.ndarray
+    entry_particle: np.ndarray
+    entry_candidate: np.ndarray
+    entry_posterior: np.ndarray
+    kernel_kind: int = GAUSSIAN
+    bandwidth: float = 2.0
+    radius_cutoff: float = -1.0
+
+    def __post_init__(self):
+        self.images = np.ascontiguousarray(self.images, np.complex128)
+        self.image_params = np.ascontiguousarray(self.image_params, np.float64).reshape(-1, 6)
+        self.poses = np.ascontiguousarray(self.poses, np.float64).reshape(-1, 3)
+        self.shifts = np.ascontiguousarray(self.shifts, np.int32).reshape(-1, 2)
+        self.entry_particle = np.ascontiguousarray(self.entry_particle, np.int64)
+        self.entry_candidate = np.ascontiguousarray(self.entry_candidate, np.uint32)
+        self.entry_posterior = np.ascontiguousarray(self.entry_posterior, np.float64)
+
+    @property
+    def side_n(self) -> int:
+        return int(self.images.shape[-1])
+
+    def to_c(self) -> cm_bp_input:
+        d = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+        return cm_bp_input(
+            int(self.images.shape[0]), d(self.images), d(self.image_params),
+            int(self.poses.shape[0]), d(self.poses), int(self.shifts.shape[0]), d(self.shifts),
+            int(self.entry_posterior.size), d(self.entry_particle), d(self.entry_candidate),
+            d(self.entry_posterior), int(self.kernel_kind), float(self.bandwidth),
+            float(self.radius_cutoff))
+
+
+def backproject_into(ctx: Context, inp: BackprojectInput, download: bool = True):
+    """Accumulate on the device into ctx's resident accumulator (finalized);
+    returns the AccumulatorPair copy when `download`."""
+    n = ctx.n
+    if inp.side_n != n:
+        from .regularizer import GridMismatch
+        raise GridMismatch(f"backproject: images of side {inp.side_n}, context side {n}")
+    c = inp.to_c()
+    w = np.empty((n, n, n), np.float64) if download else None
+    y = np.empty((n, n, n), np.complex128) if download else None
+    _check(ctx.lib.cm_backproject(ctx.ptr, C.byref(c), None if w is None else w.ctypes.data,
+                                  None if y is None else y.ctypes.data))
+    if not download:
+        return None
+    vox = float(inp.image_params[0, 5]) if inp.image_params.size else 1.0
+    return AccumulatorPair(n, y, w, True, vox)
+
+
+def backproject_accumulate(inp: BackprojectInput, precision: int | None = None) -> AccumulatorPair:
+    """backproject_accumulate (backproject.hpp:26) on the device, host result."""
+    ctx = Context(inp.side_n, precision=precision)
+    try:
+        return backproject_into(ctx, inp, download=True)
+    finally:
+        ctx.close()

@@ -9,6 +9,7 @@
 #include "dist.cuh"
 #include "impl.cuh"
 #include "mrc_io.h"
+#include "backproject.cuh"
 
 namespace cm {
 
@@ -245,6 +246,22 @@ int cm_write_volume_mrc(cm_ctx* ctx, const char* path, double voxel_size) {
     if (!ctx->mrc) ctx->mrc.reset(new MrcRing());
     CKS(ctx->mrc->ensure());
     return mrc_write_volume(path, ctx->n, voxel_size, src, *ctx->mrc, ctx->impl->stream);
+}
+
+int cm_backproject(cm_ctx* ctx, const cm_bp_input* in, double* weight_out, double* numerator_out) {
+    CTX_GUARD(ctx);
+    ImplBase* im = ctx->impl.get();
+    double* stage = im->acc_stage();
+    im->acc_set = false;  // the staging grid is about to be overwritten
+    CKS(backproject_run(ctx->n, in, stage, im->stream));
+    const size_t L = (size_t)ctx->n * ctx->n * ctx->n;
+    if (weight_out &&
+        cudaMemcpyAsync(weight_out, stage, sizeof(double) * L, cudaMemcpyDeviceToHost, im->stream) != cudaSuccess)
+        return fail(CM_ERR_CUDA, "backproject: download failed");
+    if (numerator_out && cudaMemcpyAsync(numerator_out, stage + L, sizeof(double) * 2 * L,
+                                         cudaMemcpyDeviceToHost, im->stream) != cudaSuccess)
+        return fail(CM_ERR_CUDA, "backproject: download failed");
+    return im->commit_acc_stage(1);
 }
 
 int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap) {

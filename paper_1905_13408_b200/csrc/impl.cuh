@@ -333,6 +333,10 @@ struct ImplBase {
     virtual int mrc_commit(int which) = 0;
     // the resident result as float32 on the device (stream-ordered), or null
     virtual const float* mrc_result_f32() = 0;
+    // accumulator staging (3L doubles: weight, numerator interleaved) and its
+    // conversion to the resident W / Y (backproject.cuh writes it on the device)
+    virtual double* acc_stage() = 0;
+    virtual int commit_acc_stage(int finalized) = 0;
 
     cudaStream_t stream = nullptr;
     int n = 0;
@@ -721,6 +725,12 @@ struct Impl final : ImplBase {
     int set_accumulator(const double* w, const double* y, int finalized) override {
         CK(cudaMemcpyAsync(stage, w, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(stage + L, y, sizeof(double) * 2 * L, cudaMemcpyHostToDevice, stream));
+        return commit_acc_stage(finalized);
+    }
+    double* acc_stage() override { return stage; }
+    // the accumulator in `stage` (weight [L], numerator [L] complex interleaved),
+    // written there by set_accumulator's upload or by the device backprojection
+    int commit_acc_stage(int finalized) override {
         CK(cudaMemsetAsync(maxes, 0, sizeof(unsigned long long) * 4, stream));
         const int blocks = grid_for(NN * (Nh + 1), 256);
         convert_acc_kernel<R><<<blocks, 256, 0, stream>>>(N, stage, stage + L, W, Wn, Yh, Yn,

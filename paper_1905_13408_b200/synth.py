@@ -229,3 +229,46 @@ def synthetic_problem(n: int, n_blobs: int | None = None, phantom_seed: int = 77
     y = w * fft3_centered(x0)
     eps = 0.1 * float(np.max(np.abs(t)))
     return Problem(n, t, w, y, x0, eps, eps / 3.0)
+
+
+def synthetic_backprojection(n: int, n_images: int, n_poses: int = 12, trans_radius: int = 1,
+                             entries_per_image: int = 3, kernel_kind: int = 0,
+                             radius_cutoff: float = -1.0, seed: int = 0,
+                             grid_angles: bool = True, identity_ctf: bool = False):
+    """Backprojection inputs of the reference's shapes (ParticleSet, posterior
+    rows, OrientationGrid): random Fourier images, realistic CTFs
+    (ctf.hpp:9-14 defaults, defocus varied per image), poses on a 15-degree
+    lattice (grid_angles; exercises exact-.5 rotated points) or uniform, the
+    integer shift disc of radius trans_radius (orientation.hpp:17), and a few
+    candidates per image with random posteriors, one of them 0 (skipped,
+    backproject.cpp:43)."""
+    from .backproject import BackprojectInput
+    rng = np.random.default_rng(seed)
+    images = (rng.standard_normal((n_images, n, n)) + 1j * rng.standard_normal((n_images, n, n)))
+    params = np.zeros((n_images, 6))
+    params[:, 0] = 300.0
+    params[:, 1] = rng.uniform(8000.0, 25000.0, n_images)
+    params[:, 2] = 2.0
+    params[:, 3] = 0.07
+    params[:, 4] = 1.0 if identity_ctf else 0.0
+    params[:, 5] = 1.2
+    if grid_angles:
+        poses = np.stack([rng.integers(0, 24, n_poses) * 15.0, rng.integers(0, 13, n_poses) * 15.0,
+                          rng.integers(0, 24, n_poses) * 15.0], axis=1)
+    else:
+        poses = np.stack([rng.uniform(0, 360, n_poses), rng.uniform(0, 180, n_poses),
+                          rng.uniform(0, 360, n_poses)], axis=1)
+    r = trans_radius
+    shifts = np.array([(dx, dy) for dy in range(-r, r + 1) for dx in range(-r, r + 1)
+                       if dx * dx + dy * dy <= r * r], np.int32)
+    ncand = n_poses * len(shifts)
+    ep, ec, epost = [], [], []
+    for i in range(n_images):
+        cands = rng.choice(ncand, size=min(entries_per_image, ncand), replace=False)
+        post = rng.dirichlet(np.ones(len(cands)))
+        post[-1] = 0.0
+        ep += [i] * len(cands)
+        ec += list(cands)
+        epost += list(post)
+    return BackprojectInput(images, params, poses, shifts, np.array(ep), np.array(ec),
+                            np.array(epost), kernel_kind, 2.0, radius_cutoff)

@@ -254,6 +254,21 @@ class Reference(_Lib):
         assert rc == 0, self.last_error()
         return out
 
+    def backproject(self, inp, threads=1):
+        """backproject_accumulate (backproject.cpp:12) on a BackprojectInput
+        -> (status, weight, numerator)."""
+        n = inp.side_n
+        w = np.zeros((n, n, n))
+        y = np.zeros((n, n, n), np.complex128)
+        p = lambda a: C.c_void_p(a.ctypes.data if a.size else None)  # noqa: E731
+        rc = self.f("backproject")(
+            n, inp.images.shape[0], p(inp.images), p(inp.image_params), inp.poses.shape[0],
+            p(inp.poses), inp.shifts.shape[0], p(inp.shifts), C.c_longlong(inp.entry_posterior.size),
+            p(inp.entry_particle), p(inp.entry_candidate), p(inp.entry_posterior),
+            int(inp.kernel_kind), C.c_double(inp.bandwidth), C.c_double(inp.radius_cutoff),
+            int(threads), _d(w), C.c_void_p(y.ctypes.data))
+        return rc, w, y
+
     def write_mrc_volume(self, path, x, voxel_size=1.0):
         """write_mrc(path, Volume3D) by the reference (mrc.cpp:134)."""
         x = np.ascontiguousarray(x, np.float64)
