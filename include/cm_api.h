@@ -168,6 +168,31 @@ typedef struct {
 int cm_backproject(cm_ctx* ctx, const cm_bp_input* in, double* weight_out,
                    double* numerator_out);
 
+/* E-step: e_step (estep.hpp:44-54, estep.cpp:64-270) on
+ * the device. posterior receives the dense [n_images][n_poses * n_shifts]
+ * matrix: row i holds PosteriorRow i's entries at their candidate indices
+ * (pose * n_shifts + shift) and exact zeros elsewhere (pruned candidates),
+ * each row summing to 1. volume NULL: V = fft3_centered of the context's
+ * resident solve result (the M-step -> E-step hand-off of em_refine,
+ * refine.cpp:182 -> 150, with no V transfer). */
+typedef struct {
+    int n_images;
+    const double* images;       /* as cm_bp_input */
+    const double* image_params; /* as cm_bp_input */
+    int n_poses;
+    const double* poses;        /* [n_poses][3] */
+    int n_shifts;
+    const int* shifts;          /* [n_shifts][2]; must include (0, 0) */
+    int kernel_kind;
+    double bandwidth;
+    double radius_cutoff;       /* < 0: Nyquist (estep.cpp:14-17) */
+    int n_sigma2;
+    const double* sigma2;       /* NoiseSpectrum::sigma2, per 2D shell */
+    double prune_floor;         /* estep.hpp:52 default 1e-8 */
+    const double* volume;       /* FourierVolume [n^3] complex interleaved, or NULL */
+} cm_estep_input;
+int cm_estep(cm_ctx* ctx, const cm_estep_input* in, double* posterior);
+
 /* Diagnostics: when on, cm_solve launches every kernel individually between
  * CUDA events on the context stream (no graph) and accumulates per-kernel
  * device time, ms7 = {z pass (tile + column-0 kernels), y inverse, x C2R,

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "cryomap/backproject.hpp"
+#include "cryomap/estep.hpp"
 #include "cryomap/fourier.hpp"
 #include "cryomap/fsc.hpp"
 #include "cryomap/gradient.hpp"
@@ -358,6 +359,50 @@ int ref_backproject(int n, int n_images, const double* images, const double* ima
         AccumulatorPair acc = backproject_accumulate(parts, rows, kernel, grid, radius_cutoff, threads);
         std::memcpy(weight_out, acc.weight.data(), sizeof(double) * acc.weight.size());
         std::memcpy(numerator_out, acc.numerator.data(), sizeof(double) * 2 * acc.numerator.size());
+    });
+}
+
+// e_step (estep.cpp:64-270) over the flat cm_estep_input layout; the rows are
+// scattered into a dense [n_images][n_poses * n_shifts] matrix
+int ref_estep(int n, int n_images, const double* images, const double* image_params, int n_poses,
+              const double* poses, int n_shifts, const int* shifts, int kernel_kind, double bandwidth,
+              double radius_cutoff, int n_sigma2, const double* sigma2, double prune_floor,
+              const double* volume, int threads, double* dense_out) {
+    return guard([&] {
+        ParticleSet parts;
+        parts.side_n = n;
+        parts.voxel_size = n_images > 0 ? image_params[5] : 1.0;
+        const size_t plane = size_t(n) * n;
+        for (int i = 0; i < n_images; ++i) {
+            ParticleImage img;
+            img.side_n = n;
+            const double* ip = image_params + 6 * size_t(i);
+            img.ctf.voltage_kv = ip[0];
+            img.ctf.defocus_A = ip[1];
+            img.ctf.cs_mm = ip[2];
+            img.ctf.amplitude_contrast = ip[3];
+            img.ctf.identity_flag = ip[4] != 0.0;
+            img.voxel_size = ip[5];
+            img.f.resize(plane);
+            std::memcpy(img.f.data(), images + 2 * plane * size_t(i), sizeof(double) * 2 * plane);
+            parts.items.push_back(std::move(img));
+        }
+        OrientationGrid grid;
+        grid.side_n = n;
+        for (int q = 0; q < n_poses; ++q)
+            grid.poses.push_back(Pose{poses[3 * q], poses[3 * q + 1], poses[3 * q + 2], 0.0, 0.0});
+        for (int q = 0; q < n_shifts; ++q) grid.shifts.emplace_back(shifts[2 * q], shifts[2 * q + 1]);
+        FourierVolume V(n, parts.voxel_size);
+        std::memcpy(V.data.data(), volume, sizeof(double) * 2 * V.data.size());
+        NoiseSpectrum noise;
+        noise.sigma2.assign(sigma2, sigma2 + n_sigma2);
+        const KernelSpec kernel{kernel_kind == 0 ? KernelKind::gaussian : KernelKind::trilinear,
+                                bandwidth};
+        auto rows = e_step(parts, V, grid, kernel, noise, radius_cutoff, prune_floor, threads);
+        const size_t nc = size_t(n_poses) * n_shifts;
+        std::memset(dense_out, 0, sizeof(double) * nc * n_images);
+        for (const PosteriorRow& r : rows)
+            for (const auto& [c, w] : r.entries) dense_out[r.particle * nc + c] = w;
     });
 }
 

@@ -14,7 +14,9 @@ from .regularizer import (  # noqa: F401
 )
 
 from . import slab  # noqa: F401,E402
-from .backproject import BackprojectInput, backproject_accumulate, backproject_into  # noqa: F401,E402
+from .backproject import (  # noqa: F401,E402
+    BackprojectInput, backproject_accumulate, backproject_into, e_step, posterior_entries,
+)
 from .slab import SlabContext, SlabPlan  # noqa: F401,E402
 
 __version__ = "0.1.0"

@@ -110,3 +110,55 @@ def backproject_accumulate(inp: BackprojectInput, precision: int | None = None) 
         return backproject_into(ctx, inp, download=True)
     finally:
         ctx.close()
+
+
+class cm_estep_input(C.Structure):
+    _fields_ = [
+        ("n_images", C.c_int),
+        ("images", C.c_void_p),
+        ("image_params", C.c_void_p),
+        ("n_poses", C.c_int),
+        ("poses", C.c_void_p),
+        ("n_shifts", C.c_int),
+        ("shifts", C.c_void_p),
+        ("kernel_kind", C.c_int),
+        ("bandwidth", C.c_double),
+        ("radius_cutoff", C.c_double),
+        ("n_sigma2", C.c_int),
+        ("sigma2", C.c_void_p),
+        ("prune_floor", C.c_double),
+        ("volume", C.c_void_p),
+    ]
+
+
+def e_step(ctx: Context, inp: BackprojectInput, sigma2, volume=None,
+           prune_floor: float = 1e-8) -> np.ndarray:
+    """e_step (estep.hpp:44-54) on the device -> dense posterior
+    [images][poses * shifts] (PosteriorRow entries at their candidate index,
+    exact zeros elsewhere). The particles, grid and kernel come from `inp`
+    (its entry arrays are ignored); volume None: V = fft3_centered of ctx's
+    resident solve result, never leaving the device."""
+    n = ctx.n
+    if inp.side_n != n:
+        from .regularizer import GridMismatch
+        raise GridMismatch(f"e_step: images of side {inp.side_n}, context side {n}")
+    s2 = np.ascontiguousarray(sigma2, np.float64).ravel()
+    V = None if volume is None else np.ascontiguousarray(volume, np.complex128)
+    if V is not None and V.shape != (n, n, n):
+        from .regularizer import GridMismatch
+        raise GridMismatch("e_step: volume side differs from the context")
+    d = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
+    c = cm_estep_input(int(inp.images.shape[0]), d(inp.images), d(inp.image_params),
+                       int(inp.poses.shape[0]), d(inp.poses), int(inp.shifts.shape[0]),
+                       d(inp.shifts), int(inp.kernel_kind), float(inp.bandwidth),
+                       float(inp.radius_cutoff), int(s2.size), d(s2), float(prune_floor), d(V))
+    out = np.zeros((inp.images.shape[0], inp.poses.shape[0] * inp.shifts.shape[0]))
+    _check(ctx.lib.cm_estep(ctx.ptr, C.byref(c), out.ctypes.data))
+    return out
+
+
+def posterior_entries(dense: np.ndarray):
+    """Dense posterior -> the flat (particle, candidate, weight) entry arrays
+    of cm_bp_input, in PosteriorRow order."""
+    part, cand = np.nonzero(dense)
+    return part.astype(np.int64), cand.astype(np.uint32), dense[part, cand]

@@ -10,6 +10,7 @@
 #include "impl.cuh"
 #include "mrc_io.h"
 #include "backproject.cuh"
+#include "estep.cuh"
 
 namespace cm {
 
@@ -262,6 +263,17 @@ int cm_backproject(cm_ctx* ctx, const cm_bp_input* in, double* weight_out, doubl
                                          cudaMemcpyDeviceToHost, im->stream) != cudaSuccess)
         return fail(CM_ERR_CUDA, "backproject: download failed");
     return im->commit_acc_stage(1);
+}
+
+int cm_estep(cm_ctx* ctx, const cm_estep_input* in, double* posterior) {
+    CTX_GUARD(ctx);
+    if (!in || !posterior) return fail(CM_ERR_INVALID_ARGUMENT, "e_step: null argument");
+    const double* vdev = nullptr;
+    if (!in->volume) {
+        vdev = ctx->impl->result_spectrum_device(1);
+        if (!vdev) return fail(CM_ERR_STATE, "e_step: no volume given and no solver result resident");
+    }
+    return estep_run(ctx->n, in, in->volume, vdev, posterior, ctx->impl->stream);
 }
 
 int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap) {

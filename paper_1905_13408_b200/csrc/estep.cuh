@@ -1,0 +1,371 @@
+// E-step on the device (reference: e_step,
+// estep.cpp:64-270, with sample_slice slice.cpp:24-45).
+//
+// Posterior over (pose, shift) candidates per particle, proportional to
+// exp(-R/2) with the whitened residual
+//   R = A + b - 2 Re sum_j (w ctf X_j) conj(S_j) ph_s,j,
+//   A = sum_j w |X_j|^2,  b = sum_j w ctf^2 |S_j|^2,
+// the reference's exact-safe pose pruning (lower bound LB = A + b - 2 sum_j
+// w |ctf| |X_j| |S_j| against the best zero-shift residual U plus
+// 2 ln(1 / prune_floor)), a max-subtracted softmax over the surviving
+// candidates, then the prune_floor cut and renormalisation.
+//
+// Mapping: slices S[pose][j] are gathered once (one thread per pose and
+// component: the 27 / 8 kernel taps of the rotated frequency, 24 MB at 128^2 x
+// 100 poses -- L2-resident for the sweeps); the per-particle tables
+// (w ctf X, w ctf^2, w |ctf| |X|) once; then one CTA per (particle, pose)
+// reduces over the components, particle-major so a particle's table and all
+// slices stay in L2 while its poses are swept. Pass 2 evaluates all shifts of
+// a surviving pose from one read of its terms, eight shifts per reduction.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/cm_api.h"
+#include "backproject.cuh"
+#include "cm_common.cuh"
+
+namespace cm {
+
+struct EsDev {
+    const double2* V;       // FourierVolume [n^3] (storage indices)
+    const double2* img;     // [npart][n*n]
+    const double* ip;       // [npart][6]
+    const double* mats;     // [npose][9]
+    const int2* comps;      // [ncomp]
+    const double* invsig;   // [ncomp]
+    double* phr;            // [nshift][ncomp]
+    double* phi;
+    double2* slice;         // [npose][ncomp]
+    double *p1r, *p1i, *p2, *pab;  // [npart][ncomp]
+    double *A, *R0, *LB, *U;
+    double* res;            // [npart][npose * nshift]
+    int n, ncomp, npose, nshift, npart;
+    double slack, floor_, bandwidth;
+};
+
+constexpr int ES_NT = 256;
+
+template <int NV>
+__device__ __forceinline__ void es_block_sum(double (&v)[NV], double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) red[w * NV + q] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double s = 0.0;
+        for (int k = 0; k < ES_NT / 32; ++k) s += red[k * NV + q];
+        v[q] = s;
+    }
+}
+
+__device__ __forceinline__ double es_block_min(double v, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = red[0];
+    for (int k = 1; k < ES_NT / 32; ++k) s = fmin(s, red[k]);
+    return s;
+}
+
+// sample_slice (slice.cpp:24-45): kernel-weighted normalised interpolation
+template <int KIND>
+__global__ void es_slice_kernel(EsDev p) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)p.npose * p.ncomp) return;
+    const int pose = (int)(t / p.ncomp), j = (int)(t % p.ncomp);
+    const int n = p.n, lo = -n / 2, hi = n / 2 - 1;
+    const double* R = p.mats + 9 * (size_t)pose;
+    const int k = p.comps[j].x, l = p.comps[j].y;
+    double nj[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)  // as in backproject.cuh (the reference's as-built order)
+        nj[a] = __dadd_rn(__fma_rn(R[3 * a], (double)k, __dmul_rn(R[3 * a + 1], (double)l)),
+                          __dmul_rn(R[3 * a + 2], 0.0));
+    double ar = 0.0, ai = 0.0, ws = 0.0;
+    auto tap = [&](int px, int py, int pz, double w) {
+        if (px < lo || px > hi || py < lo || py > hi || pz < lo || pz > hi) return;
+        const double2 v = p.V[((size_t)bp_store(pz, n) * n + bp_store(py, n)) * n + bp_store(px, n)];
+        ar += w * v.x;
+        ai += w * v.y;
+        ws += w;
+    };
+    if constexpr (KIND == 0) {
+        int anc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) anc[a] = (int)llround(nj[a]);
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int q[3] = {anc[0] + dx, anc[1] + dy, anc[2] + dz};
+                    double d2 = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const double d = nj[a] - (double)q[a];
+                        d2 += d * d;
+                    }
+                    tap(q[0], q[1], q[2], exp(-d2 / p.bandwidth));
+                }
+    } else {
+        int lo3[3];
+        double fr[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo3[a] = (int)floor(nj[a]);
+            fr[a] = nj[a] - (double)lo3[a];
+        }
+        const int cz1 = fr[2] == 0.0 ? 0 : 1, cy1 = fr[1] == 0.0 ? 0 : 1, cx1 = fr[0] == 0.0 ? 0 : 1;
+        for (int cz = 0; cz <= cz1; ++cz)
+            for (int cy = 0; cy <= cy1; ++cy)
+                for (int cx = 0; cx <= cx1; ++cx)
+                    tap(lo3[0] + cx, lo3[1] + cy, lo3[2] + cz,
+                        (cx ? fr[0] : 1.0 - fr[0]) * (cy ? fr[1] : 1.0 - fr[1]) *
+                            (cz ? fr[2] : 1.0 - fr[2]));
+    }
+    p.slice[t] = ws > 0.0 ? make_double2(ar / ws, ai / ws) : make_double2(0.0, 0.0);
+}
+
+// shift phase tables (slice.cpp:47-50), [nshift][ncomp]
+__global__ void es_phase_kernel(EsDev p, const int2* shifts) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)p.nshift * p.ncomp) return;
+    const int s = (int)(t / p.ncomp), j = (int)(t % p.ncomp);
+    const int k = p.comps[j].x, l = p.comps[j].y;
+    const double ph = -2.0 * 3.14159265358979323846 * ((double)k * shifts[s].x + (double)l * shifts[s].y) /
+                      (double)p.n;
+    double sn, cs;
+    sincos(ph, &sn, &cs);
+    p.phr[t] = cs;
+    p.phi[t] = sn;
+}
+
+// per-particle tables (estep.cpp:167-186) and A by one CTA per particle
+__global__ void __launch_bounds__(ES_NT) es_ptab_kernel(EsDev p) {
+    __shared__ double red[ES_NT / 32];
+    const int part = blockIdx.x, n = p.n;
+    const double* ip = p.ip + 6 * (size_t)part;
+    double a = 0.0;
+    for (int j = threadIdx.x; j < p.ncomp; j += ES_NT) {
+        const int k = p.comps[j].x, l = p.comps[j].y;
+        const double s = __dsqrt_rn((double)(k * k + l * l)) / ((double)n * ip[5]);
+        const double ctf = bp_ctf(ip, s);
+        const double w = p.invsig[j];
+        const double2 x = p.img[(size_t)part * n * n + (size_t)bp_store(l, n) * n + bp_store(k, n)];
+        a += w * (x.x * x.x + x.y * x.y);
+        const size_t o = (size_t)part * p.ncomp + j;
+        const double wc = w * ctf;
+        p.p1r[o] = wc * x.x;
+        p.p1i[o] = wc * x.y;
+        p.p2[o] = wc * ctf;
+        p.pab[o] = w * fabs(ctf) * hypot(x.x, x.y);
+    }
+    double v[1] = {a};
+    es_block_sum<1>(v, red);
+    if (threadIdx.x == 0) p.A[part] = v[0];
+}
+
+// pass 1 (estep.cpp:189-208): zero-shift residual R0 and the bound LB
+__global__ void __launch_bounds__(ES_NT) es_pass1_kernel(EsDev p) {
+    __shared__ double red[3 * ES_NT / 32];
+    const int part = blockIdx.x / p.npose, pose = blockIdx.x % p.npose;
+    const double* p1r = p.p1r + (size_t)part * p.ncomp;
+    const double* p1i = p.p1i + (size_t)part * p.ncomp;
+    const double* p2 = p.p2 + (size_t)part * p.ncomp;
+    const double* pa = p.pab + (size_t)part * p.ncomp;
+    const double2* S = p.slice + (size_t)pose * p.ncomp;
+    double v[3] = {0.0, 0.0, 0.0};  // b, cross, absum
+    for (int j = threadIdx.x; j < p.ncomp; j += ES_NT) {
+        const double2 s = S[j];
+        const double t1 = s.x * s.x + s.y * s.y;
+        v[0] += p2[j] * t1;
+        v[1] += p1r[j] * s.x + p1i[j] * s.y;
+        v[2] += pa[j] * sqrt(t1);
+    }
+    es_block_sum<3>(v, red);
+    if (threadIdx.x == 0) {
+        const double A = p.A[part];
+        p.R0[blockIdx.x] = A + v[0] - 2.0 * v[1];
+        p.LB[blockIdx.x] = A + v[0] - 2.0 * v[2];
+    }
+}
+
+// U: best zero-shift residual per particle (estep.cpp:210-215)
+__global__ void __launch_bounds__(ES_NT) es_min_kernel(EsDev p) {
+    __shared__ double red[ES_NT / 32];
+    const int part = blockIdx.x;
+    double m = INFINITY;
+    for (int q = threadIdx.x; q < p.npose; q += ES_NT) m = fmin(m, p.R0[(size_t)part * p.npose + q]);
+    m = es_block_min(m, red);
+    if (threadIdx.x == 0) p.U[part] = m;
+}
+
+// pass 2 (estep.cpp:217-249): every shift of each surviving (particle, pose)
+__global__ void __launch_bounds__(ES_NT) es_pass2_kernel(EsDev p) {
+    constexpr int SB = 8;
+    __shared__ double red[(SB + 1) * ES_NT / 32];
+    const int part = blockIdx.x / p.npose, pose = blockIdx.x % p.npose;
+    double* out = p.res + (size_t)part * p.npose * p.nshift + (size_t)pose * p.nshift;
+    if (p.LB[blockIdx.x] > p.U[part] + p.slack) {  // pruned pose: no candidates
+        for (int s = threadIdx.x; s < p.nshift; s += ES_NT) out[s] = INFINITY;
+        return;
+    }
+    const double* p1r = p.p1r + (size_t)part * p.ncomp;
+    const double* p1i = p.p1i + (size_t)part * p.ncomp;
+    const double* p2 = p.p2 + (size_t)part * p.ncomp;
+    const double2* S = p.slice + (size_t)pose * p.ncomp;
+    double base = 0.0;
+    for (int s0 = 0; s0 < p.nshift; s0 += SB) {
+        double v[SB + 1];
+#pragma unroll
+        for (int q = 0; q <= SB; ++q) v[q] = 0.0;
+        for (int j = threadIdx.x; j < p.ncomp; j += ES_NT) {
+            const double2 s = S[j];
+            if (s0 == 0) v[SB] += p2[j] * (s.x * s.x + s.y * s.y);
+            const double cr = p1r[j] * s.x + p1i[j] * s.y;
+            const double ci = p1i[j] * s.x - p1r[j] * s.y;
+#pragma unroll
+            for (int q = 0; q < SB; ++q)
+                if (s0 + q < p.nshift) {
+                    const size_t o = (size_t)(s0 + q) * p.ncomp + j;
+                    v[q] += cr * p.phr[o] + ci * p.phi[o];
+                }
+        }
+        es_block_sum<SB + 1>(v, red);
+        if (s0 == 0) base = p.A[part] + v[SB];
+        if (threadIdx.x == 0)
+            for (int q = 0; q < SB && s0 + q < p.nshift; ++q) out[s0 + q] = base - 2.0 * v[q];
+    }
+}
+
+// softmax, prune, renormalise (estep.cpp:251-268): dense posterior row
+__global__ void __launch_bounds__(ES_NT) es_softmax_kernel(EsDev p, double* post) {
+    __shared__ double red[ES_NT / 32];
+    const int part = blockIdx.x;
+    const int nc = p.npose * p.nshift;
+    const double* r = p.res + (size_t)part * nc;
+    double* o = post + (size_t)part * nc;
+    double m = INFINITY;
+    for (int c = threadIdx.x; c < nc; c += ES_NT) m = fmin(m, r[c]);
+    const double rmin = es_block_min(m, red);
+    double v[1] = {0.0};
+    for (int c = threadIdx.x; c < nc; c += ES_NT)
+        if (r[c] < INFINITY) v[0] += exp(-(r[c] - rmin) / 2.0);
+    es_block_sum<1>(v, red);
+    const double z = v[0];
+    double kv[1] = {0.0};
+    for (int c = threadIdx.x; c < nc; c += ES_NT) {
+        double w = 0.0;
+        if (r[c] < INFINITY) {
+            w = exp(-(r[c] - rmin) / 2.0) / z;
+            if (!(w >= p.floor_)) w = 0.0;
+        }
+        o[c] = w;
+        kv[0] += w;
+    }
+    es_block_sum<1>(kv, red);
+    const double kept = kv[0];
+    for (int c = threadIdx.x; c < nc; c += ES_NT) o[c] = o[c] / kept;
+}
+
+// Host side. V: device FourierVolume (host upload or the resident spectrum).
+inline int estep_run(int n, const cm_estep_input* in, const double* V_host, const double* V_dev,
+                     double* post_host, cudaStream_t st) {
+    if (in->n_poses <= 0 || in->n_shifts <= 0)
+        return fail(CM_ERR_INVALID_ARGUMENT, "e_step: empty orientation grid");
+    if (in->kernel_kind != 0 && in->kernel_kind != 1)
+        return fail(CM_ERR_INVALID_ARGUMENT, "e_step: unknown kernel kind");
+    if (in->kernel_kind == 0 && !(in->bandwidth > 0.0))
+        return fail(CM_ERR_INVALID_ARGUMENT, "gaussian kernel bandwidth must be positive");
+    if (in->n_images < 0 || !in->poses || !in->shifts || in->n_sigma2 < 1 || !in->sigma2 ||
+        (in->n_images > 0 && (!in->images || !in->image_params)))
+        return fail(CM_ERR_INVALID_ARGUMENT, "e_step: missing input array");
+    if (!(in->prune_floor > 0.0)) return fail(CM_ERR_INVALID_ARGUMENT, "e_step: prune_floor must be positive");
+    bool zero_shift = false;
+    for (int s = 0; s < in->n_shifts; ++s)
+        zero_shift |= in->shifts[2 * s] == 0 && in->shifts[2 * s + 1] == 0;
+    if (!zero_shift) return fail(CM_ERR_INVALID_ARGUMENT, "e_step: orientation grid lacks the zero shift");
+    if (in->n_images == 0) return CM_OK;
+    // build_comp_tables (estep.cpp:26-40) with effective_cutoff (:14-17)
+    const double nyq = double(n / 2);
+    const double cutoff = in->radius_cutoff < 0.0 ? nyq : std::min(in->radius_cutoff, nyq);
+    std::vector<int2> comps;
+    std::vector<double> invsig;
+    for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) {
+            const int k = a < n / 2 ? a : a - n, l = b < n / 2 ? b : b - n;
+            const long r = std::lround(std::hypot(double(k), double(l)));
+            if (r > std::lround(cutoff)) continue;
+            comps.push_back(make_int2(k, l));
+            invsig.push_back(1.0 / in->sigma2[std::min<long>(r, in->n_sigma2 - 1)]);
+        }
+    std::vector<double> mats(9 * (size_t)in->n_poses);
+    for (int q = 0; q < in->n_poses; ++q) bp_rotation(in->poses + 3 * (size_t)q, mats.data() + 9 * (size_t)q);
+    const int ncomp = (int)comps.size(), np = in->n_images, npose = in->n_poses, ns = in->n_shifts;
+    const size_t L = (size_t)n * n * n, nc = (size_t)npose * ns;
+
+    BpBuffers B;
+    EsDev p{};
+    double2* img = nullptr;
+    double2* Vd = nullptr;
+    double *ip = nullptr, *dm = nullptr, *isg = nullptr, *phr = nullptr, *phi = nullptr;
+    int2 *cmp = nullptr, *shf = nullptr;
+    double2* slice = nullptr;
+    double *p1r = nullptr, *p1i = nullptr, *p2 = nullptr, *pab = nullptr, *A = nullptr, *R0 = nullptr,
+           *LB = nullptr, *U = nullptr, *res = nullptr, *post = nullptr;
+    if (V_host) {
+        CKS(B.put(&Vd, reinterpret_cast<const double2*>(V_host), L, st));
+    }
+    CKS(B.put(&img, reinterpret_cast<const double2*>(in->images), (size_t)np * n * n, st));
+    CKS(B.put(&ip, in->image_params, (size_t)np * 6, st));
+    CKS(B.put(&dm, mats.data(), mats.size(), st));
+    CKS(B.put(&cmp, comps.data(), comps.size(), st));
+    CKS(B.put(&isg, invsig.data(), invsig.size(), st));
+    CKS(B.put(&shf, reinterpret_cast<const int2*>(in->shifts), (size_t)ns, st));
+    CKS(B.put(&phr, (const double*)nullptr, (size_t)ns * ncomp, st));
+    CKS(B.put(&phi, (const double*)nullptr, (size_t)ns * ncomp, st));
+    CKS(B.put(&slice, (const double2*)nullptr, (size_t)npose * ncomp, st));
+    for (double** q : {&p1r, &p1i, &p2, &pab}) CKS(B.put(q, (const double*)nullptr, (size_t)np * ncomp, st));
+    CKS(B.put(&A, (const double*)nullptr, (size_t)np, st));
+    CKS(B.put(&U, (const double*)nullptr, (size_t)np, st));
+    CKS(B.put(&R0, (const double*)nullptr, (size_t)np * npose, st));
+    CKS(B.put(&LB, (const double*)nullptr, (size_t)np * npose, st));
+    CKS(B.put(&res, (const double*)nullptr, (size_t)np * nc, st));
+    CKS(B.put(&post, (const double*)nullptr, (size_t)np * nc, st));
+    p = EsDev{V_host ? Vd : reinterpret_cast<const double2*>(V_dev), img, ip, dm, cmp, isg, phr, phi, slice,
+              p1r, p1i, p2, pab, A, R0, LB, U, res, n, ncomp, npose, ns, np,
+              2.0 * std::log(1.0 / in->prune_floor), in->prune_floor, in->bandwidth};
+    auto blocks = [](long long t) { return (unsigned)((t + ES_NT - 1) / ES_NT); };
+    if (ncomp > 0) {
+        es_phase_kernel<<<blocks((long long)ns * ncomp), ES_NT, 0, st>>>(p, shf);
+        if (in->kernel_kind == 0)
+            es_slice_kernel<0><<<blocks((long long)npose * ncomp), ES_NT, 0, st>>>(p);
+        else
+            es_slice_kernel<1><<<blocks((long long)npose * ncomp), ES_NT, 0, st>>>(p);
+    }
+    es_ptab_kernel<<<np, ES_NT, 0, st>>>(p);
+    es_pass1_kernel<<<(unsigned)((size_t)np * npose), ES_NT, 0, st>>>(p);
+    es_min_kernel<<<np, ES_NT, 0, st>>>(p);
+    es_pass2_kernel<<<(unsigned)((size_t)np * npose), ES_NT, 0, st>>>(p);
+    es_softmax_kernel<<<np, ES_NT, 0, st>>>(p, post);
+    if (cudaGetLastError() != cudaSuccess) return fail(CM_ERR_CUDA, "e_step: launch failed");
+    if (cudaMemcpyAsync(post_host, post, sizeof(double) * np * nc, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(CM_ERR_CUDA, "e_step: kernel failed");
+    return CM_OK;
+}
+
+} // namespace cm

@@ -337,6 +337,9 @@ struct ImplBase {
     // conversion to the resident W / Y (backproject.cuh writes it on the device)
     virtual double* acc_stage() = 0;
     virtual int commit_acc_stage(int finalized) = 0;
+    // fft3(_centered) of the resident result as a full fp64 grid in the staging
+    // buffer (stream-ordered; estep.cuh reads V from it), or null
+    virtual const double* result_spectrum_device(int centered) = 0;
 
     cudaStream_t stream = nullptr;
     int n = 0;
@@ -1354,6 +1357,13 @@ struct Impl final : ImplBase {
             curve[r] = den > 0.0 ? h[3 * r] / den : 0.0;  // fsc.cpp:36-39
         }
         return CM_OK;
+    }
+
+    const double* result_spectrum_device(int centered) override {
+        if (!vol_set || !result_valid) return nullptr;
+        if (result_to_spectrum() != CM_OK) return nullptr;
+        unpack_full_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(N, S, stage, centered);
+        return cudaGetLastError() == cudaSuccess ? stage : nullptr;
     }
 
     int result_spectrum(double* out, int centered) override {

@@ -269,6 +269,20 @@ class Reference(_Lib):
             int(threads), _d(w), C.c_void_p(y.ctypes.data))
         return rc, w, y
 
+    def estep(self, inp, volume, sigma2, prune_floor=1e-8, threads=1):
+        """e_step (estep.cpp:64) -> (status, dense posterior [images][candidates])."""
+        n = inp.side_n
+        V = np.ascontiguousarray(volume, np.complex128)
+        s2 = np.ascontiguousarray(sigma2, np.float64)
+        out = np.zeros((inp.images.shape[0], inp.poses.shape[0] * inp.shifts.shape[0]))
+        p = lambda a: C.c_void_p(a.ctypes.data if a.size else None)  # noqa: E731
+        rc = self.f("estep")(
+            n, inp.images.shape[0], p(inp.images), p(inp.image_params), inp.poses.shape[0],
+            p(inp.poses), inp.shifts.shape[0], p(inp.shifts), int(inp.kernel_kind),
+            C.c_double(inp.bandwidth), C.c_double(inp.radius_cutoff), s2.size, p(s2),
+            C.c_double(prune_floor), p(V), int(threads), _d(out))
+        return rc, out
+
     def write_mrc_volume(self, path, x, voxel_size=1.0):
         """write_mrc(path, Volume3D) by the reference (mrc.cpp:134)."""
         x = np.ascontiguousarray(x, np.float64)

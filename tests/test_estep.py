@@ -1,0 +1,126 @@
+"""Device E-step (cm_estep) against the unmodified reference e_step
+(estep.cpp:64-270, through oracle/_ref) on identical inputs.
+
+Bar: every posterior within 1e-10 (absolute; posteriors are in [0, 1]) and the
+same set of surviving (nonzero) candidates per particle -- the pose pruning and
+the prune_floor cut must agree. Device sums run in a different order and its
+sin/cos/exp differ from glibc by an ulp, so agreement is to roundoff.
+"""
+import numpy as np
+import pytest
+
+import paper_1905_13408_b200 as cm
+from paper_1905_13408_b200 import synth
+from paper_1905_13408_b200.backproject import GAUSSIAN, TRILINEAR
+from oracle_lib import Reference, have_reference
+
+needs_ref = pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built")
+
+
+def problem(n, m, kind, cut, scale, seed, grid=True, r=1, n_poses=12):
+    inp = synth.synthetic_backprojection(n, m, n_poses=n_poses, trans_radius=r, kernel_kind=kind,
+                                         radius_cutoff=cut, seed=seed, grid_angles=grid)
+    rng = np.random.default_rng(seed + 100)
+    V = rng.standard_normal((n, n, n)) + 1j * rng.standard_normal((n, n, n))
+    shells = np.arange(n // 2 + 1)
+    sigma2 = scale * n * (1.0 + 0.05 * shells)
+    return inp, V, sigma2
+
+
+@needs_ref
+def test_reference_wrapper_rows_normalised():
+    R = Reference()
+    inp, V, s2 = problem(8, 4, GAUSSIAN, -1.0, 1.0, 1)
+    rc, post = R.estep(inp, V, s2)
+    assert rc == 0, R.last_error()
+    np.testing.assert_allclose(post.sum(axis=1), 1.0, rtol=1e-12)
+
+
+CASES = [
+    # n, images, kernel, cutoff, sigma scale, grid angles, shift radius
+    (8, 6, GAUSSIAN, -1.0, 1.0, True, 1),
+    (8, 6, TRILINEAR, -1.0, 1.0, False, 1),
+    (16, 10, GAUSSIAN, 5.0, 0.5, True, 2),
+    (16, 10, TRILINEAR, -1.0, 2.0, True, 1),
+    (32, 8, GAUSSIAN, -1.0, 1.0, False, 2),
+    (32, 8, GAUSSIAN, 10.0, 0.05, True, 1),  # peaked: pose pruning active
+]
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("n,m,kind,cut,scale,grid,r", CASES)
+def test_matches_reference(n, m, kind, cut, scale, grid, r):
+    R = Reference()
+    inp, V, s2 = problem(n, m, kind, cut, scale, n + m, grid, r)
+    rc, want = R.estep(inp, V, s2)
+    assert rc == 0, R.last_error()
+    ctx = cm.Context(n)
+    got = cm.e_step(ctx, inp, s2, volume=V)
+    ctx.close()
+    np.testing.assert_array_equal(got != 0, want != 0)
+    assert np.abs(got - want).max() <= 1e-10
+    np.testing.assert_allclose(got.sum(axis=1), 1.0, rtol=1e-12)
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_spread_posteriors_exercise_many_candidates():
+    """The parity cases above are not degenerate one-hot rows."""
+    R = Reference()
+    inp, V, s2 = problem(16, 10, GAUSSIAN, -1.0, 2.0, 26, True, 1)
+    rc, want = R.estep(inp, V, s2)
+    assert rc == 0
+    assert (want > 0).sum(axis=1).max() > 3
+
+
+@pytest.mark.gpu
+def test_resident_volume_and_em_round():
+    """V = fft3_centered of the resident solve result (volume=None) equals
+    passing that spectrum from the host; then the posteriors feed the device
+    backprojection and the next M-step with nothing but images on the host."""
+    n = 16
+    inp, _, s2 = problem(n, 8, GAUSSIAN, -1.0, 1.0, 5)
+    p = synth.synthetic_problem(n)
+    ctx = cm.Context(n, precision=64)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 4
+    ctx.set_volumes(p.x0)
+    ctx.solve(cfg)
+    V = ctx.get_spectrum(centered=True)
+    a = cm.e_step(ctx, inp, s2, volume=V)
+    b = cm.e_step(ctx, inp, s2)
+    np.testing.assert_array_equal(a != 0, b != 0)
+    assert np.abs(a - b).max() <= 1e-12
+    ep, ec, ew = cm.posterior_entries(b)
+    inp.entry_particle, inp.entry_candidate, inp.entry_posterior = ep, ec, ew
+    cm.backproject_into(ctx, inp, download=False)
+    s2_ = ctx.scale_data()
+    assert s2_.s_n > 0
+    ctx.set_volumes(ctx.get_volume())
+    ctx.solve(cfg)
+    assert np.isfinite(ctx.get_volume()).all()
+    ctx.close()
+
+
+@pytest.mark.gpu
+def test_errors():
+    n = 8
+    ctx = cm.Context(n)
+    inp, V, s2 = problem(n, 2, GAUSSIAN, -1.0, 1.0, 3)
+    no_zero = synth.synthetic_backprojection(n, 2, seed=3)
+    no_zero.shifts = np.array([[1, 0]], np.int32)
+    with pytest.raises(cm.InvalidArgument):
+        cm.e_step(ctx, no_zero, s2, volume=V)
+    empty = synth.synthetic_backprojection(n, 2, seed=3)
+    empty.poses = np.zeros((0, 3))
+    with pytest.raises(cm.InvalidArgument):
+        cm.e_step(ctx, empty, s2, volume=V)
+    with pytest.raises(cm.Error):  # no volume and no solver result resident
+        cm.e_step(ctx, inp, s2)
+    with pytest.raises(cm.GridMismatch):
+        cm.e_step(ctx, inp, s2, volume=V[:4, :4, :4])
+    ctx.close()
