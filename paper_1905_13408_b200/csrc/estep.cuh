@@ -16,7 +16,7 @@
 // (w ctf X, w ctf^2, w |ctf| |X|) once; then one CTA per (particle, pose)
 // reduces over the components, particle-major so a particle's table and all
 // slices stay in L2 while its poses are swept. Pass 2 evaluates all shifts of
-// a surviving pose from one read of its terms, eight shifts per reduction.
+// four poses at a time from one read of the particle's terms and the phases.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -213,41 +213,68 @@ __global__ void __launch_bounds__(ES_NT) es_min_kernel(EsDev p) {
     if (threadIdx.x == 0) p.U[part] = m;
 }
 
-// pass 2 (estep.cpp:217-249): every shift of each surviving (particle, pose)
+// pass 2 (estep.cpp:217-249): every shift of each surviving (particle, pose).
+// One CTA per particle and group of ES_PG poses: the particle's terms and the
+// shift-phase tables are read once per group instead of once per pose (the
+// kernel is L2-bound on exactly those reads).
+constexpr int ES_PG = 4, ES_SB = 4;
 __global__ void __launch_bounds__(ES_NT) es_pass2_kernel(EsDev p) {
-    constexpr int SB = 8;
-    __shared__ double red[(SB + 1) * ES_NT / 32];
-    const int part = blockIdx.x / p.npose, pose = blockIdx.x % p.npose;
-    double* out = p.res + (size_t)part * p.npose * p.nshift + (size_t)pose * p.nshift;
-    if (p.LB[blockIdx.x] > p.U[part] + p.slack) {  // pruned pose: no candidates
-        for (int s = threadIdx.x; s < p.nshift; s += ES_NT) out[s] = INFINITY;
-        return;
+    constexpr int PG = ES_PG, SB = ES_SB, NV = PG * SB + PG;
+    __shared__ double red[NV * ES_NT / 32];
+    const int ngrp = (p.npose + PG - 1) / PG;
+    const int part = blockIdx.x / ngrp, pose0 = (blockIdx.x % ngrp) * PG;
+    const double U = p.U[part] + p.slack;
+    bool alive[PG];
+    bool any = false;
+#pragma unroll
+    for (int g = 0; g < PG; ++g) {
+        const int pose = pose0 + g;
+        alive[g] = pose < p.npose && !(p.LB[(size_t)part * p.npose + pose] > U);
+        any |= alive[g];
+        if (pose < p.npose && !alive[g]) {  // pruned pose: no candidates
+            double* out = p.res + ((size_t)part * p.npose + pose) * p.nshift;
+            for (int s = threadIdx.x; s < p.nshift; s += ES_NT) out[s] = INFINITY;
+        }
     }
+    if (!any) return;
     const double* p1r = p.p1r + (size_t)part * p.ncomp;
     const double* p1i = p.p1i + (size_t)part * p.ncomp;
     const double* p2 = p.p2 + (size_t)part * p.ncomp;
-    const double2* S = p.slice + (size_t)pose * p.ncomp;
-    double base = 0.0;
+    double base[PG];
     for (int s0 = 0; s0 < p.nshift; s0 += SB) {
-        double v[SB + 1];
+        double v[NV];
 #pragma unroll
-        for (int q = 0; q <= SB; ++q) v[q] = 0.0;
+        for (int q = 0; q < NV; ++q) v[q] = 0.0;
         for (int j = threadIdx.x; j < p.ncomp; j += ES_NT) {
-            const double2 s = S[j];
-            if (s0 == 0) v[SB] += p2[j] * (s.x * s.x + s.y * s.y);
-            const double cr = p1r[j] * s.x + p1i[j] * s.y;
-            const double ci = p1i[j] * s.x - p1r[j] * s.y;
+            const double ar = p1r[j], ai = p1i[j], a2 = p2[j];
+            double phr[SB], phi[SB];
 #pragma unroll
-            for (int q = 0; q < SB; ++q)
-                if (s0 + q < p.nshift) {
-                    const size_t o = (size_t)(s0 + q) * p.ncomp + j;
-                    v[q] += cr * p.phr[o] + ci * p.phi[o];
-                }
+            for (int q = 0; q < SB; ++q) {
+                const bool ok = s0 + q < p.nshift;
+                const size_t o = (size_t)(ok ? s0 + q : 0) * p.ncomp + j;
+                phr[q] = ok ? p.phr[o] : 0.0;
+                phi[q] = ok ? p.phi[o] : 0.0;
+            }
+#pragma unroll
+            for (int g = 0; g < PG; ++g) {
+                if (!alive[g]) continue;
+                const double2 sv = p.slice[(size_t)(pose0 + g) * p.ncomp + j];
+                if (s0 == 0) v[PG * SB + g] += a2 * (sv.x * sv.x + sv.y * sv.y);
+                const double cr = ar * sv.x + ai * sv.y;
+                const double ci = ai * sv.x - ar * sv.y;
+#pragma unroll
+                for (int q = 0; q < SB; ++q) v[g * SB + q] += cr * phr[q] + ci * phi[q];
+            }
         }
-        es_block_sum<SB + 1>(v, red);
-        if (s0 == 0) base = p.A[part] + v[SB];
-        if (threadIdx.x == 0)
-            for (int q = 0; q < SB && s0 + q < p.nshift; ++q) out[s0 + q] = base - 2.0 * v[q];
+        es_block_sum<NV>(v, red);
+#pragma unroll
+        for (int g = 0; g < PG; ++g) {
+            if (s0 == 0) base[g] = p.A[part] + v[PG * SB + g];
+            if (threadIdx.x == 0 && alive[g]) {
+                double* out = p.res + ((size_t)part * p.npose + pose0 + g) * p.nshift;
+                for (int q = 0; q < SB && s0 + q < p.nshift; ++q) out[s0 + q] = base[g] - 2.0 * v[g * SB + q];
+            }
+        }
     }
 }
 
@@ -359,7 +386,7 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
     es_ptab_kernel<<<np, ES_NT, 0, st>>>(p);
     es_pass1_kernel<<<(unsigned)((size_t)np * npose), ES_NT, 0, st>>>(p);
     es_min_kernel<<<np, ES_NT, 0, st>>>(p);
-    es_pass2_kernel<<<(unsigned)((size_t)np * npose), ES_NT, 0, st>>>(p);
+    es_pass2_kernel<<<(unsigned)((size_t)np * ((npose + ES_PG - 1) / ES_PG)), ES_NT, 0, st>>>(p);
     es_softmax_kernel<<<np, ES_NT, 0, st>>>(p, post);
     if (cudaGetLastError() != cudaSuccess) return fail(CM_ERR_CUDA, "e_step: launch failed");
     if (cudaMemcpyAsync(post_host, post, sizeof(double) * np * nc, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
