@@ -7,11 +7,13 @@
 // frequency components within the cutoff and the kernel window's in-grid taps,
 // followed by the Friedel average of every orbit with its conjugated mate.
 //
-// Mapping: one thread per (entry, component); the entry's rotation, shift and
-// image are per-block broadcasts, the per-component work (CTF, shift phase, the
-// rotated point and its 8 / 27 taps) is independent fp64 arithmetic, and the
-// taps land with fp64 atomics in the fp64 staging grid that commit_acc_stage
-// then converts into the solver's resident W / Y. The arithmetic that decides
+// Mapping: entries are grouped by pose on the host; bp_gather_kernel (one
+// thread per (pose, component)) sums post * CTF * Xhat and post * CTF^2 over
+// the pose's entries -- CTF, shift phase and image read per entry, no atomics
+// -- and bp_spread_kernel spreads each (pose, component) once through its 8 / 27
+// taps with fp64 atomics into the fp64 staging grid that commit_acc_stage then
+// converts into the solver's resident W / Y. (CM_BP_DIRECT=1 selects the
+// per-entry scatter, the reference's loop order, for A/B.) The arithmetic that decides
 // tap positions (the rotation and the rotated point) is written with explicit
 // rounding intrinsics in the reference's evaluation order, so a point on a
 // floor / lround boundary (15-degree grid poses put many exactly on .5) lands
@@ -24,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -66,6 +69,120 @@ __device__ __forceinline__ double bp_ctf(const double* ip, double s) {
     return -(sqrt(1.0 - a * a) * sin(chi) + a * cos(chi));
 }
 
+// The window of a rotated frequency (kernel_taps, kernel.cpp:36-78) with the
+// in-grid test of backproject.cpp:58-61: f(px, py, pz, w) per tap.
+template <int KIND, typename F>
+__device__ __forceinline__ void bp_window(const double* R, int k, int l, double bandwidth, int n, F&& f) {
+    const int lo = -n / 2, hi = n / 2 - 1;
+    double nj[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)  // the reference's as-built order (see bp_scatter_kernel)
+        nj[a] = __dadd_rn(__fma_rn(R[3 * a], (double)k, __dmul_rn(R[3 * a + 1], (double)l)),
+                          __dmul_rn(R[3 * a + 2], 0.0));
+    auto tap = [&](int px, int py, int pz, double w) {
+        if (px < lo || px > hi || py < lo || py > hi || pz < lo || pz > hi) return;
+        f(((size_t)bp_store(pz, n) * n + bp_store(py, n)) * n + bp_store(px, n), w);
+    };
+    if constexpr (KIND == 0) {
+        int anc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) anc[a] = (int)llround(nj[a]);
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int q[3] = {anc[0] + dx, anc[1] + dy, anc[2] + dz};
+                    double d2 = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const double d = __dsub_rn(nj[a], (double)q[a]);
+                        d2 = __dadd_rn(d2, __dmul_rn(d, d));
+                    }
+                    tap(q[0], q[1], q[2], exp(-d2 / bandwidth));
+                }
+    } else {
+        int lo3[3];
+        double fr[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo3[a] = (int)floor(nj[a]);
+            fr[a] = __dsub_rn(nj[a], (double)lo3[a]);
+        }
+        const int cz1 = fr[2] == 0.0 ? 0 : 1, cy1 = fr[1] == 0.0 ? 0 : 1, cx1 = fr[0] == 0.0 ? 0 : 1;
+        for (int cz = 0; cz <= cz1; ++cz)
+            for (int cy = 0; cy <= cy1; ++cy)
+                for (int cx = 0; cx <= cx1; ++cx) {
+                    const double wx = cx ? fr[0] : 1.0 - fr[0];
+                    const double wy = cy ? fr[1] : 1.0 - fr[1];
+                    const double wz = cz ? fr[2] : 1.0 - fr[2];
+                    tap(lo3[0] + cx, lo3[1] + cy, lo3[2] + cz, __dmul_rn(__dmul_rn(wx, wy), wz));
+                }
+    }
+}
+
+// Pose-grouped form (the default). Every entry of one pose spreads its
+// components through the same windows, so the per-entry sums
+//   Z(pose, j) = sum_e post_e ctf_e(j) Xhat_e(j),  Wt(pose, j) = sum_e post_e ctf_e(j)^2
+// are formed first (a gather, no atomics), and only (pose, component) pairs are
+// spread: tap w adds w Z and w Wt. Fewer REDs by the entries-per-pose factor;
+// the sums associate differently from the reference's per-entry adds (1e-16
+// relative per term).
+struct BpGroup {
+    const int* pose_of;     // [nused] pose index of each used pose
+    const int* off;         // [nused + 1] into ent
+    const int* ent;         // entry ids grouped by pose
+    double2* Z;             // [batch][ncomp]
+    double* Wt;
+};
+
+__global__ void __launch_bounds__(128) bp_gather_kernel(BpDev p, BpGroup g, int u0) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int u = u0 + blockIdx.y;
+    if (j >= p.ncomp) return;
+    const int n = p.n;
+    const int k = p.comps[j].x, l = p.comps[j].y;
+    const double r = __dsqrt_rn((double)(k * k + l * l));
+    const size_t pix = (size_t)bp_store(l, n) * n + bp_store(k, n);
+    double zr = 0.0, zi = 0.0, wt = 0.0;
+    for (int q = g.off[u]; q < g.off[u + 1]; ++q) {
+        const int e = g.ent[q];
+        const double post = p.epost[e];
+        const int2 sh = p.shifts[p.ecand[e] % (unsigned)p.n_shifts];
+        const long long part = p.epart[e];
+        const double* ip = p.iparams + 6 * part;
+        const double ctf = bp_ctf(ip, r / ((double)n * ip[5]));
+        const double2 f = p.img[(size_t)part * n * n + pix];
+        const double ph = -2.0 * 3.14159265358979323846 * ((double)k * sh.x + (double)l * sh.y) / (double)n;
+        double sp, cp;
+        sincos(ph, &sp, &cp);
+        const double xr = f.x * cp - f.y * (-sp), xi = f.x * (-sp) + f.y * cp;
+        const double pc = post * ctf;
+        zr += pc * xr;
+        zi += pc * xi;
+        wt += pc * ctf;
+    }
+    const size_t o = (size_t)blockIdx.y * p.ncomp + j;
+    g.Z[o] = make_double2(zr, zi);
+    g.Wt[o] = wt;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(128) bp_spread_kernel(BpDev p, BpGroup g, int u0) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= p.ncomp) return;
+    const size_t o = (size_t)blockIdx.y * p.ncomp + j;
+    const double2 z = g.Z[o];
+    const double wt = g.Wt[o];
+    if (z.x == 0.0 && z.y == 0.0 && wt == 0.0) return;
+    const double* R = p.mats + 9 * (size_t)g.pose_of[u0 + blockIdx.y];
+    bp_window<KIND>(R, p.comps[j].x, p.comps[j].y, p.bandwidth, p.n, [&](size_t vi, double w) {
+        atomicAdd(&p.num[vi].x, w * z.x);
+        atomicAdd(&p.num[vi].y, w * z.y);
+        atomicAdd(&p.weight[vi], w * wt);
+    });
+}
+
+// Per-entry form (CM_BP_DIRECT=1; the reference's loop order, one RED triple per tap and entry)
 template <int KIND>  // 0 gaussian (27 taps), 1 trilinear (<= 8 taps)
 __global__ void __launch_bounds__(128) bp_scatter_kernel(BpDev p, long long nblocks_total, int cblocks) {
     const int n = p.n, lo = -n / 2, hi = n / 2 - 1;
@@ -277,7 +394,48 @@ inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStre
         CKS(bufs.put(&post, in->entry_posterior, (size_t)in->n_entries, st));
         p = BpDev{img, ipar, dm, shf, cmp, ep, ec, post, stage, reinterpret_cast<double2*>(stage + L),
                   in->n_entries, (int)comps.size(), n, in->n_shifts, in->bandwidth};
-        if (!comps.empty()) {
+        const char* direct = getenv("CM_BP_DIRECT");
+        if (!comps.empty() && !(direct && direct[0] == '1')) {
+            // group the nonzero entries by pose (stable: row order within a pose)
+            std::vector<int> cnt(in->n_poses + 1, 0);
+            for (long long e = 0; e < in->n_entries; ++e)
+                if (in->entry_posterior[e] > 0.0) ++cnt[in->entry_candidate[e] / (unsigned)in->n_shifts];
+            std::vector<int> pose_of, off{0};
+            std::vector<int> slot(in->n_poses, -1);
+            for (int q = 0; q < in->n_poses; ++q)
+                if (cnt[q] > 0) {
+                    slot[q] = (int)pose_of.size();
+                    pose_of.push_back(q);
+                    off.push_back(off.back() + cnt[q]);
+                }
+            std::vector<int> ent(off.back()), fill(off.begin(), off.end() - 1);
+            for (long long e = 0; e < in->n_entries; ++e)
+                if (in->entry_posterior[e] > 0.0)
+                    ent[fill[slot[in->entry_candidate[e] / (unsigned)in->n_shifts]]++] = (int)e;
+            const int nused = (int)pose_of.size();
+            const int ncomp = (int)comps.size();
+            // pose batches bounded to ~1 GB of (Z, Wt)
+            const int batch = (int)std::max<size_t>(1, std::min<size_t>(std::min<size_t>((size_t)nused, (size_t)65535), (size_t(1) << 30) / (24 * (size_t)ncomp)));
+            BpGroup g{};
+            int *d_pose = nullptr, *d_off = nullptr, *d_ent = nullptr;
+            double2* Z = nullptr;
+            double* Wt = nullptr;
+            CKS(bufs.put(&d_pose, pose_of.data(), pose_of.size(), st));
+            CKS(bufs.put(&d_off, off.data(), off.size(), st));
+            CKS(bufs.put(&d_ent, ent.data(), ent.size(), st));
+            CKS(bufs.put(&Z, (const double2*)nullptr, (size_t)batch * ncomp, st));
+            CKS(bufs.put(&Wt, (const double*)nullptr, (size_t)batch * ncomp, st));
+            g = BpGroup{d_pose, d_off, d_ent, Z, Wt};
+            for (int u0 = 0; u0 < nused; u0 += batch) {
+                const dim3 grid((ncomp + 127) / 128, std::min(batch, nused - u0));
+                bp_gather_kernel<<<grid, 128, 0, st>>>(p, g, u0);
+                if (in->kernel_kind == 0)
+                    bp_spread_kernel<0><<<grid, 128, 0, st>>>(p, g, u0);
+                else
+                    bp_spread_kernel<1><<<grid, 128, 0, st>>>(p, g, u0);
+                if (cudaGetLastError() != cudaSuccess) return fail(CM_ERR_CUDA, "backproject: launch failed");
+            }
+        } else if (!comps.empty()) {
             const int cblocks = ((int)comps.size() + 127) / 128;
             const long long total = in->n_entries * cblocks;
             int sms = 148, dev = 0;
