@@ -193,6 +193,12 @@ typedef struct {
 } cm_estep_input;
 int cm_estep(cm_ctx* ctx, const cm_estep_input* in, double* posterior);
 
+/* Particle images resident on the device across EM iterations: after
+ * cm_set_particles, a cm_bp_input / cm_estep_input with images == NULL (and
+ * image_params == NULL) and the same n_images reads the resident set, so an
+ * EM iteration moves no image data. Replaces any previous set. */
+int cm_set_particles(cm_ctx* ctx, int n_images, const double* images, const double* image_params);
+
 /* Diagnostics: when on, cm_solve launches every kernel individually between
  * CUDA events on the context stream (no graph) and accumulates per-kernel
  * device time, ms7 = {z pass (tile + column-0 kernels), y inverse, x C2R,

@@ -75,24 +75,35 @@ class BackprojectInput:
     def side_n(self) -> int:
         return int(self.images.shape[-1])
 
-    def to_c(self) -> cm_bp_input:
+    def to_c(self, resident_images: bool = False) -> cm_bp_input:
         d = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+        img = None if resident_images else d(self.images)
+        par = None if resident_images else d(self.image_params)
         return cm_bp_input(
-            int(self.images.shape[0]), d(self.images), d(self.image_params),
+            int(self.images.shape[0]), img, par,
             int(self.poses.shape[0]), d(self.poses), int(self.shifts.shape[0]), d(self.shifts),
             int(self.entry_posterior.size), d(self.entry_particle), d(self.entry_candidate),
             d(self.entry_posterior), int(self.kernel_kind), float(self.bandwidth),
             float(self.radius_cutoff))
 
 
-def backproject_into(ctx: Context, inp: BackprojectInput, download: bool = True):
+def set_particles(ctx: Context, inp: BackprojectInput) -> None:
+    """Upload the particle images once (cm_set_particles); later calls with
+    resident_images=True read them on the device."""
+    d = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+    _check(ctx.lib.cm_set_particles(ctx.ptr, int(inp.images.shape[0]), d(inp.images),
+                                    d(inp.image_params)))
+
+
+def backproject_into(ctx: Context, inp: BackprojectInput, download: bool = True,
+                     resident_images: bool = False):
     """Accumulate on the device into ctx's resident accumulator (finalized);
     returns the AccumulatorPair copy when `download`."""
     n = ctx.n
     if inp.side_n != n:
         from .regularizer import GridMismatch
         raise GridMismatch(f"backproject: images of side {inp.side_n}, context side {n}")
-    c = inp.to_c()
+    c = inp.to_c(resident_images)
     w = np.empty((n, n, n), np.float64) if download else None
     y = np.empty((n, n, n), np.complex128) if download else None
     _check(ctx.lib.cm_backproject(ctx.ptr, C.byref(c), None if w is None else w.ctypes.data,
@@ -132,7 +143,7 @@ class cm_estep_input(C.Structure):
 
 
 def e_step(ctx: Context, inp: BackprojectInput, sigma2, volume=None,
-           prune_floor: float = 1e-8) -> np.ndarray:
+           prune_floor: float = 1e-8, resident_images: bool = False) -> np.ndarray:
     """e_step (estep.hpp:44-54) on the device -> dense posterior
     [images][poses * shifts] (PosteriorRow entries at their candidate index,
     exact zeros elsewhere). The particles, grid and kernel come from `inp`
@@ -148,7 +159,9 @@ def e_step(ctx: Context, inp: BackprojectInput, sigma2, volume=None,
         from .regularizer import GridMismatch
         raise GridMismatch("e_step: volume side differs from the context")
     d = lambda a: a.ctypes.data if a is not None and a.size else None  # noqa: E731
-    c = cm_estep_input(int(inp.images.shape[0]), d(inp.images), d(inp.image_params),
+    img = None if resident_images else d(inp.images)
+    par = None if resident_images else d(inp.image_params)
+    c = cm_estep_input(int(inp.images.shape[0]), img, par,
                        int(inp.poses.shape[0]), d(inp.poses), int(inp.shifts.shape[0]),
                        d(inp.shifts), int(inp.kernel_kind), float(inp.bandwidth),
                        float(inp.radius_cutoff), int(s2.size), d(s2), float(prune_floor), d(V))

@@ -317,6 +317,52 @@ inline void bp_rotation(const double* ang, double* out) {
     std::memcpy(out, r, sizeof r);
 }
 
+// Particle images resident on the device across EM iterations (cm_set_particles):
+// the E-step and the backprojection of every iteration read them in place.
+struct ParticleDev {
+    double2* img = nullptr;  // [n_images][n*n]
+    double* ip = nullptr;    // [n_images][6]
+    int n_images = 0;
+    ~ParticleDev() { release(); }
+    void release() {
+        if (img) cudaFree(img);
+        if (ip) cudaFree(ip);
+        img = nullptr;
+        ip = nullptr;
+        n_images = 0;
+    }
+    int set(int n, int m, const double* images, const double* params, cudaStream_t st) {
+        release();
+        if (m < 0 || (m > 0 && (!images || !params)))
+            return fail(CM_ERR_INVALID_ARGUMENT, "set_particles: missing images");
+        if (m == 0) return CM_OK;
+        const size_t ni = (size_t)m * n * n;
+        if (cudaMalloc(&img, sizeof(double2) * ni) != cudaSuccess ||
+            cudaMalloc(&ip, sizeof(double) * 6 * (size_t)m) != cudaSuccess) {
+            release();
+            return fail(CM_ERR_CUDA, "set_particles: device allocation failed");
+        }
+        if (cudaMemcpyAsync(img, images, sizeof(double2) * ni, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(ip, params, sizeof(double) * 6 * (size_t)m, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            release();
+            return fail(CM_ERR_CUDA, "set_particles: upload failed");
+        }
+        n_images = m;
+        return CM_OK;
+    }
+};
+
+// images == NULL in a call selects the resident set, which must hold as many images
+inline int particles_of(int n_images, const double* images, const double* params, const ParticleDev* res,
+                        bool* host) {
+    *host = images != nullptr;
+    if (images) return params ? CM_OK : fail(CM_ERR_INVALID_ARGUMENT, "image_params missing");
+    if (!res || res->n_images == 0) return fail(CM_ERR_STATE, "no images given and none resident (cm_set_particles)");
+    if (res->n_images != n_images) return fail(CM_ERR_INVALID_ARGUMENT, "n_images differs from the resident particle set");
+    return CM_OK;
+}
+
 // Device allocations of one call, released on every exit path.
 struct BpBuffers {
     std::vector<void*> ptrs;
@@ -340,7 +386,8 @@ struct BpBuffers {
 
 // Host side: validation, the component list and rotations, launch, finalize.
 // `stage` = [weight L | numerator L complex] on the device (ImplBase::acc_stage).
-inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStream_t st) {
+inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStream_t st,
+                           const ParticleDev* resident = nullptr) {
     if (!in) return fail(CM_ERR_INVALID_ARGUMENT, "backproject: null input");
     if (in->kernel_kind != 0 && in->kernel_kind != 1)
         return fail(CM_ERR_INVALID_ARGUMENT, "backproject: unknown kernel kind");
@@ -349,9 +396,10 @@ inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStre
     if (in->n_images < 0 || in->n_poses < 0 || in->n_shifts < 0 || in->n_entries < 0)
         return fail(CM_ERR_INVALID_ARGUMENT, "backproject: negative count");
     if (in->n_entries > 0 && (!in->entry_particle || !in->entry_candidate || !in->entry_posterior ||
-                              !in->images || !in->image_params || !in->poses || !in->shifts ||
-                              in->n_shifts == 0))
+                              !in->poses || !in->shifts || in->n_shifts == 0))
         return fail(CM_ERR_INVALID_ARGUMENT, "backproject: null input array");
+    bool host_images = true;
+    if (in->n_entries > 0) CKS(particles_of(in->n_images, in->images, in->image_params, resident, &host_images));
     const unsigned long long ncand = (unsigned long long)in->n_poses * (unsigned long long)in->n_shifts;
     for (long long e = 0; e < in->n_entries; ++e) {
         if (in->entry_particle[e] < 0 || in->entry_particle[e] >= in->n_images)
@@ -384,8 +432,13 @@ inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStre
     long long* ep = nullptr;
     unsigned* ec = nullptr;
     if (in->n_entries > 0) {
-        CKS(bufs.put(&img, reinterpret_cast<const double2*>(in->images), (size_t)in->n_images * n * n, st));
-        CKS(bufs.put(&ipar, in->image_params, (size_t)in->n_images * 6, st));
+        if (host_images) {
+            CKS(bufs.put(&img, reinterpret_cast<const double2*>(in->images), (size_t)in->n_images * n * n, st));
+            CKS(bufs.put(&ipar, in->image_params, (size_t)in->n_images * 6, st));
+        } else {
+            img = resident->img;
+            ipar = resident->ip;
+        }
         CKS(bufs.put(&dm, mats.data(), mats.size(), st));
         CKS(bufs.put(&shf, reinterpret_cast<const int2*>(in->shifts), (size_t)in->n_shifts, st));
         CKS(bufs.put(&cmp, comps.data(), comps.size(), st));

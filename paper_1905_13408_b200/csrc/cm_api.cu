@@ -59,6 +59,7 @@ struct cm_ctx {
     int precision = 32;
     int device = 0;
     std::unique_ptr<MrcRing> mrc;  // pinned MRC staging, on first use
+    ParticleDev particles;         // resident particle images (cm_set_particles)
 };
 
 #define CTX_GUARD(ctx)                                                         \
@@ -254,7 +255,7 @@ int cm_backproject(cm_ctx* ctx, const cm_bp_input* in, double* weight_out, doubl
     ImplBase* im = ctx->impl.get();
     double* stage = im->acc_stage();
     im->acc_set = false;  // the staging grid is about to be overwritten
-    CKS(backproject_run(ctx->n, in, stage, im->stream));
+    CKS(backproject_run(ctx->n, in, stage, im->stream, &ctx->particles));
     const size_t L = (size_t)ctx->n * ctx->n * ctx->n;
     if (weight_out &&
         cudaMemcpyAsync(weight_out, stage, sizeof(double) * L, cudaMemcpyDeviceToHost, im->stream) != cudaSuccess)
@@ -273,7 +274,12 @@ int cm_estep(cm_ctx* ctx, const cm_estep_input* in, double* posterior) {
         vdev = ctx->impl->result_spectrum_device(1);
         if (!vdev) return fail(CM_ERR_STATE, "e_step: no volume given and no solver result resident");
     }
-    return estep_run(ctx->n, in, in->volume, vdev, posterior, ctx->impl->stream);
+    return estep_run(ctx->n, in, in->volume, vdev, posterior, ctx->impl->stream, &ctx->particles);
+}
+
+int cm_set_particles(cm_ctx* ctx, int n_images, const double* images, const double* image_params) {
+    CTX_GUARD(ctx);
+    return ctx->particles.set(ctx->n, n_images, images, image_params, ctx->impl->stream);
 }
 
 int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap) {

@@ -310,16 +310,17 @@ __global__ void __launch_bounds__(ES_NT) es_softmax_kernel(EsDev p, double* post
 
 // Host side. V: device FourierVolume (host upload or the resident spectrum).
 inline int estep_run(int n, const cm_estep_input* in, const double* V_host, const double* V_dev,
-                     double* post_host, cudaStream_t st) {
+                     double* post_host, cudaStream_t st, const ParticleDev* resident = nullptr) {
     if (in->n_poses <= 0 || in->n_shifts <= 0)
         return fail(CM_ERR_INVALID_ARGUMENT, "e_step: empty orientation grid");
     if (in->kernel_kind != 0 && in->kernel_kind != 1)
         return fail(CM_ERR_INVALID_ARGUMENT, "e_step: unknown kernel kind");
     if (in->kernel_kind == 0 && !(in->bandwidth > 0.0))
         return fail(CM_ERR_INVALID_ARGUMENT, "gaussian kernel bandwidth must be positive");
-    if (in->n_images < 0 || !in->poses || !in->shifts || in->n_sigma2 < 1 || !in->sigma2 ||
-        (in->n_images > 0 && (!in->images || !in->image_params)))
+    if (in->n_images < 0 || !in->poses || !in->shifts || in->n_sigma2 < 1 || !in->sigma2)
         return fail(CM_ERR_INVALID_ARGUMENT, "e_step: missing input array");
+    bool host_images = true;
+    if (in->n_images > 0) CKS(particles_of(in->n_images, in->images, in->image_params, resident, &host_images));
     if (!(in->prune_floor > 0.0)) return fail(CM_ERR_INVALID_ARGUMENT, "e_step: prune_floor must be positive");
     bool zero_shift = false;
     for (int s = 0; s < in->n_shifts; ++s)
@@ -356,8 +357,13 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
     if (V_host) {
         CKS(B.put(&Vd, reinterpret_cast<const double2*>(V_host), L, st));
     }
-    CKS(B.put(&img, reinterpret_cast<const double2*>(in->images), (size_t)np * n * n, st));
-    CKS(B.put(&ip, in->image_params, (size_t)np * 6, st));
+    if (host_images) {
+        CKS(B.put(&img, reinterpret_cast<const double2*>(in->images), (size_t)np * n * n, st));
+        CKS(B.put(&ip, in->image_params, (size_t)np * 6, st));
+    } else {
+        img = resident->img;
+        ip = resident->ip;
+    }
     CKS(B.put(&dm, mats.data(), mats.size(), st));
     CKS(B.put(&cmp, comps.data(), comps.size(), st));
     CKS(B.put(&isg, invsig.data(), invsig.size(), st));

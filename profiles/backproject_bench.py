@@ -33,7 +33,16 @@ for _ in range(5):
     cm.backproject_into(ctx, inp, download=False)
     ts.append(time.perf_counter() - t)
 dev = min(ts)
-res = {"n": n, "images": m, "kernel": ["gaussian", "trilinear"][kind],
+cm.set_particles(ctx, inp)
+ts = []
+for _ in range(5):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    cm.backproject_into(ctx, inp, download=False, resident_images=True)
+    ts.append(time.perf_counter() - t)
+dev_res = min(ts)
+res = {"device_s_resident_images": dev_res, "device_pairs_per_s_resident_images": work / dev_res,
+       "n": n, "images": m, "kernel": ["gaussian", "trilinear"][kind],
        "entries_nonzero": int((inp.entry_posterior > 0).sum()), "components": ncomp,
        "device_s_incl_upload_and_commit": dev, "device_pairs_per_s": work / dev}
 # reference on a bounded sample (first ms images), all host threads

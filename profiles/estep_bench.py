@@ -42,7 +42,16 @@ for _ in range(3):
     post = cm.e_step(ctx, inp, s2, volume=V)
     ts.append(time.perf_counter() - t)
 dev = min(ts)
-res = {"n": n, "images": m, "poses": npose, "shifts": int(inp.shifts.shape[0]),
+cm.set_particles(ctx, inp)
+ts = []
+for _ in range(3):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    cm.e_step(ctx, inp, s2, volume=V, resident_images=True)
+    ts.append(time.perf_counter() - t)
+dev_res = min(ts)
+res = {"device_s_resident_images": dev_res, "device_pairs_per_s_resident_images": m * npose / dev_res,
+       "n": n, "images": m, "poses": npose, "shifts": int(inp.shifts.shape[0]),
        "device_s_incl_transfers": dev, "device_pairs_per_s": m * npose / dev,
        "mean_entries_per_row": float((post > 0).sum(axis=1).mean())}
 ms = int(os.environ.get("REF_IMAGES", "64"))

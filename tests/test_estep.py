@@ -124,3 +124,27 @@ def test_errors():
     with pytest.raises(cm.GridMismatch):
         cm.e_step(ctx, inp, s2, volume=V[:4, :4, :4])
     ctx.close()
+
+
+@pytest.mark.gpu
+def test_resident_particles():
+    """cm_set_particles once, then E-step and backprojection with images=NULL:
+    the same posteriors (bitwise: the E-step has no atomics) and accumulator."""
+    n = 16
+    inp, V, s2 = problem(n, 8, GAUSSIAN, -1.0, 1.0, 8)
+    ctx = cm.Context(n)
+    with pytest.raises(cm.Error):  # nothing resident yet
+        cm.e_step(ctx, inp, s2, volume=V, resident_images=True)
+    cm.set_particles(ctx, inp)
+    a = cm.e_step(ctx, inp, s2, volume=V)
+    b = cm.e_step(ctx, inp, s2, volume=V, resident_images=True)
+    np.testing.assert_array_equal(a, b)
+    inp.entry_particle, inp.entry_candidate, inp.entry_posterior = cm.posterior_entries(b)
+    x = cm.backproject_into(ctx, inp)
+    y = cm.backproject_into(ctx, inp, resident_images=True)
+    assert np.abs(x.numerator - y.numerator).max() <= 1e-13 * np.abs(x.numerator).max()
+    assert np.abs(x.weight - y.weight).max() <= 1e-13 * x.weight.max()
+    fewer = synth.synthetic_backprojection(n, 3, seed=1)
+    with pytest.raises(cm.InvalidArgument):  # count differs from the resident set
+        cm.e_step(ctx, fewer, s2, volume=V, resident_images=True)
+    ctx.close()
