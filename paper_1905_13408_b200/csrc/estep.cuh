@@ -16,7 +16,7 @@
 // (w ctf X, w ctf^2, w |ctf| |X|) once; then one CTA per (particle, pose)
 // reduces over the components, particle-major so a particle's table and all
 // slices stay in L2 while its poses are swept. Pass 2 evaluates all shifts of
-// four poses at a time from one read of the particle's terms and the phases.
+// two poses at a time from one read of the particle's terms and the phases.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(ES_NT) es_min_kernel(EsDev p) {
 
 // pass 2 (estep.cpp:217-249): every shift of each surviving (particle, pose).
 // One CTA per particle and group of ES_PG poses: the particle's terms and the
-// shift-phase tables are read once per group instead of once per pose (the
-// kernel is L2-bound on exactly those reads).
-constexpr int ES_PG = 4, ES_SB = 4;
-__global__ void __launch_bounds__(ES_NT) es_pass2_kernel(EsDev p) {
+// shift-phase tables are read once per group instead of once per pose; PG = 2,
+// SB = 4 keeps it at 2 CTAs / SM without spills (PG = 4 needs 250 registers).
+constexpr int ES_PG = 2, ES_SB = 4;
+__global__ void __launch_bounds__(ES_NT, 2) es_pass2_kernel(EsDev p) {
     constexpr int PG = ES_PG, SB = ES_SB, NV = PG * SB + PG;
     __shared__ double red[NV * ES_NT / 32];
     const int ngrp = (p.npose + PG - 1) / PG;
