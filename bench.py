@@ -629,6 +629,10 @@ def run_ours(args):
                       "the host) and the FSC of two resident results; the reference does both "
                       "on the host (full-grid FFTW transforms + shell loop, refine.cpp:182,194)"}
         del V, ctx2
+        try:
+            em["iteration_128"] = em_iteration(local)
+        except Exception as e:  # reported, never fatal to the headline line
+            em["iteration_128"] = {"error": str(e)[:200]}
 
     big = None
     if args.big_n:
@@ -667,6 +671,54 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def em_iteration(device: int = 0, n: int = 128, m: int = 1000, n_poses: int = 200,
+                 iters: int = 50, rounds: int = 3) -> dict:
+    """One device-resident EM iteration of em_refine (refine.cpp:150-183) on a
+    synthetic particle set: M-step (the solver) -> E-step with V from the
+    resident result -> backprojection into the resident accumulator, images
+    uploaded once (cm_set_particles). Per-stage seconds (host clock around
+    synchronised calls; the posterior matrix crosses to the host and back as
+    entry lists, everything else stays on the device)."""
+    import torch
+
+    import paper_1905_13408_b200 as cm
+    from paper_1905_13408_b200 import synth
+    inp = synth.synthetic_backprojection(n, m, n_poses=n_poses, trans_radius=2,
+                                         entries_per_image=3, seed=11)
+    sigma2 = np.ones(n // 2 + 1)  # the data's per-shell |X|^2 / 2 (init_noise_from_data)
+    ctx = cm.Context(n, 32, device=device)
+    cm.set_particles(ctx, inp)
+    cm.backproject_into(ctx, inp, download=False, resident_images=True)
+    s = ctx.scale_data()
+    cfg = cm.derive_config(s.s_y, s.s_n, 1e-3, 1e-3)
+    cfg.inner_iters = iters
+    x = np.zeros((n, n, n))
+    ctx.set_volumes(x)
+    out = {"n": n, "particles": m, "poses": n_poses, "shifts": int(inp.shifts.shape[0]),
+           "m_step_iters": iters, "rounds": []}
+    for _ in range(rounds):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.solve(cfg)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        post = cm.e_step(ctx, inp, sigma2, resident_images=True)
+        t2 = time.perf_counter()
+        inp.entry_particle, inp.entry_candidate, inp.entry_posterior = cm.posterior_entries(post)
+        cm.backproject_into(ctx, inp, download=False, resident_images=True)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        ctx.set_volumes(ctx.get_volume())  # the next M-step starts from this one's result
+        out["rounds"].append({"m_step_s": t1 - t0, "e_step_s": t2 - t1, "backproject_s": t3 - t2,
+                              "entries": int(inp.entry_posterior.size)})
+    ctx.close()
+    best = min(out["rounds"], key=lambda r: r["m_step_s"] + r["e_step_s"] + r["backproject_s"])
+    out["iteration_s"] = best["m_step_s"] + best["e_step_s"] + best["backproject_s"]
+    out["note"] = ("device-resident EM iteration; reference per-stage CPU rates on the same "
+                   "shapes are in profiles/r1_estep_128.json and r1_backproject_128.json")
+    return out
 
 
 def main():
