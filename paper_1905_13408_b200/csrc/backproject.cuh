@@ -133,8 +133,28 @@ struct BpGroup {
     const int* ent;         // entry ids grouped by pose
     double2* Z;             // [batch][ncomp]
     double* Wt;
+    const double2* ph;      // [n_shifts][ncomp] shift phases (slice.cpp:47-50)
 };
 
+// shift phase table: the per-entry sincos of the gather, evaluated once per
+// (shift, component) with the same expression
+__global__ void bp_phase_kernel(int n, int ncomp, int nshift, const int2* comps, const int2* shifts,
+                                double2* ph) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)nshift * ncomp) return;
+    const int s = (int)(t / ncomp), j = (int)(t % ncomp);
+    const int k = comps[j].x, l = comps[j].y;
+    const double a = -2.0 * 3.14159265358979323846 * ((double)k * shifts[s].x + (double)l * shifts[s].y) / (double)n;
+    double sp, cp;
+    sincos(a, &sp, &cp);
+    ph[t] = make_double2(cp, sp);
+}
+
+// Entries of a pose arrive in PosteriorRow order (particle-major), so the runs
+// of one particle share its CTF and image sample: per run
+//   Z += ctf X conj(sum_s post_s ph_s),  Wt += ctf^2 sum_s post_s
+// with the phase from the table -- one CTF and one image read per
+// (pose, particle, component) instead of per entry.
 __global__ void __launch_bounds__(128) bp_gather_kernel(BpDev p, BpGroup g, int u0) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int u = u0 + blockIdx.y;
@@ -144,22 +164,27 @@ __global__ void __launch_bounds__(128) bp_gather_kernel(BpDev p, BpGroup g, int 
     const double r = __dsqrt_rn((double)(k * k + l * l));
     const size_t pix = (size_t)bp_store(l, n) * n + bp_store(k, n);
     double zr = 0.0, zi = 0.0, wt = 0.0;
-    for (int q = g.off[u]; q < g.off[u + 1]; ++q) {
-        const int e = g.ent[q];
-        const double post = p.epost[e];
-        const int2 sh = p.shifts[p.ecand[e] % (unsigned)p.n_shifts];
-        const long long part = p.epart[e];
+    const int qe = g.off[u + 1];
+    int q = g.off[u];
+    while (q < qe) {
+        const long long part = p.epart[g.ent[q]];
+        double sr = 0.0, si = 0.0, sw = 0.0;  // sum over the particle's run of post ph, post
+        for (; q < qe; ++q) {
+            const int e = g.ent[q];
+            if (p.epart[e] != part) break;
+            const double post = p.epost[e];
+            const double2 ph = g.ph[(size_t)(p.ecand[e] % (unsigned)p.n_shifts) * p.ncomp + j];
+            sr = fma(post, ph.x, sr);
+            si = fma(post, ph.y, si);
+            sw += post;
+        }
         const double* ip = p.iparams + 6 * part;
         const double ctf = bp_ctf(ip, r / ((double)n * ip[5]));
         const double2 f = p.img[(size_t)part * n * n + pix];
-        const double ph = -2.0 * 3.14159265358979323846 * ((double)k * sh.x + (double)l * sh.y) / (double)n;
-        double sp, cp;
-        sincos(ph, &sp, &cp);
-        const double xr = f.x * cp - f.y * (-sp), xi = f.x * (-sp) + f.y * cp;
-        const double pc = post * ctf;
-        zr += pc * xr;
-        zi += pc * xi;
-        wt += pc * ctf;
+        // X conj(e^{i ph}) summed: the shift moves the image by -shift (slice.cpp:47-50)
+        zr += ctf * (f.x * sr + f.y * si);
+        zi += ctf * (f.y * sr - f.x * si);
+        wt += ctf * ctf * sw;
     }
     const size_t o = (size_t)blockIdx.y * p.ncomp + j;
     g.Z[o] = make_double2(zr, zi);
@@ -478,7 +503,11 @@ inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStre
             CKS(bufs.put(&d_ent, ent.data(), ent.size(), st));
             CKS(bufs.put(&Z, (const double2*)nullptr, (size_t)batch * ncomp, st));
             CKS(bufs.put(&Wt, (const double*)nullptr, (size_t)batch * ncomp, st));
-            g = BpGroup{d_pose, d_off, d_ent, Z, Wt};
+            double2* ph = nullptr;
+            const long long nph = (long long)in->n_shifts * ncomp;
+            CKS(bufs.put(&ph, (const double2*)nullptr, (size_t)nph, st));
+            bp_phase_kernel<<<(unsigned)((nph + 255) / 256), 256, 0, st>>>(n, ncomp, in->n_shifts, cmp, shf, ph);
+            g = BpGroup{d_pose, d_off, d_ent, Z, Wt, ph};
             for (int u0 = 0; u0 < nused; u0 += batch) {
                 const dim3 grid((ncomp + 127) / 128, std::min(batch, nused - u0));
                 bp_gather_kernel<<<grid, 128, 0, st>>>(p, g, u0);
