@@ -129,24 +129,23 @@ __device__ __forceinline__ void bp_window(const double* R, int k, int l, double 
 // relative per term).
 struct BpGroup {
     const int* pose_of;     // [nused] pose index of each used pose
-    const int* off;         // [nused + 1] into ent
-    const int* ent;         // entry ids grouped by pose
+    const int* off;         // [nused + 1] into the grouped entries
     double2* Z;             // [batch][ncomp]
     double* Wt;
-    const double2* ph;      // [n_shifts][ncomp] shift phases (slice.cpp:47-50)
+    const double2* ph;      // [n] roots e^{-2 pi i t / n}: the shift phase of (k, l, s) is
+                            // ph[(k sx + l sy) mod n] (slice.cpp:47-50, reduced exactly)
+    const int* gpart;       // per grouped entry: particle, shift, posterior
+    const int2* gsh;
+    const double* gpost;
 };
 
-// shift phase table: the per-entry sincos of the gather, evaluated once per
-// (shift, component) with the same expression
-__global__ void bp_phase_kernel(int n, int ncomp, int nshift, const int2* comps, const int2* shifts,
-                                double2* ph) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= (long long)nshift * ncomp) return;
-    const int s = (int)(t / ncomp), j = (int)(t % ncomp);
-    const int k = comps[j].x, l = comps[j].y;
-    const double a = -2.0 * 3.14159265358979323846 * ((double)k * shifts[s].x + (double)l * shifts[s].y) / (double)n;
+// the n-th roots of unity of the shift phases, from sincospi of the reduced
+// argument (the integer k sx + l sy reduced mod n exactly)
+__global__ void bp_roots_kernel(int n, double2* ph) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
     double sp, cp;
-    sincos(a, &sp, &cp);
+    sincospi(-2.0 * (double)t / (double)n, &sp, &cp);
     ph[t] = make_double2(cp, sp);
 }
 
@@ -156,24 +155,31 @@ __global__ void bp_phase_kernel(int n, int ncomp, int nshift, const int2* comps,
 // with the phase from the table -- one CTF and one image read per
 // (pose, particle, component) instead of per entry.
 __global__ void __launch_bounds__(128) bp_gather_kernel(BpDev p, BpGroup g, int u0) {
+    extern __shared__ double2 roots[];  // [n]
+    const int n = p.n;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) roots[t] = g.ph[t];
+    __syncthreads();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int u = u0 + blockIdx.y;
     if (j >= p.ncomp) return;
-    const int n = p.n;
     const int k = p.comps[j].x, l = p.comps[j].y;
+    // (k sx + l sy) mod n by a mask when n is a power of two
+    const int kk = k < 0 ? k + n : k, ll = l < 0 ? l + n : l;
+    const bool pow2 = (n & (n - 1)) == 0;
     const double r = __dsqrt_rn((double)(k * k + l * l));
     const size_t pix = (size_t)bp_store(l, n) * n + bp_store(k, n);
     double zr = 0.0, zi = 0.0, wt = 0.0;
     const int qe = g.off[u + 1];
     int q = g.off[u];
     while (q < qe) {
-        const long long part = p.epart[g.ent[q]];
+        const int part = g.gpart[q];
         double sr = 0.0, si = 0.0, sw = 0.0;  // sum over the particle's run of post ph, post
-        for (; q < qe; ++q) {
-            const int e = g.ent[q];
-            if (p.epart[e] != part) break;
-            const double post = p.epost[e];
-            const double2 ph = g.ph[(size_t)(p.ecand[e] % (unsigned)p.n_shifts) * p.ncomp + j];
+        for (; q < qe && g.gpart[q] == part; ++q) {
+            const double post = g.gpost[q];
+            const int2 sh = g.gsh[q];
+            int t = kk * sh.x + ll * sh.y;  // |.| < 2 n^2 (shifts are within the box)
+            t = pow2 ? (t & (n - 1)) : ((t % n) + n) % n;
+            const double2 ph = roots[t];
             sr = fma(post, ph.x, sr);
             si = fma(post, ph.y, si);
             sw += post;
@@ -486,31 +492,42 @@ inline int backproject_run(int n, const cm_bp_input* in, double* stage, cudaStre
                     pose_of.push_back(q);
                     off.push_back(off.back() + cnt[q]);
                 }
-            std::vector<int> ent(off.back()), fill(off.begin(), off.end() - 1);
+            std::vector<int> fill(off.begin(), off.end() - 1);
+            std::vector<int> gpart(off.back());
+            std::vector<int2> gsh(off.back());
+            std::vector<double> gpost(off.back());
             for (long long e = 0; e < in->n_entries; ++e)
-                if (in->entry_posterior[e] > 0.0)
-                    ent[fill[slot[in->entry_candidate[e] / (unsigned)in->n_shifts]]++] = (int)e;
+                if (in->entry_posterior[e] > 0.0) {
+                    const int at = fill[slot[in->entry_candidate[e] / (unsigned)in->n_shifts]]++;
+                    gpart[at] = (int)in->entry_particle[e];
+                    gsh[at] = reinterpret_cast<const int2*>(in->shifts)[in->entry_candidate[e] % (unsigned)in->n_shifts];
+                    gpost[at] = in->entry_posterior[e];
+                }
             const int nused = (int)pose_of.size();
             const int ncomp = (int)comps.size();
             // pose batches bounded to ~1 GB of (Z, Wt)
             const int batch = (int)std::max<size_t>(1, std::min<size_t>(std::min<size_t>((size_t)nused, (size_t)65535), (size_t(1) << 30) / (24 * (size_t)ncomp)));
             BpGroup g{};
-            int *d_pose = nullptr, *d_off = nullptr, *d_ent = nullptr;
+            int *d_pose = nullptr, *d_off = nullptr;
             double2* Z = nullptr;
             double* Wt = nullptr;
             CKS(bufs.put(&d_pose, pose_of.data(), pose_of.size(), st));
             CKS(bufs.put(&d_off, off.data(), off.size(), st));
-            CKS(bufs.put(&d_ent, ent.data(), ent.size(), st));
             CKS(bufs.put(&Z, (const double2*)nullptr, (size_t)batch * ncomp, st));
             CKS(bufs.put(&Wt, (const double*)nullptr, (size_t)batch * ncomp, st));
             double2* ph = nullptr;
-            const long long nph = (long long)in->n_shifts * ncomp;
-            CKS(bufs.put(&ph, (const double2*)nullptr, (size_t)nph, st));
-            bp_phase_kernel<<<(unsigned)((nph + 255) / 256), 256, 0, st>>>(n, ncomp, in->n_shifts, cmp, shf, ph);
-            g = BpGroup{d_pose, d_off, d_ent, Z, Wt, ph};
+            CKS(bufs.put(&ph, (const double2*)nullptr, (size_t)n, st));
+            bp_roots_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, ph);
+            int* d_gpart = nullptr;
+            int2* d_gsh = nullptr;
+            double* d_gpost = nullptr;
+            CKS(bufs.put(&d_gpart, gpart.data(), gpart.size(), st));
+            CKS(bufs.put(&d_gsh, gsh.data(), gsh.size(), st));
+            CKS(bufs.put(&d_gpost, gpost.data(), gpost.size(), st));
+            g = BpGroup{d_pose, d_off, Z, Wt, ph, d_gpart, d_gsh, d_gpost};
             for (int u0 = 0; u0 < nused; u0 += batch) {
                 const dim3 grid((ncomp + 127) / 128, std::min(batch, nused - u0));
-                bp_gather_kernel<<<grid, 128, 0, st>>>(p, g, u0);
+                bp_gather_kernel<<<grid, 128, sizeof(double2) * n, st>>>(p, g, u0);
                 if (in->kernel_kind == 0)
                     bp_spread_kernel<0><<<grid, 128, 0, st>>>(p, g, u0);
                 else
