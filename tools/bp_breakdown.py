@@ -1,3 +1,5 @@
+"""Per-stage host-clock breakdown of the device EM iteration's E-step and
+backprojection at 128^3 (bench.em_iteration's shapes)."""
 import time, json, numpy as np, torch, sys, os
 sys.path.insert(0, os.getcwd())
 import paper_1905_13408_b200 as cm
@@ -8,7 +10,11 @@ sigma2 = np.ones(n // 2 + 1)
 ctx = cm.Context(n, 32, device=0)
 cm.set_particles(ctx, inp)
 cm.backproject_into(ctx, inp, download=False, resident_images=True)
+s = ctx.scale_data()
+cfg = cm.derive_config(s.s_y, s.s_n, 1e-3, 1e-3)
+cfg.inner_iters = 50
 x = np.zeros((n, n, n)); ctx.set_volumes(x)
+ctx.solve(cfg)
 for r in range(2):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     post = cm.e_step(ctx, inp, sigma2, resident_images=True)
