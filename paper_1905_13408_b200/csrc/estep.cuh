@@ -46,6 +46,8 @@ struct EsDev {
     double* res;            // [npart][npose * nshift]
     int n, ncomp, npose, nshift, npart;
     double slack, floor_, bandwidth;
+    const int* sidx;        // [nsh2] the shifts pass 2 evaluates (all but the zero shift)
+    int nsh2, zsh;          // zsh: index of the zero shift (-1: none); its residual is R0
 };
 
 constexpr int ES_NT = 256;
@@ -215,7 +217,8 @@ __global__ void __launch_bounds__(ES_NT) es_min_kernel(EsDev p) {
 
 // pass 2 (estep.cpp:217-249): every shift of each surviving (particle, pose).
 // One CTA per particle and group of ES_PG poses: the particle's terms and the
-// shift-phase tables are read once per group instead of once per pose; PG = 2,
+// shift-phase tables are read once per group instead of once per pose; the
+// zero shift is pass 1's R0 (13 shifts -> 3 batches of 4, not 4); PG = 2,
 // SB = 4 keeps it at 2 CTAs / SM without spills (PG = 4 needs 250 registers).
 constexpr int ES_PG = 2, ES_SB = 4;
 __global__ void __launch_bounds__(ES_NT, 2) es_pass2_kernel(EsDev p) {
@@ -240,8 +243,14 @@ __global__ void __launch_bounds__(ES_NT, 2) es_pass2_kernel(EsDev p) {
     const double* p1r = p.p1r + (size_t)part * p.ncomp;
     const double* p1i = p.p1i + (size_t)part * p.ncomp;
     const double* p2 = p.p2 + (size_t)part * p.ncomp;
+    if (p.zsh >= 0 && threadIdx.x == 0)  // the zero shift's residual is pass 1's R0
+#pragma unroll
+        for (int g = 0; g < PG; ++g)
+            if (alive[g])
+                p.res[((size_t)part * p.npose + pose0 + g) * p.nshift + p.zsh] =
+                    p.R0[(size_t)part * p.npose + pose0 + g];
     double base[PG];
-    for (int s0 = 0; s0 < p.nshift; s0 += SB) {
+    for (int s0 = 0; s0 < p.nsh2; s0 += SB) {
         double v[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) v[q] = 0.0;
@@ -250,8 +259,8 @@ __global__ void __launch_bounds__(ES_NT, 2) es_pass2_kernel(EsDev p) {
             double phr[SB], phi[SB];
 #pragma unroll
             for (int q = 0; q < SB; ++q) {
-                const bool ok = s0 + q < p.nshift;
-                const size_t o = (size_t)(ok ? s0 + q : 0) * p.ncomp + j;
+                const bool ok = s0 + q < p.nsh2;
+                const size_t o = (size_t)(ok ? p.sidx[s0 + q] : 0) * p.ncomp + j;
                 phr[q] = ok ? p.phr[o] : 0.0;
                 phi[q] = ok ? p.phi[o] : 0.0;
             }
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(ES_NT, 2) es_pass2_kernel(EsDev p) {
             if (s0 == 0) base[g] = p.A[part] + v[PG * SB + g];
             if (threadIdx.x == 0 && alive[g]) {
                 double* out = p.res + ((size_t)part * p.npose + pose0 + g) * p.nshift;
-                for (int q = 0; q < SB && s0 + q < p.nshift; ++q) out[s0 + q] = base[g] - 2.0 * v[g * SB + q];
+                for (int q = 0; q < SB && s0 + q < p.nsh2; ++q) out[p.sidx[s0 + q]] = base[g] - 2.0 * v[g * SB + q];
             }
         }
     }
@@ -381,6 +390,18 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
     p = EsDev{V_host ? Vd : reinterpret_cast<const double2*>(V_dev), img, ip, dm, cmp, isg, phr, phi, slice,
               p1r, p1i, p2, pab, A, R0, LB, U, res, n, ncomp, npose, ns, np,
               2.0 * std::log(1.0 / in->prune_floor), in->prune_floor, in->bandwidth};
+    // pass 2 skips the zero shift: its residual is pass 1's R0 (the same sums)
+    std::vector<int> sidx;
+    int zsh = -1;
+    for (int q = 0; q < ns; ++q) {
+        if (zsh < 0 && in->shifts[2 * q] == 0 && in->shifts[2 * q + 1] == 0) zsh = q;
+        else sidx.push_back(q);
+    }
+    int* d_sidx = nullptr;
+    CKS(B.put(&d_sidx, sidx.data(), sidx.size(), st));
+    p.sidx = d_sidx;
+    p.nsh2 = (int)sidx.size();
+    p.zsh = zsh;
     auto blocks = [](long long t) { return (unsigned)((t + ES_NT - 1) / ES_NT); };
     if (ncomp > 0) {
         es_phase_kernel<<<blocks((long long)ns * ncomp), ES_NT, 0, st>>>(p, shf);
