@@ -47,10 +47,12 @@ def parse():
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--iters", type=int, default=100, help="ISTA iterations per step")
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--cpu-n", type=int, default=256, help="CPU-baseline sample side")
-    ap.add_argument("--cpu-iters", type=int, default=1)
-    ap.add_argument("--cpu-procs", type=int, default=0,
-                    help="concurrent reference m_step calls (0: one per host core)")
+    ap.add_argument("--cpu-n", type=int, default=512, help="CPU reference sample side")
+    ap.add_argument("--cpu-iters", type=int, default=1, help="iterations per reference call")
+    ap.add_argument("--cpu-threads", type=int, default=1,
+                    help="FFT threads under the reference (1: the reference as written)")
+    ap.add_argument("--ref-all-cores", type=int, default=0,
+                    help="reference arm: also time a labelled all-cores-FFT variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -217,84 +219,107 @@ def ncu_traffic(n: int):
 
 
 # ---------------------------------------------------------------------------------
-_CPU_JOB = {}
+_CPU_PROBLEM = {}
 
 
-def _cpu_one(_):
-    j = _CPU_JOB
-    t0 = time.perf_counter()
-    rc, x, tr = j["lib"].m_step(j["w"], j["y"], j["x0"], j["x0"], j["cfg"], trace=False)
-    secs = time.perf_counter() - t0
-    return rc, (j["lib"].last_seconds if j["kind"] == "reference" else secs)
-
-
-def cpu_baseline(args, prefer_reference=True):
-    """The reference solver on the host cores (oracle/_ref), bounded sample: one
-    independent m_step per core in parallel processes (m_step itself is
-    single-threaded as written), aggregate voxel-iterations per wall second."""
-    import multiprocessing as mp
-
+def reference_sample(args, threads: int, prefer_reference=True, problem=None) -> dict:
+    """One m_step call of the reference solver on the host (BASELINE config 3's
+    workload: args.cpu_n^3 synthetic blob phantom, lipschitz step with the
+    monotone audit, per_inner reweighting — the same RegConfig semantics as the
+    GPU arm), timed with std::chrono around m_step inside oracle/_ref (inputs
+    already in the reference's host types). The FFT under it is the FFTW3-API
+    shim over oneMKL DFTI with `threads` threads (the reference itself is
+    single-threaded: threads=1 is the unmodified baseline)."""
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import REF_DIR, Oracle, Reference
     from paper_1905_13408_b200 import synth
 
     kind = "reference" if (prefer_reference and (REF_DIR / "libcryomap_ref.so").exists()) else "port"
+    os.environ["CM_REF_FFT_THREADS"] = str(threads)
     lib = Reference() if kind == "reference" else Oracle()
     n = args.cpu_n
-    p = synth.synthetic_problem(n)
-    rc, sy, sn = lib.scale_data(p.weight, p.numerator)
-    rc, cfg = lib.derive_config(sy, sn, p.eps, p.eps_prime)
+    if _CPU_PROBLEM.get("n") != n:
+        _CPU_PROBLEM.clear()
+        p = problem if (problem is not None and problem.n == n) else synth.synthetic_problem(n)
+        rc, sy, sn = lib.scale_data(p.weight, p.numerator)
+        rc, cfg = lib.derive_config(sy, sn, p.eps, p.eps_prime)
+        _CPU_PROBLEM.update(n=n, p=p, cfg=cfg)
+    p, cfg = _CPU_PROBLEM["p"], _CPU_PROBLEM["cfg"]
     cfg.inner_iters = args.cpu_iters
-    procs = max(1, args.cpu_procs or (os.cpu_count() or 1))
-    _CPU_JOB.update(lib=lib, w=p.weight, y=p.numerator, x0=p.x0, cfg=cfg, kind=kind)
     t0 = time.perf_counter()
-    if procs == 1:
-        res = [_cpu_one(0)]
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(_cpu_one, range(procs))
+    rc, x, tr = lib.m_step(p.weight, p.numerator, p.x0, p.x0, cfg, trace=False)
     wall = time.perf_counter() - t0
-    assert all(r[0] == 0 for r in res), res
-    per_call = statistics.median(r[1] for r in res)
-    v = procs * n ** 3 * args.cpu_iters / wall
-    src = "unmodified reference sources + FFTW3-API shim (oracle/fftc.c)" if kind == "reference" \
-        else "oracle C restatement"
+    assert rc == 0, rc
+    secs = lib.last_seconds if kind == "reference" else wall
+    fft = ("FFTW3-API shim over oneMKL DFTI (libtorch_cpu.so), "
+           f"{threads} FFT thread(s)") if kind == "reference" else "oracle/fftc.c"
+    src = ("unmodified reference sources (oracle/_ref/libcryomap_ref.so)" if kind == "reference"
+           else "oracle C restatement")
     return {
-        "value": v, "unit": "voxel-iterations/s", "cores": procs, "kind": kind,
-        "sample": f"{src}; {procs} concurrent independent m_step calls (one per host core; "
-                  f"m_step is single-threaded as written) on {n}^3, {args.cpu_iters} "
-                  f"iteration(s) each, lipschitz step with audit, per_inner reweighting; "
-                  f"wall {wall:.2f} s, median call {per_call:.2f} s; host nproc={os.cpu_count()}",
-        "seconds": wall, "voxel_iterations": procs * n ** 3 * args.cpu_iters,
+        "value": n ** 3 * args.cpu_iters / secs, "unit": "voxel-iterations/s", "cores": threads,
+        "kind": kind, "seconds": secs, "voxel_iterations": n ** 3 * args.cpu_iters,
+        "sample": f"{src} + {fft}; one m_step call on the {n}^3 synthetic blob phantom "
+                  f"(BASELINE config 3 inputs), {args.cpu_iters} iteration(s), lipschitz step "
+                  f"with audit, per_inner reweighting; m_step wall {secs:.2f} s (std::chrono "
+                  f"around the call, inputs resident in host memory); host nproc={os.cpu_count()}",
     }
 
 
+def cpu_baseline(args, problem=None):
+    """The reference on ONE host core (m_step and its FFTW calls are
+    single-threaded as written), bounded sample: one call of one
+    iteration (about 95 s at 512^3: the reference's non-FFT passes over its
+    fp64 full-grid temporaries dominate, not its FFTs)."""
+    cb = reference_sample(args, 1, problem=problem)
+    cb.pop("seconds", None)
+    cb.pop("voxel_iterations", None)
+    return cb
+
+
 def run_reference(args):
-    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    """--impl reference: the unmodified reference m_step on the host cores, the
+    same workload (512^3, reference semantics) as the GPU arm; rank 0 only.
+    Each step = one m_step call of args.cpu_iters iteration(s) (about 95 s at
+    512^3 on one core), so K and W are capped to keep the run to a few minutes:
+    one step and no warm-up at 512^3 (the call allocates and faults in its own
+    temporaries every time, warm or not)."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 3))
-    warm = min(args.warmup, 1)
+    big = args.cpu_n >= 512
+    steps = 1 if big else max(1, min(args.steps, 2))
+    warm = 0 if big else min(args.warmup, 1)
     secs, work = 0.0, 0
     cb = None
     for s in range(warm + steps):
-        cb = cpu_baseline(args)
+        cb = reference_sample(args, args.cpu_threads)
         if s >= warm:
             secs += cb["seconds"]
             work += cb["voxel_iterations"]
     v = work / secs
+    secondary = None
+    if args.ref_all_cores and args.cpu_threads == 1 and (os.cpu_count() or 1) > 1:
+        # labelled modified baseline: the same call with the FFT shim on all cores
+        mt = reference_sample(args, os.cpu_count())
+        secondary = {"value": mt["value"], "unit": mt["unit"], "cores": mt["cores"],
+                     "note": "MODIFIED baseline: reference m_step with its FFTs multi-threaded "
+                             "(the reference never calls fftw_init_threads)",
+                     "sample": mt["sample"]}
     line = {
         "metric": "solver voxel-iterations/s (512^3 m_step, ISTA, per-inner reweighting, audit)",
         "value": v, "unit": "voxel-iterations/s", "impl": "reference", "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": 1e3 * secs / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"m_step {args.n}^3 (bounded CPU sample at {args.cpu_n}^3)",
-                   "side": args.cpu_n, "iters_per_step": args.cpu_iters},
+        "config": {"workload": f"m_step {args.cpu_n}^3 synthetic blob phantom (BASELINE config 3),"
+                               f" {args.cpu_iters} ISTA iteration(s) per step",
+                   "side": args.cpu_n, "iters_per_step": args.cpu_iters, "step_rule": "lipschitz",
+                   "refresh": "per_inner", "audit": True},
         "cpu_baseline": {k: cb[k] for k in ("kind", "cores", "sample")} | {"value": v,
                                                                            "unit": cb["unit"]},
         "e2e": {"value": v, "unit": "voxel-iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "secondary_all_cores": secondary,
     }
     print(json.dumps(line), flush=True)
 
@@ -642,9 +667,7 @@ def run_ours(args):
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(args)
-            cb.pop("seconds", None)
-            cb.pop("voxel_iterations", None)
+            cb = cpu_baseline(args, problem=p)
         except Exception as e:  # noqa: BLE001
             cb = {"value": None, "error": str(e)[:200]}
 

@@ -254,7 +254,8 @@ int cm_backproject(cm_ctx* ctx, const cm_bp_input* in, double* weight_out, doubl
     CTX_GUARD(ctx);
     ImplBase* im = ctx->impl.get();
     double* stage = im->acc_stage();
-    im->acc_set = false;  // the staging grid is about to be overwritten
+    // the staging grid is scratch: the resident W / Yh (and acc_set) change only
+    // in commit_acc_stage, so a call rejected by validation leaves them usable
     CKS(backproject_run(ctx->n, in, stage, im->stream, &ctx->particles));
     const size_t L = (size_t)ctx->n * ctx->n * ctx->n;
     if (weight_out &&

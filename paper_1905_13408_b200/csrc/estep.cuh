@@ -314,7 +314,9 @@ __global__ void __launch_bounds__(ES_NT) es_softmax_kernel(EsDev p, double* post
     }
     es_block_sum<1>(kv, red);
     const double kept = kv[0];
-    for (int c = threadIdx.x; c < nc; c += ES_NT) o[c] = o[c] / kept;
+    // every candidate below prune_floor: the reference's row is empty
+    // (estep.cpp:257-263 pushes no entry), not 0/0
+    for (int c = threadIdx.x; c < nc; c += ES_NT) o[c] = kept > 0.0 ? o[c] / kept : 0.0;
 }
 
 // Host side. V: device FourierVolume (host upload or the resident spectrum).

@@ -159,6 +159,20 @@ class Oracle(_Lib):
         return rc, out
 
 
+def _preload_mkl() -> None:
+    """The reference's FFTW shim runs on oneMKL DFTI from libtorch_cpu.so
+    (oracle/fftw_shim/fftw_shim_mkl.c). Load that library RTLD_GLOBAL before the
+    reference: loaded after numpy's OpenBLAS without it, the process aborts at
+    exit (free(): invalid pointer)."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("torch")
+    if spec and spec.origin:
+        lib = Path(spec.origin).parent / "lib" / "libtorch_cpu.so"
+        if lib.exists():
+            C.CDLL(str(lib), mode=C.RTLD_GLOBAL)
+
+
 class Reference(_Lib):
     """The unmodified reference library (oracle/_ref/libcryomap_ref.so)."""
 
@@ -166,6 +180,7 @@ class Reference(_Lib):
     libname = "libcryomap_ref.so"
 
     def __init__(self):
+        _preload_mkl()
         super().__init__()
         self.f("last_error").restype = C.c_char_p
 

@@ -15,7 +15,7 @@ ROOT = Path(__file__).resolve().parent.parent
                     reason="oracle/_ref not built")
 def test_reference_arm_json_line():
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "0", "--cpu-n", "16", "--cpu-procs", "2"],
+                        "--warmup", "0", "--cpu-n", "16", "--cpu-threads", "2"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -28,6 +28,7 @@ def test_reference_arm_json_line():
     assert line["higher_is_better"] is True
     cb = line["cpu_baseline"]
     assert cb["kind"] == "reference" and cb["cores"] == 2 and cb["value"] == line["value"]
+    assert "oneMKL" in cb["sample"] and line["config"]["side"] == 16
     assert line["e2e"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in line["config"]

@@ -63,6 +63,51 @@ def test_matches_reference(n, m, kind, cut, scale, grid, r):
     np.testing.assert_allclose(got.sum(axis=1), 1.0, rtol=1e-12)
 
 
+# production-shaped grids: 128^2 images, >= 200 poses (odd: pass 2's tail group
+# of one pose), the zero-shift-only grid (no pass-2 shifts), one CTA pair per pose
+BIG_CASES = [
+    # n, images, n_poses, shift radius, sigma scale, prune_floor
+    (128, 24, 201, 2, 0.02, 1e-8),   # broad: ~2300 of 2613 candidates survive
+    (128, 24, 201, 2, 0.005, 1e-8),  # peaked: pose pruning active, 6-75 survive
+    (128, 16, 13, 0, 0.005, 1e-8),
+    (64, 20, 211, 1, 0.003, 1e-6),   # 1-7 survivors, a larger floor
+]
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("n,m,npose,r,scale,floor", BIG_CASES)
+def test_matches_reference_production_grids(n, m, npose, r, scale, floor):
+    R = Reference()
+    inp, V, s2 = problem(n, m, GAUSSIAN, -1.0, scale, 3 * n + m, True, r, n_poses=npose)
+    rc, want = R.estep(inp, V, s2, prune_floor=floor, threads=8)
+    assert rc == 0, R.last_error()
+    ctx = cm.Context(n)
+    got = cm.e_step(ctx, inp, s2, volume=V, prune_floor=floor)
+    ctx.close()
+    np.testing.assert_array_equal(got != 0, want != 0)
+    assert np.abs(got - want).max() <= 1e-10
+    np.testing.assert_allclose(got.sum(axis=1), 1.0, rtol=1e-12)
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_prune_floor_above_every_candidate_gives_empty_rows():
+    """prune_floor larger than the best candidate's posterior: the reference
+    pushes no entry (estep.cpp:257-263), the device writes zeros (not 0/0)."""
+    R = Reference()
+    inp, V, s2 = problem(16, 6, GAUSSIAN, -1.0, 1e6, 9, True, 1)  # flat posteriors
+    rc, want = R.estep(inp, V, s2, prune_floor=0.9)
+    assert rc == 0, R.last_error()
+    ctx = cm.Context(16)
+    got = cm.e_step(ctx, inp, s2, volume=V, prune_floor=0.9)
+    ctx.close()
+    assert np.isfinite(got).all()
+    np.testing.assert_array_equal(got != 0, want != 0)
+    assert np.abs(got - want).max() <= 1e-10
+    assert (want.sum(axis=1) == 0).any()
+
+
 @pytest.mark.gpu
 @needs_ref
 def test_spread_posteriors_exercise_many_candidates():
