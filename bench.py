@@ -64,6 +64,7 @@ def parse():
                     help="side of the device-rendered z-slab scaling run (0: skip)")
     ap.add_argument("--big-iters", type=int, default=20)
     ap.add_argument("--em", type=int, default=1, help="time the EM-block extras (V, FSC)")
+    ap.add_argument("--prec64", type=int, default=1, help="also time the fp64 parity mode")
     return ap.parse_args()
 
 
@@ -659,6 +660,30 @@ def run_ours(args):
         except Exception as e:  # reported, never fatal to the headline line
             em["iteration_128"] = {"error": str(e)[:200]}
 
+    # ---- the fp64 parity mode (the C++ adapter's default precision): same solve
+    p64 = None
+    if args.prec64 and world == 1 and args.precision == 32:
+        c64 = cm.Context(n, 64, device=local)
+        c64.set_accumulator(acc)
+        c64.set_volumes(p.x0, p.x0)
+        k64 = cm.RegConfig(**{**cfg.__dict__, "inner_iters": 20})
+        c64.solve(k64)
+        torch.cuda.synchronize()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record()
+        for _ in range(3):
+            c64.solve(k64)
+        h1.record()
+        torch.cuda.synchronize()
+        ms64 = h0.elapsed_time(h1) / (3 * 20)
+        p64 = {"dtype": "f64", "iters_per_step": 20, "steps": 3, "ms_per_iter": ms64,
+               "value": float(n) ** 3 / (ms64 / 1e3), "unit": "voxel-iterations/s",
+               "note": "same 512^3 solve in the fp64 parity mode (cm_ctx_create precision 64, "
+                       "the C++ adapter's default): every device array twice the bytes"}
+        c64.close()
+        del c64
+
     big = None
     if args.big_n:
         del ctx
@@ -688,6 +713,7 @@ def run_ours(args):
             "device_ms_solver_stream": dev_ms, "gen_seconds": gen_s,
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches, "time_to_tolerance": ttt, "big": big, "em_block": em,
+            "precision64": p64,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,0 +1,143 @@
+// Host <-> device transfers of the drop-in's PAGEABLE buffers.
+//
+// The reference API hands the solver plain std::vector storage
+// (regularizer.hpp:98-100: AccumulatorPair, Volume3D by const&; the result
+// returned by value), i.e. pageable memory. cudaMemcpyAsync from pageable
+// memory is synchronous and staged by the driver through small bounce
+// buffers. HostXfer instead streams such buffers through a ring of pinned
+// 64 MiB chunks: the host copy of chunk i+1 (split over a few threads) runs
+// while the DMA of chunk i is in flight on the context's stream, so the
+// transfer runs at the PCIe rate rather than memcpy + DMA in series.
+// Pinned (page-locked or cudaHostRegister'ed) host pointers go straight to
+// cudaMemcpyAsync.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/cm_api.h"
+
+namespace cm {
+
+int fail(int code, const std::string& msg);
+
+struct HostXfer {
+    static constexpr size_t kChunk = size_t(64) << 20;
+    static constexpr int kBufs = 3;
+    unsigned char* buf[kBufs] = {};
+    cudaEvent_t done[kBufs] = {};
+    int threads = std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+
+    ~HostXfer() {
+        for (int q = 0; q < kBufs; ++q) {
+            if (buf[q]) cudaFreeHost(buf[q]);
+            if (done[q]) cudaEventDestroy(done[q]);
+        }
+    }
+    int ensure() {
+        for (int q = 0; q < kBufs; ++q) {
+            if (!buf[q] && cudaHostAlloc((void**)&buf[q], kChunk, cudaHostAllocDefault) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "pinned staging allocation failed");
+            if (!done[q] && cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "staging event creation failed");
+        }
+        return CM_OK;
+    }
+    static bool pinned(const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+    // memcpy split over `threads` threads (host-side bandwidth of one core is
+    // well below the PCIe rate)
+    void pcopy(void* dst, const void* src, size_t bytes) const {
+        const int nt = bytes >= (size_t(8) << 20) ? threads : 1;
+        if (nt <= 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        const size_t part = (bytes / nt + 4095) & ~size_t(4095);
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) {
+            const size_t off = part * t;
+            if (off >= bytes) break;
+            pool.emplace_back([=] {
+                std::memcpy((unsigned char*)dst + off, (const unsigned char*)src + off,
+                            std::min(part, bytes - off));
+            });
+        }
+        std::memcpy(dst, src, std::min(part, bytes));
+        for (auto& th : pool) th.join();
+    }
+
+    // stream-ordered on return for pinned sources; for pageable sources the
+    // host buffer may be reused on return (the last chunk is in flight from the
+    // pinned ring, which the next call waits for)
+    int h2d(void* dev, const void* host, size_t bytes, cudaStream_t st) {
+        if (bytes == 0) return CM_OK;
+        if (pinned(host)) {
+            if (cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "host-to-device copy failed");
+            return CM_OK;
+        }
+        if (int rc = ensure()) return rc;
+        size_t off = 0;
+        for (int i = 0; off < bytes; ++i, off += kChunk) {
+            const int b = i % kBufs;
+            const size_t len = std::min(kChunk, bytes - off);
+            if (cudaEventSynchronize(done[b]) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "staging wait failed");
+            pcopy(buf[b], (const unsigned char*)host + off, len);
+            if (cudaMemcpyAsync((unsigned char*)dev + off, buf[b], len, cudaMemcpyHostToDevice, st) !=
+                    cudaSuccess ||
+                cudaEventRecord(done[b], st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "host-to-device copy failed");
+        }
+        return CM_OK;
+    }
+
+    // synchronous: the host buffer holds the data on return
+    int d2h(void* host, const void* dev, size_t bytes, cudaStream_t st) {
+        if (bytes == 0) return CM_OK;
+        if (pinned(host)) {
+            if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "device-to-host copy failed");
+            return CM_OK;
+        }
+        if (int rc = ensure()) return rc;
+        const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+        auto issue = [&](size_t i) -> int {
+            const int b = (int)(i % kBufs);
+            const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+            if (cudaMemcpyAsync(buf[b], (const unsigned char*)dev + off, len, cudaMemcpyDeviceToHost,
+                                st) != cudaSuccess ||
+                cudaEventRecord(done[b], st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "device-to-host copy failed");
+            return CM_OK;
+        };
+        // keep kBufs-1 chunks in flight ahead of the host copy
+        for (size_t i = 0; i < std::min(nchunk, (size_t)kBufs - 1); ++i)
+            if (int rc = issue(i)) return rc;
+        for (size_t i = 0; i < nchunk; ++i) {
+            const int b = (int)(i % kBufs);
+            if (cudaEventSynchronize(done[b]) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "device-to-host copy failed");
+            if (i + kBufs - 1 < nchunk)
+                if (int rc = issue(i + kBufs - 1)) return rc;
+            const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+            pcopy((unsigned char*)host + off, buf[b], len);
+        }
+        return CM_OK;
+    }
+};
+
+} // namespace cm

@@ -28,11 +28,24 @@
 #include "xyfused.cuh"
 #include "zpass.cuh"
 #include "tma.cuh"
+#include "host_xfer.h"
+
+#include <nvtx3/nvToolsExt.h>
 
 namespace cm {
 
+// NVTX range for profilers (nsys / ncu --nvtx): scoped push / pop
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // thread-local last error (defined in cm_api.cu)
 int fail(int code, const std::string& msg);
+
+} // namespace cm
+#include "zpass_tma.cuh"
+namespace cm {
 
 #define CK(call)                                                                         \
     do {                                                                                 \
@@ -342,6 +355,7 @@ struct ImplBase {
     virtual const double* result_spectrum_device(int centered) = 0;
 
     cudaStream_t stream = nullptr;
+    HostXfer xfer;  // pinned chunk ring for the drop-in's pageable host buffers
     int n = 0;
     bool acc_set = false, acc_finalized = false, vol_set = false, anchor_is_init = false;
     double residue = 0.0, max_weight = 0.0, s_y = 0.0, s_n = 0.0;
@@ -384,6 +398,11 @@ struct Impl final : ImplBase {
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
+    // TMA-fed persistent z pass (zpass_tma.cuh): fp32, N in {256, 512}; CM_ZT=0 -> zmain
+    static constexpr bool ZT = std::is_same<R, float>::value && ZtGeo<N>::OK;
+    bool use_zt = false;
+    int zt_grid = 0;
+    CUtensorMap tmz_S{}, tmz_W{}, tmz_Y{};
     // programmatic dependent launch between the per-iteration kernels (each
     // waits on griddepcontrol before touching its predecessor's output); opt-in:
     // measured neutral (dependents cannot start work before the predecessor
@@ -594,6 +613,22 @@ struct Impl final : ImplBase {
             s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
         }
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
+        if constexpr (ZT) {
+            using ZT_ = ZtGeo<N>;
+            const char* e = std::getenv("CM_ZT");
+            use_zt = !(e && e[0] == '0');
+            CK(zt_prepare<N>());
+            int occt = 0, devt = 0, smst = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occt, zt_kernel<N, ZM_FULL>, ZT_::NT,
+                                                             ZT_::SMEM));
+            CK(cudaGetDevice(&devt));
+            CK(cudaDeviceGetAttribute(&smst, cudaDevAttrMultiProcessorCount, devt));
+            zt_grid = std::max(1, std::min(ZT_::NTILES, smst * std::max(occt, 1)));
+            if (zt_grid > ZGeo<R, N>::NBM) use_zt = false;
+            CKS(zt_make_map(S, N, true, ZT_::TW, ZT_::BOXC, &tmz_S));
+            CKS(zt_make_map(W, N, false, ZT_::TW, ZT_::BOXC, &tmz_W));
+            CKS(zt_make_map(Yh, N, true, ZT_::TW, ZT_::BOXC, &tmz_Y));
+        }
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
         CKS(dalloc(&st, 1));
@@ -703,15 +738,27 @@ struct Impl final : ImplBase {
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
         ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
-        dim3 grid(Nh / ZG::TW, N);
-        CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
+        if constexpr (ZT) {
+            if (use_zt) {
+                CK(launch_pdl(use_pdl, zt_kernel<N, MODE>, dim3(zt_grid), dim3(ZtGeo<N>::NT),
+                              ZtGeo<N>::SMEM, stream, p, tmz_S, tmz_W, tmz_Y));
+            } else {
+                dim3 grid(Nh / ZG::TW, N);
+                CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN,
+                              stream, p));
+            }
+        } else {
+            dim3 grid(Nh / ZG::TW, N);
+            CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN,
+                          stream, p));
+        }
         if constexpr (MODE != ZM_FWD)
             CK(launch_pdl(use_pdl, zcol0_kernel<R, N, MODE>, dim3(N / 2 + 1), dim3(ZG::NT0),
                           ZG::SMEM_COL0, stream, p));
         return CM_OK;
     }
     int upload_real(const double* host, R* dst) {
-        CK(cudaMemcpyAsync(stage, host, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
+        CKS(xfer.h2d(stage, host, sizeof(double) * L, stream));
         to_real_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(stage, dst, L);
         CK(cudaGetLastError());
         return CM_OK;
@@ -719,15 +766,14 @@ struct Impl final : ImplBase {
     int download_real(const R* src, double* host) {
         to_double_kernel<R><<<grid_for(L, 256), 256, 0, stream>>>(src, stage, L);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(host, stage, sizeof(double) * L, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
+        CKS(xfer.d2h(host, stage, sizeof(double) * L, stream));
         return CM_OK;
     }
 
     // ---- accumulator ---------------------------------------------------------------
     int set_accumulator(const double* w, const double* y, int finalized) override {
-        CK(cudaMemcpyAsync(stage, w, sizeof(double) * L, cudaMemcpyHostToDevice, stream));
-        CK(cudaMemcpyAsync(stage + L, y, sizeof(double) * 2 * L, cudaMemcpyHostToDevice, stream));
+        CKS(xfer.h2d(stage, w, sizeof(double) * L, stream));
+        CKS(xfer.h2d(stage + L, y, sizeof(double) * 2 * L, stream));
         return commit_acc_stage(finalized);
     }
     double* acc_stage() override { return stage; }
@@ -785,6 +831,7 @@ struct Impl final : ImplBase {
 
     // ---- the solver ------------------------------------------------------------------
     int solve(const cm_reg_config* c, cm_trace_row* trace, int cap, cm_solve_stats* stats) override {
+        NvtxRange nvtx_solve("cm_m_step_solve");
         CKS(validate(c));
         CKS(require_acc());
         if (!vol_set) return fail(CM_ERR_STATE, "volumes not set");
@@ -897,8 +944,15 @@ struct Impl final : ImplBase {
         cudaEvent_t pev[8] = {};
         if (profiling)
             for (auto& e : pev) CK(cudaEventCreate(&e));
+        static const char* const kPhase[8] = {"z_pass", "y_inverse", "x_c2r", "stencil",
+                                              "finalize", "x_r2c", "y_forward", "end"};
         auto mark = [&](int q) -> int {
-            if (profiling) CK(cudaEventRecord(pev[q], stream));
+            if (profiling) {
+                CK(cudaEventRecord(pev[q], stream));
+                // per-kernel NVTX ranges in the profiling solve (kernels launched one by one)
+                if (q > 0) nvtxRangePop();
+                if (q < 7) nvtxRangePushA(kPhase[q]);
+            }
             return CM_OK;
         };
         auto sweep_and_finalize = [&](int g, cudaEvent_t mid) -> int {
