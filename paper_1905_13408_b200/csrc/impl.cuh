@@ -44,7 +44,7 @@ struct NvtxRange {
 int fail(int code, const std::string& msg);
 
 } // namespace cm
-#include "zpass_tma.cuh"
+#include "ypass_tma.cuh"
 namespace cm {
 
 #define CK(call)                                                                         \
@@ -75,7 +75,7 @@ template <typename R>
 __global__ void convert_acc_kernel(int n, const double* __restrict__ W,
                                    const double* __restrict__ Y, R* Wm, R* Wn, Cx<R>* Ym,
                                    Cx<R>* Yn, double* part, unsigned long long* maxes,
-                                   Cx<R>* Q0 = nullptr) {
+                                   Cx<R>* Q0 = nullptr, int ztw = 0) {
     using C = Cx<R>;
     const int nh = n / 2;
     const size_t total = (size_t)n * n * (nh + 1);
@@ -120,7 +120,9 @@ __global__ void convert_acc_kernel(int n, const double* __restrict__ W,
         const double pr = sg * 0.5 * (yr + mr), pi = sg * 0.5 * (yi - mi);
         if (!Wm) {  // statistics only (z-slab ranks convert their own rows)
         } else if (a < nh) {
-            const size_t o = ((size_t)c * n + b) * nh + a;
+            // ztw > 0: z-tiled [b * nh/ztw + a/ztw][c][ztw] (zmain_kernel's W / Yh tiles)
+            const size_t o = ztw ? (((size_t)b * (nh / ztw) + a / ztw) * n + c) * ztw + a % ztw
+                                 : ((size_t)c * n + b) * nh + a;
             Wm[o] = R(wp);
             Ym[o] = cx<C>(R(pr), R(pi));
         } else {
@@ -398,11 +400,11 @@ struct Impl final : ImplBase {
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
-    // TMA-fed persistent z pass (zpass_tma.cuh): fp32, N in {256, 512}; CM_ZT=0 -> zmain
-    static constexpr bool ZT = std::is_same<R, float>::value && ZtGeo<N>::OK;
-    bool use_zt = false;
-    int zt_grid = 0;
-    CUtensorMap tmz_S{}, tmz_W{}, tmz_Y{};
+    // TMA-fed persistent y pass (ypass_tma.cuh): fp32, N in {256, 512}; CM_YT=0 -> ypass
+    static constexpr bool YT = std::is_same<R, float>::value && YtGeo<N>::OK;
+    bool use_yt = false;
+    int yt_grid = 0;
+    CUtensorMap tmy_S{};
     // programmatic dependent launch between the per-iteration kernels (each
     // waits on griddepcontrol before touching its predecessor's output); opt-in:
     // measured neutral (dependents cannot start work before the predecessor
@@ -613,21 +615,18 @@ struct Impl final : ImplBase {
             s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
         }
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
-        if constexpr (ZT) {
-            using ZT_ = ZtGeo<N>;
-            const char* e = std::getenv("CM_ZT");
-            use_zt = !(e && e[0] == '0');
-            CK(zt_prepare<N>());
+        if constexpr (YT) {
+            using YG_ = YtGeo<N>;
+            const char* e = std::getenv("CM_YT");
+            use_yt = !(e && e[0] == '0');
+            CK(yt_prepare<N>());
             int occt = 0, devt = 0, smst = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occt, zt_kernel<N, ZM_FULL>, ZT_::NT,
-                                                             ZT_::SMEM));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occt, ytma_kernel<N, true>, YG_::NT,
+                                                             YG_::SMEM));
             CK(cudaGetDevice(&devt));
             CK(cudaDeviceGetAttribute(&smst, cudaDevAttrMultiProcessorCount, devt));
-            zt_grid = std::max(1, std::min(ZT_::NTILES, smst * std::max(occt, 1)));
-            if (zt_grid > ZGeo<R, N>::NBM) use_zt = false;
-            CKS(zt_make_map(S, N, true, ZT_::TW, ZT_::BOXC, &tmz_S));
-            CKS(zt_make_map(W, N, false, ZT_::TW, ZT_::BOXC, &tmz_W));
-            CKS(zt_make_map(Yh, N, true, ZT_::TW, ZT_::BOXC, &tmz_Y));
+            yt_grid = std::max(1, std::min(YG_::NTILES, smst * std::max(occt, 1)));
+            CKS(yt_make_map(S, N, YG_::TW, YG_::BOXB, &tmy_S));
         }
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
@@ -689,6 +688,18 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
     int launch_y(bool fwd, DevState* s) {
+        if constexpr (YT) {
+            if (use_yt) {
+                const int* stop = s ? (fwd ? &s->done_y : &s->done) : nullptr;
+                if (fwd)
+                    CK(launch_pdl(use_pdl, ytma_kernel<N, true>, dim3(yt_grid), dim3(YtGeo<N>::NT),
+                                  YtGeo<N>::SMEM, stream, S, twN, stop, tmy_S));
+                else
+                    CK(launch_pdl(use_pdl, ytma_kernel<N, false>, dim3(yt_grid), dim3(YtGeo<N>::NT),
+                                  YtGeo<N>::SMEM, stream, S, twN, stop, tmy_S));
+                return CM_OK;
+            }
+        }
         const SpecLayout nat = spec_layout((long long)N * Nh, 0, N, Nh);
         YParams<R> p{S, twN, fwd ? twF4 : twI4, s ? (fwd ? &s->done_y : &s->done) : nullptr,
                      nullptr, nat, nat, N, 0, Nh / G::TWY};
@@ -738,20 +749,8 @@ struct Impl final : ImplBase {
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
         ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
-        if constexpr (ZT) {
-            if (use_zt) {
-                CK(launch_pdl(use_pdl, zt_kernel<N, MODE>, dim3(zt_grid), dim3(ZtGeo<N>::NT),
-                              ZtGeo<N>::SMEM, stream, p, tmz_S, tmz_W, tmz_Y));
-            } else {
-                dim3 grid(Nh / ZG::TW, N);
-                CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN,
-                              stream, p));
-            }
-        } else {
-            dim3 grid(Nh / ZG::TW, N);
-            CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN,
-                          stream, p));
-        }
+        dim3 grid(Nh / ZG::TW, N);
+        CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
         if constexpr (MODE != ZM_FWD)
             CK(launch_pdl(use_pdl, zcol0_kernel<R, N, MODE>, dim3(N / 2 + 1), dim3(ZG::NT0),
                           ZG::SMEM_COL0, stream, p));
@@ -783,7 +782,7 @@ struct Impl final : ImplBase {
         CK(cudaMemsetAsync(maxes, 0, sizeof(unsigned long long) * 4, stream));
         const int blocks = grid_for(NN * (Nh + 1), 256);
         convert_acc_kernel<R><<<blocks, 256, 0, stream>>>(N, stage, stage + L, W, Wn, Yh, Yn,
-                                                          part_acc, maxes, Q0);
+                                                          part_acc, maxes, Q0, ZGeo<R, N>::TW);
         CK(cudaGetLastError());
         std::vector<double> parts(2 * (size_t)blocks);
         unsigned long long mx[4];

@@ -136,10 +136,18 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     R w[E];
     C y[E];
     constexpr bool PREFETCH = ZGeo<R, N>::PREFETCH && MODE != ZM_FWD;
+    // W / Yh layout: one GPU (NR = N) stores them z-tiled, [tile][c][TW] with
+    // tile = b * NTX + h / TW (convert_acc_kernel), so a CTA's W / Yh tile is
+    // one contiguous 32 / 64 KB block instead of 128-byte segments 1 MB apart;
+    // b-slab ranks keep [c][b][h]
+    auto wy_index = [&](int c) -> size_t {
+        if constexpr (NR != 0) return ((size_t)tile * N + c) * TW + col;
+        else return ((size_t)c * nrows + b) * hl + hloc;
+    };
     if constexpr (PREFETCH) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const size_t gi = ((size_t)(t + T * m) * nrows + b) * hl + hloc;
+            const size_t gi = wy_index(t + T * m);
             w[m] = __ldg(p.W + gi);
             y[m] = __ldg(p.Yh + gi);
         }
@@ -153,8 +161,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         for (int m = 0; m < E; ++m) sbase[(size_t)(t + T * m) * splane] = v[m];
         return;
     }
-    R quad = R(0), cross = R(0);
-    const size_t lplane = opaque(plane);
+    // two accumulator pairs (even / odd m): half-length dependency chains
+    R quad = R(0), cross = R(0), quad1 = R(0), cross1 = R(0);
     if (h == 0) {
 #pragma unroll
         for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
             if constexpr (!PREFETCH) {
 #pragma unroll
                 for (int m = g0; m < g0 + G; ++m) {
-                    const size_t gi = (size_t)(t + T * m) * lplane + (size_t)b * hl + hloc;
+                    const size_t gi = wy_index(t + T * m);
                     w[m] = __ldg(p.W + gi);
                     y[m] = p.Yh[gi];
                 }
@@ -175,15 +183,21 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
 #pragma unroll
             for (int m = g0; m < g0 + G; ++m) {
                 const C f = v[m];
-                quad += w[m] * (f.x * f.x + f.y * f.y);
-                cross += y[m].x * f.x + y[m].y * f.y;
+                if (m & 1) {
+                    quad1 += w[m] * (f.x * f.x + f.y * f.y);
+                    cross1 += y[m].x * f.x + y[m].y * f.y;
+                } else {
+                    quad += w[m] * (f.x * f.x + f.y * f.y);
+                    cross += y[m].x * f.x + y[m].y * f.y;
+                }
                 v[m] = cx<C>(w[m] * f.x - y[m].x, w[m] * f.y - y[m].y);
             }
             if constexpr (!PREFETCH) asm volatile("" ::: "memory");
         }
     }
     if (p.part) {
-        double acc[2] = {2.0 * (double)quad, 2.0 * (double)cross};  // mates 0 < h < N/2
+        double acc[2] = {2.0 * ((double)quad + (double)quad1),
+                         2.0 * ((double)cross + (double)cross1)};  // mates 0 < h < N/2
         block_sum<2>(acc, red);
         if (threadIdx.x == 0) {
             p.part[tile * NP3 + 0] = acc[0];
