@@ -573,8 +573,29 @@ def run_ours(args):
                       "frac": iter_bytes / (ms_iter / 1e3) / 1e9 / hbm},
     }
 
-    # ---- end to end through the C ABI with pinned host buffers -----------------------
-    e2e = None
+    # ---- end to end through the C ABI -----------------------------------------------
+    # e2e: PAGEABLE numpy buffers, what the drop-in receives (std::vector storage
+    # behind regularizer.hpp's AccumulatorPair / Volume3D; the library streams them
+    # through its pinned chunk ring); e2e_pinned: the same from page-locked buffers
+    e2e = e2e_pinned = None
+    if not args.no_e2e:
+        L = n ** 3
+        out_pg = np.empty((n, n, n))
+        ctx.m_step_host(acc, p.x0, p.x0, cfg, out_pg)  # warm
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            ctx.m_step_host(acc, p.x0, p.x0, cfg, out_pg)
+        f1.record()
+        torch.cuda.synchronize()
+        e_ms = allreduce_max(f0.elapsed_time(f1), world)
+        e2e = {"value": float(n) ** 3 * iters * args.e2e_steps * world / (e_ms / 1e3),
+               "unit": "voxel-iterations/s", "h2d_bytes_per_step": 32 * L,
+               "d2h_bytes_per_step": 8 * L, "steps": args.e2e_steps,
+               "ms_per_step": e_ms / args.e2e_steps, "host_buffers": "pageable (numpy)",
+               "api": "cm_m_step: fp64 full-grid W, Y, x_init (= anchor) in, x out"}
     if not args.no_e2e:
         L = n ** 3
         pin_w = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy().reshape(n, n, n)
@@ -596,10 +617,10 @@ def run_ours(args):
         f1.record()
         torch.cuda.synchronize()
         e_ms = allreduce_max(f0.elapsed_time(f1), world)
-        e2e = {"value": float(n) ** 3 * iters * args.e2e_steps * world / (e_ms / 1e3),
-               "unit": "voxel-iterations/s", "h2d_bytes_per_step": 32 * L,
-               "d2h_bytes_per_step": 8 * L, "steps": args.e2e_steps,
-               "ms_per_step": e_ms / args.e2e_steps}
+        e2e_pinned = {"value": float(n) ** 3 * iters * args.e2e_steps * world / (e_ms / 1e3),
+                      "unit": "voxel-iterations/s", "h2d_bytes_per_step": 32 * L,
+                      "d2h_bytes_per_step": 8 * L, "steps": args.e2e_steps,
+                      "ms_per_step": e_ms / args.e2e_steps, "host_buffers": "page-locked"}
 
     # ---- time to tolerance ----------------------------------------------------------------
     # "Medium accuracy" = relative error <= 1e-2 against a converged
@@ -711,7 +732,8 @@ def run_ours(args):
                        "l2": "working set (>2 GB) larger than the 126 MB L2; no flush needed",
                        "parallelism": f"replicas{world}"},
             "device_ms_solver_stream": dev_ms, "gen_seconds": gen_s,
-            "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "clocks": clocks,
+            "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "e2e_pinned": e2e_pinned,
+            "clocks": clocks,
             "gpu_launches": launches, "time_to_tolerance": ttt, "big": big, "em_block": em,
             "precision64": p64,
         }
@@ -728,8 +750,9 @@ def em_iteration(device: int = 0, n: int = 128, m: int = 1000, n_poses: int = 20
     synthetic particle set: M-step (the solver) -> E-step with V from the
     resident result -> backprojection into the resident accumulator, images
     uploaded once (cm_set_particles). Per-stage seconds (host clock around
-    synchronised calls; the posterior matrix crosses to the host and back as
-    entry lists, everything else stays on the device)."""
+    synchronised calls; the posteriors cross to the host as sparse PosteriorRow
+    lists (cm_estep_sparse) and back as entry lists, everything else stays on
+    the device)."""
     import torch
 
     import paper_1905_13408_b200 as cm
@@ -753,9 +776,9 @@ def em_iteration(device: int = 0, n: int = 128, m: int = 1000, n_poses: int = 20
         ctx.solve(cfg)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        post = cm.e_step(ctx, inp, sigma2, resident_images=True)
+        rows = cm.e_step(ctx, inp, sigma2, resident_images=True, sparse=True)
         t2 = time.perf_counter()
-        inp.entry_particle, inp.entry_candidate, inp.entry_posterior = cm.posterior_entries(post)
+        inp.entry_particle, inp.entry_candidate, inp.entry_posterior = cm.sparse_entries(*rows)
         cm.backproject_into(ctx, inp, download=False, resident_images=True)
         torch.cuda.synchronize()
         t3 = time.perf_counter()

@@ -192,6 +192,16 @@ typedef struct {
     const double* volume;       /* FourierVolume [n^3] complex interleaved, or NULL */
 } cm_estep_input;
 int cm_estep(cm_ctx* ctx, const cm_estep_input* in, double* posterior);
+/* The same posteriors as sparse PosteriorRow lists (estep.hpp:30-34, the
+ * reference's e_step return value): row i's entries are candidate[k],
+ * weight[k] for row_ptr[i] <= k < row_ptr[i+1], in ascending candidate order.
+ * row_ptr has n_images + 1 slots; candidate / weight hold `capacity` entries.
+ * *nnz = entries written, or, with CM_ERR_INVALID_ARGUMENT when capacity is
+ * too small, the entries needed (call again with that capacity). Particles
+ * are processed in device-memory-bounded batches (CM_ESTEP_BATCH_BYTES,
+ * default 1 GiB), so the posterior never exists densely anywhere. */
+int cm_estep_sparse(cm_ctx* ctx, const cm_estep_input* in, long long* row_ptr, int* candidate,
+                    double* weight, long long capacity, long long* nnz);
 
 /* Particle images resident on the device across EM iterations: after
  * cm_set_particles, a cm_bp_input / cm_estep_input with images == NULL (and

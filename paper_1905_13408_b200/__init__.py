@@ -16,6 +16,7 @@ from .regularizer import (  # noqa: F401
 from . import slab  # noqa: F401,E402
 from .backproject import (  # noqa: F401,E402
     BackprojectInput, backproject_accumulate, backproject_into, e_step, posterior_entries,
+    sparse_entries,
     set_particles,
 )
 from .slab import SlabContext, SlabPlan  # noqa: F401,E402

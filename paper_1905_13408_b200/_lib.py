@@ -78,6 +78,7 @@ def load() -> C.CDLL:
         "cm_write_volume_mrc": [P, C.c_char_p, C.c_double],
         "cm_backproject": [P, P, P, P],
         "cm_estep": [P, P, P],
+        "cm_estep_sparse": [P, P, P, P, P, C.c_longlong, C.POINTER(C.c_longlong)],
         "cm_set_particles": [P, C.c_int, P, P],
         "cm_set_profiling": [P, C.c_int],
         "cm_get_profile": [P, _dp, _ip],

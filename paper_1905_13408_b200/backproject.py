@@ -143,12 +143,14 @@ class cm_estep_input(C.Structure):
 
 
 def e_step(ctx: Context, inp: BackprojectInput, sigma2, volume=None,
-           prune_floor: float = 1e-8, resident_images: bool = False) -> np.ndarray:
+           prune_floor: float = 1e-8, resident_images: bool = False, sparse: bool = False):
     """e_step (estep.hpp:44-54) on the device -> dense posterior
     [images][poses * shifts] (PosteriorRow entries at their candidate index,
-    exact zeros elsewhere). The particles, grid and kernel come from `inp`
-    (its entry arrays are ignored); volume None: V = fft3_centered of ctx's
-    resident solve result, never leaving the device."""
+    exact zeros elsewhere), or with sparse=True the PosteriorRow lists as
+    (row_ptr [images+1], candidate, weight) (cm_estep_sparse: never dense).
+    The particles, grid and kernel come from `inp` (its entry arrays are
+    ignored); volume None: V = fft3_centered of ctx's resident solve result,
+    never leaving the device."""
     n = ctx.n
     if inp.side_n != n:
         from .regularizer import GridMismatch
@@ -165,9 +167,31 @@ def e_step(ctx: Context, inp: BackprojectInput, sigma2, volume=None,
                        int(inp.poses.shape[0]), d(inp.poses), int(inp.shifts.shape[0]),
                        d(inp.shifts), int(inp.kernel_kind), float(inp.bandwidth),
                        float(inp.radius_cutoff), int(s2.size), d(s2), float(prune_floor), d(V))
-    out = np.zeros((inp.images.shape[0], inp.poses.shape[0] * inp.shifts.shape[0]))
+    m = int(inp.images.shape[0])
+    if sparse:
+        row_ptr = np.zeros(m + 1, np.int64)
+        cap = max(1, m * min(64, inp.poses.shape[0] * inp.shifts.shape[0]))
+        while True:
+            cand = np.empty(cap, np.int32)
+            w = np.empty(cap, np.float64)
+            nnz = C.c_longlong(0)
+            rc = ctx.lib.cm_estep_sparse(ctx.ptr, C.byref(c), row_ptr.ctypes.data, cand.ctypes.data,
+                                         w.ctypes.data, cap, C.byref(nnz))
+            if rc != 0 and nnz.value > cap:  # capacity too small: the call says how many
+                cap = int(nnz.value)
+                continue
+            _check(rc)
+            return row_ptr, cand[: nnz.value].copy(), w[: nnz.value].copy()
+    out = np.zeros((m, inp.poses.shape[0] * inp.shifts.shape[0]))
     _check(ctx.lib.cm_estep(ctx.ptr, C.byref(c), out.ctypes.data))
     return out
+
+
+def sparse_entries(row_ptr, cand, weight):
+    """cm_estep_sparse's PosteriorRow lists -> the flat (particle, candidate,
+    weight) entry arrays of cm_bp_input."""
+    part = np.repeat(np.arange(row_ptr.size - 1, dtype=np.int64), np.diff(row_ptr))
+    return part, cand.astype(np.uint32), weight
 
 
 def posterior_entries(dense: np.ndarray):

@@ -275,7 +275,29 @@ int cm_estep(cm_ctx* ctx, const cm_estep_input* in, double* posterior) {
         vdev = ctx->impl->result_spectrum_device(1);
         if (!vdev) return fail(CM_ERR_STATE, "e_step: no volume given and no solver result resident");
     }
-    return estep_run(ctx->n, in, in->volume, vdev, posterior, ctx->impl->stream, &ctx->particles);
+    EsSink sink;
+    sink.dense = posterior;
+    return estep_run(ctx->n, in, in->volume, vdev, sink, ctx->impl->stream, &ctx->particles);
+}
+
+int cm_estep_sparse(cm_ctx* ctx, const cm_estep_input* in, long long* row_ptr, int* candidate,
+                    double* weight, long long capacity, long long* nnz) {
+    CTX_GUARD(ctx);
+    if (!in || !row_ptr || !nnz || (capacity > 0 && (!candidate || !weight)))
+        return fail(CM_ERR_INVALID_ARGUMENT, "e_step: null argument");
+    const double* vdev = nullptr;
+    if (!in->volume) {
+        vdev = ctx->impl->result_spectrum_device(1);
+        if (!vdev) return fail(CM_ERR_STATE, "e_step: no volume given and no solver result resident");
+    }
+    EsSink sink;
+    sink.row_ptr = row_ptr;
+    sink.cand = candidate;
+    sink.weight = weight;
+    sink.cap = capacity;
+    const int rc = estep_run(ctx->n, in, in->volume, vdev, sink, ctx->impl->stream, &ctx->particles);
+    *nnz = sink.nnz;
+    return rc;
 }
 
 int cm_set_particles(cm_ctx* ctx, int n_images, const double* images, const double* image_params) {

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -319,9 +320,68 @@ __global__ void __launch_bounds__(ES_NT) es_softmax_kernel(EsDev p, double* post
     for (int c = threadIdx.x; c < nc; c += ES_NT) o[c] = kept > 0.0 ? o[c] / kept : 0.0;
 }
 
+// nonzero entries per posterior row (one CTA per particle)
+__global__ void __launch_bounds__(ES_NT) es_count_kernel(const double* post, int nc, int* cnt) {
+    __shared__ double red[ES_NT / 32];
+    const double* o = post + (size_t)blockIdx.x * nc;
+    double v[1] = {0.0};
+    for (int c = threadIdx.x; c < nc; c += ES_NT) v[0] += o[c] != 0.0 ? 1.0 : 0.0;
+    es_block_sum<1>(v, red);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = (int)v[0];
+}
+
+// PosteriorRow entries (estep.hpp:30-34) in ascending candidate order, as the
+// reference pushes them (estep.cpp:257-263): block-wide prefix sums per chunk
+__global__ void __launch_bounds__(ES_NT) es_compact_kernel(const double* post, int nc,
+                                                           const long long* off, int* cand,
+                                                           double* wout) {
+    __shared__ int wsum[ES_NT / 32];
+    __shared__ int base_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double* o = post + (size_t)blockIdx.x * nc;
+    long long base = off[blockIdx.x];
+    for (int c0 = 0; c0 < nc; c0 += ES_NT) {
+        const int c = c0 + threadIdx.x;
+        const double v = c < nc ? o[c] : 0.0;
+        const int f = v != 0.0 ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int pre = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) wsum[w] = __popc(bal);
+        __syncthreads();
+        int wpre = 0, tot = 0;
+        for (int k = 0; k < ES_NT / 32; ++k) {
+            wpre += k < w ? wsum[k] : 0;
+            tot += wsum[k];
+        }
+        if (f) {
+            cand[base + wpre + pre] = c;
+            wout[base + wpre + pre] = v;
+        }
+        if (threadIdx.x == 0) base_s = tot;
+        __syncthreads();
+        base += base_s;
+        __syncthreads();
+    }
+}
+
+// Where a batch's posterior rows go: the dense host matrix [np][nc], or the
+// sparse PosteriorRow lists (row_ptr [np+1], candidate / weight of capacity cap)
+struct EsSink {
+    double* dense = nullptr;
+    long long* row_ptr = nullptr;
+    int* cand = nullptr;
+    double* weight = nullptr;
+    long long cap = 0;
+    long long nnz = 0;      // entries so far (required count when over capacity)
+    bool overflow = false;
+};
+
 // Host side. V: device FourierVolume (host upload or the resident spectrum).
+// Particles are processed in batches sized to CM_ESTEP_BATCH_BYTES of device
+// scratch (default 1 GiB): the per-particle tables, residuals and posterior
+// rows of one batch; the slices and shift phases are built once per call.
 inline int estep_run(int n, const cm_estep_input* in, const double* V_host, const double* V_dev,
-                     double* post_host, cudaStream_t st, const ParticleDev* resident = nullptr) {
+                     EsSink& sink, cudaStream_t st, const ParticleDev* resident = nullptr) {
     if (in->n_poses <= 0 || in->n_shifts <= 0)
         return fail(CM_ERR_INVALID_ARGUMENT, "e_step: empty orientation grid");
     if (in->kernel_kind != 0 && in->kernel_kind != 1)
@@ -337,6 +397,7 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
     for (int s = 0; s < in->n_shifts; ++s)
         zero_shift |= in->shifts[2 * s] == 0 && in->shifts[2 * s + 1] == 0;
     if (!zero_shift) return fail(CM_ERR_INVALID_ARGUMENT, "e_step: orientation grid lacks the zero shift");
+    if (sink.row_ptr) sink.row_ptr[0] = 0;
     if (in->n_images == 0) return CM_OK;
     // build_comp_tables (estep.cpp:26-40) with effective_cutoff (:14-17)
     const double nyq = double(n / 2);
@@ -356,25 +417,19 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
     const int ncomp = (int)comps.size(), np = in->n_images, npose = in->n_poses, ns = in->n_shifts;
     const size_t L = (size_t)n * n * n, nc = (size_t)npose * ns;
 
+    // batch size: device bytes per particle of the batch-local arrays
+    size_t budget = size_t(1) << 30;
+    if (const char* e = std::getenv("CM_ESTEP_BATCH_BYTES")) budget = std::max<size_t>(1, std::strtoull(e, nullptr, 10));
+    const size_t per_part = 8 * (4 * (size_t)ncomp + 2 + 2 * (size_t)npose + 2 * nc) +
+                            (host_images ? 16 * (size_t)n * n + 48 : 0) + 16;
+    const int nb = (int)std::max<size_t>(1, std::min<size_t>((size_t)np, budget / per_part));
+
     BpBuffers B;
-    EsDev p{};
-    double2* img = nullptr;
     double2* Vd = nullptr;
-    double *ip = nullptr, *dm = nullptr, *isg = nullptr, *phr = nullptr, *phi = nullptr;
+    double *dm = nullptr, *isg = nullptr, *phr = nullptr, *phi = nullptr;
     int2 *cmp = nullptr, *shf = nullptr;
     double2* slice = nullptr;
-    double *p1r = nullptr, *p1i = nullptr, *p2 = nullptr, *pab = nullptr, *A = nullptr, *R0 = nullptr,
-           *LB = nullptr, *U = nullptr, *res = nullptr, *post = nullptr;
-    if (V_host) {
-        CKS(B.put(&Vd, reinterpret_cast<const double2*>(V_host), L, st));
-    }
-    if (host_images) {
-        CKS(B.put(&img, reinterpret_cast<const double2*>(in->images), (size_t)np * n * n, st));
-        CKS(B.put(&ip, in->image_params, (size_t)np * 6, st));
-    } else {
-        img = resident->img;
-        ip = resident->ip;
-    }
+    if (V_host) CKS(B.put(&Vd, reinterpret_cast<const double2*>(V_host), L, st));
     CKS(B.put(&dm, mats.data(), mats.size(), st));
     CKS(B.put(&cmp, comps.data(), comps.size(), st));
     CKS(B.put(&isg, invsig.data(), invsig.size(), st));
@@ -382,16 +437,31 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
     CKS(B.put(&phr, (const double*)nullptr, (size_t)ns * ncomp, st));
     CKS(B.put(&phi, (const double*)nullptr, (size_t)ns * ncomp, st));
     CKS(B.put(&slice, (const double2*)nullptr, (size_t)npose * ncomp, st));
-    for (double** q : {&p1r, &p1i, &p2, &pab}) CKS(B.put(q, (const double*)nullptr, (size_t)np * ncomp, st));
-    CKS(B.put(&A, (const double*)nullptr, (size_t)np, st));
-    CKS(B.put(&U, (const double*)nullptr, (size_t)np, st));
-    CKS(B.put(&R0, (const double*)nullptr, (size_t)np * npose, st));
-    CKS(B.put(&LB, (const double*)nullptr, (size_t)np * npose, st));
-    CKS(B.put(&res, (const double*)nullptr, (size_t)np * nc, st));
-    CKS(B.put(&post, (const double*)nullptr, (size_t)np * nc, st));
-    p = EsDev{V_host ? Vd : reinterpret_cast<const double2*>(V_dev), img, ip, dm, cmp, isg, phr, phi, slice,
-              p1r, p1i, p2, pab, A, R0, LB, U, res, n, ncomp, npose, ns, np,
-              2.0 * std::log(1.0 / in->prune_floor), in->prune_floor, in->bandwidth};
+    // batch-local arrays
+    double2* img_b = nullptr;
+    double* ip_b = nullptr;
+    if (host_images) {
+        CKS(B.put(&img_b, (const double2*)nullptr, (size_t)nb * n * n, st));
+        CKS(B.put(&ip_b, (const double*)nullptr, (size_t)nb * 6, st));
+    }
+    double *p1r = nullptr, *p1i = nullptr, *p2 = nullptr, *pab = nullptr, *A = nullptr, *R0 = nullptr,
+           *LB = nullptr, *U = nullptr, *res = nullptr, *post = nullptr;
+    for (double** q : {&p1r, &p1i, &p2, &pab}) CKS(B.put(q, (const double*)nullptr, (size_t)nb * ncomp, st));
+    CKS(B.put(&A, (const double*)nullptr, (size_t)nb, st));
+    CKS(B.put(&U, (const double*)nullptr, (size_t)nb, st));
+    CKS(B.put(&R0, (const double*)nullptr, (size_t)nb * npose, st));
+    CKS(B.put(&LB, (const double*)nullptr, (size_t)nb * npose, st));
+    CKS(B.put(&res, (const double*)nullptr, (size_t)nb * nc, st));
+    CKS(B.put(&post, (const double*)nullptr, (size_t)nb * nc, st));
+    int* cnt = nullptr;
+    long long* offd = nullptr;
+    if (sink.row_ptr) {
+        CKS(B.put(&cnt, (const int*)nullptr, (size_t)nb, st));
+        CKS(B.put(&offd, (const long long*)nullptr, (size_t)nb, st));
+    }
+    EsDev p{V_host ? Vd : reinterpret_cast<const double2*>(V_dev), nullptr, nullptr, dm, cmp, isg, phr, phi,
+            slice, p1r, p1i, p2, pab, A, R0, LB, U, res, n, ncomp, npose, ns, 0,
+            2.0 * std::log(1.0 / in->prune_floor), in->prune_floor, in->bandwidth};
     // pass 2 skips the zero shift: its residual is pass 1's R0 (the same sums)
     std::vector<int> sidx;
     int zsh = -1;
@@ -412,15 +482,77 @@ inline int estep_run(int n, const cm_estep_input* in, const double* V_host, cons
         else
             es_slice_kernel<1><<<blocks((long long)npose * ncomp), ES_NT, 0, st>>>(p);
     }
-    es_ptab_kernel<<<np, ES_NT, 0, st>>>(p);
-    es_pass1_kernel<<<(unsigned)((size_t)np * npose), ES_NT, 0, st>>>(p);
-    es_min_kernel<<<np, ES_NT, 0, st>>>(p);
-    es_pass2_kernel<<<(unsigned)((size_t)np * ((npose + ES_PG - 1) / ES_PG)), ES_NT, 0, st>>>(p);
-    es_softmax_kernel<<<np, ES_NT, 0, st>>>(p, post);
-    if (cudaGetLastError() != cudaSuccess) return fail(CM_ERR_CUDA, "e_step: launch failed");
-    if (cudaMemcpyAsync(post_host, post, sizeof(double) * np * nc, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-        return fail(CM_ERR_CUDA, "e_step: kernel failed");
+    std::vector<int> hcnt;
+    std::vector<long long> hoff;
+    int* dcand = nullptr;
+    double* dw = nullptr;
+    size_t dcap = 0;
+    for (int b0 = 0; b0 < np; b0 += nb) {
+        const int m = std::min(nb, np - b0);
+        if (host_images) {
+            if (cudaMemcpyAsync(img_b, in->images + (size_t)b0 * n * n * 2, sizeof(double2) * (size_t)m * n * n,
+                                cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                cudaMemcpyAsync(ip_b, in->image_params + (size_t)b0 * 6, sizeof(double) * (size_t)m * 6,
+                                cudaMemcpyHostToDevice, st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "e_step: image upload failed");
+            p.img = img_b;
+            p.ip = ip_b;
+        } else {
+            p.img = resident->img + (size_t)b0 * n * n;
+            p.ip = resident->ip + (size_t)b0 * 6;
+        }
+        p.npart = m;
+        es_ptab_kernel<<<m, ES_NT, 0, st>>>(p);
+        es_pass1_kernel<<<(unsigned)((size_t)m * npose), ES_NT, 0, st>>>(p);
+        es_min_kernel<<<m, ES_NT, 0, st>>>(p);
+        es_pass2_kernel<<<(unsigned)((size_t)m * ((npose + ES_PG - 1) / ES_PG)), ES_NT, 0, st>>>(p);
+        es_softmax_kernel<<<m, ES_NT, 0, st>>>(p, post);
+        if (cudaGetLastError() != cudaSuccess) return fail(CM_ERR_CUDA, "e_step: launch failed");
+        if (sink.dense) {
+            if (cudaMemcpyAsync(sink.dense + (size_t)b0 * nc, post, sizeof(double) * m * nc,
+                                cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "e_step: download failed");
+            continue;
+        }
+        // sparse: per-row counts -> offsets -> ordered compaction
+        es_count_kernel<<<m, ES_NT, 0, st>>>(post, (int)nc, cnt);
+        hcnt.resize(m);
+        hoff.resize(m);
+        if (cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return fail(CM_ERR_CUDA, "e_step: kernel failed");
+        long long tot = 0;
+        for (int q = 0; q < m; ++q) {
+            hoff[q] = tot;
+            tot += hcnt[q];
+            sink.row_ptr[b0 + q + 1] = sink.nnz + tot;
+        }
+        if (sink.overflow || sink.nnz + tot > sink.cap) {
+            sink.overflow = true;
+            sink.nnz += tot;
+            continue;
+        }
+        if ((size_t)tot > dcap) {
+            dcap = std::max<size_t>((size_t)tot, 2 * dcap);
+            CKS(B.put(&dcand, (const int*)nullptr, dcap, st));
+            CKS(B.put(&dw, (const double*)nullptr, dcap, st));
+        }
+        if (tot > 0) {
+            if (cudaMemcpyAsync(offd, hoff.data(), sizeof(long long) * m, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "e_step: upload failed");
+            es_compact_kernel<<<m, ES_NT, 0, st>>>(post, (int)nc, offd, dcand, dw);
+            if (cudaMemcpyAsync(sink.cand + sink.nnz, dcand, sizeof(int) * tot, cudaMemcpyDeviceToHost, st) !=
+                    cudaSuccess ||
+                cudaMemcpyAsync(sink.weight + sink.nnz, dw, sizeof(double) * tot, cudaMemcpyDeviceToHost, st) !=
+                    cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "e_step: download failed");
+        }
+        sink.nnz += tot;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(CM_ERR_CUDA, "e_step: kernel failed");
+    if (sink.overflow)
+        return fail(CM_ERR_INVALID_ARGUMENT, "e_step: entry capacity too small (*nnz holds the entries needed)");
     return CM_OK;
 }
 

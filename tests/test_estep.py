@@ -92,6 +92,36 @@ def test_matches_reference_production_grids(n, m, npose, r, scale, floor):
 
 @pytest.mark.gpu
 @needs_ref
+@pytest.mark.parametrize("batch_bytes", [None, "200000"])
+def test_sparse_rows_match_reference_in_batches(monkeypatch, batch_bytes):
+    """cm_estep_sparse: the PosteriorRow lists (ascending candidate order, as
+    estep.cpp:257-263 pushes them) equal the reference's rows; a small
+    CM_ESTEP_BATCH_BYTES forces many particle batches and a capacity retry."""
+    if batch_bytes:
+        monkeypatch.setenv("CM_ESTEP_BATCH_BYTES", batch_bytes)
+    R = Reference()
+    inp, V, s2 = problem(32, 23, GAUSSIAN, -1.0, 0.05, 41, True, 1, n_poses=37)
+    rc, want = R.estep(inp, V, s2)
+    assert rc == 0, R.last_error()
+    ctx = cm.Context(32)
+    row_ptr, cand, w = cm.e_step(ctx, inp, s2, volume=V, sparse=True)
+    dense = cm.e_step(ctx, inp, s2, volume=V)
+    ctx.close()
+    assert row_ptr[0] == 0 and row_ptr[-1] == cand.size
+    for i in range(want.shape[0]):
+        c = cand[row_ptr[i]:row_ptr[i + 1]]
+        assert np.all(np.diff(c) > 0)
+        np.testing.assert_array_equal(c, np.nonzero(want[i])[0])
+        assert np.abs(w[row_ptr[i]:row_ptr[i + 1]] - want[i, c]).max() <= 1e-10
+    np.testing.assert_array_equal(dense != 0, want != 0)
+    ep, ec, ew = cm.sparse_entries(row_ptr, cand, w)
+    dp, dc, dw = cm.posterior_entries(dense)
+    np.testing.assert_array_equal(ep, dp)
+    np.testing.assert_array_equal(ec, dc)
+
+
+@pytest.mark.gpu
+@needs_ref
 def test_prune_floor_above_every_candidate_gives_empty_rows():
     """prune_floor larger than the best candidate's posterior: the reference
     pushes no entry (estep.cpp:257-263), the device writes zeros (not 0/0)."""
