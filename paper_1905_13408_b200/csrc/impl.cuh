@@ -45,6 +45,7 @@ int fail(int code, const std::string& msg);
 
 } // namespace cm
 #include "ypass_tma.cuh"
+#include "k1f.cuh"
 namespace cm {
 
 #define CK(call)                                                                         \
@@ -400,6 +401,10 @@ struct Impl final : ImplBase {
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
+    // fused K1 (k1f.cuh): x C2R + stencil + x R2C in one cluster kernel; opt-in CM_K1F=1
+    static constexpr bool K1F = std::is_same<R, float>::value && K1Geo<N>::OK;
+    bool use_k1f = false;
+    int k1f_grid_ = 0;
     // TMA-fed persistent y pass (ypass_tma.cuh): fp32, N in {256, 512}; CM_YT=0 -> ypass
     static constexpr bool YT = std::is_same<R, float>::value && YtGeo<N>::OK;
     bool use_yt = false;
@@ -615,6 +620,21 @@ struct Impl final : ImplBase {
             s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
         }
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
+        if constexpr (K1F) {
+            // opt-in (CM_K1F=1): measured 1.40 ms per 512^3 sweep against 0.96 ms for the
+            // three separate kernels (one line per CTA-plane leaves the
+            // warp-specialised transforms latency-bound)
+            const char* e = std::getenv("CM_K1F");
+            use_k1f = e && e[0] == '1';
+            CK(k1f_prepare<N>());
+            k1f_grid_ = k1f_grid<N>(stream);
+            if (const char* g = std::getenv("CM_K1F_CLUSTERS"))  // experiments: fixed cluster count
+                k1f_grid_ = std::max(1, std::min(std::atoi(g), K1Geo<N>::NTILES)) * K1Geo<N>::NCL;
+            if (std::getenv("CM_K1F_DEBUG"))
+                std::fprintf(stderr, "k1f: N=%d grid=%d CTAs (%d clusters of %d), smem=%zu\n", N, k1f_grid_,
+                             k1f_grid_ / K1Geo<N>::NCL, K1Geo<N>::NCL, K1Geo<N>::SMEM);
+            if (k1f_grid_ <= 0) use_k1f = false;
+        }
         if constexpr (YT) {
             using YG_ = YtGeo<N>;
             const char* e = std::getenv("CM_YT");
@@ -958,7 +978,8 @@ struct Impl final : ImplBase {
             (void)mid;
             // K1a: x-line C2R -> data gradient (real space, / L); fused: the y
             // inverse of the same planes ran in the same kernel (mark 2 -> 3 is empty)
-            if (!use_fused) CKS(launch_xfft(0, gbuf, &st->done));
+            const bool k1f = K1F && use_k1f && !use_fused;
+            if (!use_fused && !k1f) CKS(launch_xfft(0, gbuf, &st->done));
             CKS(mark(3));
             // K1b: stencil sweep
             StencilParams<R> p{};
@@ -1006,15 +1027,23 @@ struct Impl final : ImplBase {
                 p.wl1src = wfixed;
             }
             const bool use_s2 = S2 && std::getenv("CM_STENCIL1") == nullptr;
+            if constexpr (K1F) {
+                if (k1f) {
+                    const int xi = fista ? 3 + g % 2 : g % 3;
+                    const int pi = fista ? 0 : (g + 2) % 3;
+                    CK(k1f_launch<N>(p, reinterpret_cast<float2*>(S), reinterpret_cast<const float2*>(twN),
+                                     k1f_grid_, stream, tm2_x[xi], tm2_p[pi], tm2_a));
+                }
+            }
             if constexpr (S2) {
-                if (use_s2) {
+                if (use_s2 && !k1f) {
                     const int xi = fista ? 3 + g % 2 : g % 3;
                     const int pi = fista ? 0 : (g + 2) % 3;
                     CK(stencil2_launch<N>(p, s2_grid, stream, tm2_x[xi], tm2_p[pi], tm2_g, tm2_a,
                                           use_pdl));
                 }
             }
-            if (!use_s2)
+            if (!use_s2 && !k1f)
                 stencil_kernel<R, N><<<sweep_grid, StGeo<R, N>::NT, StGeo<R, N>::SMEM, stream>>>(
                     p, *tmx, *tmp, tm_gt, tm_at);
             CK(cudaGetLastError());
@@ -1023,7 +1052,7 @@ struct Impl final : ImplBase {
             FinParams f{};
             f.st = st;
             f.part1 = need_part1 ? part1 : nullptr;
-            f.nb1 = use_s2 ? s2_grid : sweep_grid;  // partial slots of the stencil launched
+            f.nb1 = k1f ? k1f_grid_ : use_s2 ? s2_grid : sweep_grid;  // partial slots of the sweep
             f.part3 = audit ? part3 : nullptr;
             f.nb3 = NB3;
             f.trace = want_trace ? trace_d : nullptr;
@@ -1036,7 +1065,7 @@ struct Impl final : ImplBase {
             CKS(mark(5));
             // K1c: x-line R2C of the new iterate (FISTA: of y_{k+1}); fused: + y forward
             if (use_fused) CKS(launch_fused(1, spec_src, &st->done_y));
-            else CKS(launch_xfft(1, spec_src, &st->done_y));
+            else if (!k1f) CKS(launch_xfft(1, spec_src, &st->done_y));  // k1f: done in the sweep
             CKS(mark(6));
             return CM_OK;
         };

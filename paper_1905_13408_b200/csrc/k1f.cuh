@@ -44,6 +44,12 @@ namespace cm {
 #ifndef CM_K1F_KC
 #define CM_K1F_KC 32
 #endif
+#ifndef CM_K1F_NFFT
+#define CM_K1F_NFFT 2  // warps per transform direction (planes alternate between them)
+#endif
+#ifndef CM_K1F_MINB
+#define CM_K1F_MINB 2
+#endif
 
 template <int N> struct K1Geo {
     static constexpr bool OK = (N == 256 || N == 512);
@@ -51,8 +57,9 @@ template <int N> struct K1Geo {
     static constexpr int NCL = N / CI;             // CTAs per cluster (full x lines)
     static constexpr int LPC = TJ / NCL;           // FFT lines per CTA per plane
     static constexpr int NWS = TJ + 1;             // stencil warps (+ halo row)
-    static constexpr int WC2R = NWS, WR2C = NWS + 1;
-    static constexpr int NT = (NWS + 2) * 32;
+    static constexpr int NF = CM_K1F_NFFT;         // C2R warps, then NF R2C warps
+    static constexpr int WC2R = NWS, WR2C = NWS + NF;
+    static constexpr int NT = (NWS + 2 * NF) * 32;
     static constexpr int NST = NWS * 32;           // threads of the stencil named barrier
     static constexpr int Nh = N / 2;
     static constexpr int E = Nh / 32;              // line elements per lane (one warp per line)
@@ -72,7 +79,7 @@ template <int N> struct K1Geo {
     static constexpr size_t OFF_L = OFF_G + NG * GSLOT;
     static constexpr uint32_t LSLOT = (uint32_t)LPC * Nh * 8;
     // assembled real lines for the R2C warp, NLN planes (LPC lines of N floats)
-    static constexpr int NLN = 2;
+    static constexpr int NLN = 4;
     static constexpr size_t OFF_LN = OFF_L + NL * (size_t)LSLOT;
     static constexpr uint32_t LNSLOT = (uint32_t)LPC * N * 4;
     // s ring, FFT exchange buffers, twiddles, reductions, barriers
@@ -80,14 +87,16 @@ template <int N> struct K1Geo {
     static constexpr size_t SROW3 = (size_t)(TJ + 1) * SW;
     static constexpr size_t OFF_S = al(OFF_LN + NLN * (size_t)LNSLOT);
     static constexpr int PADX = (Nh + (Nh >> 3) + 2) / 2 * 2;
-    static constexpr size_t OFF_X = al(OFF_S + 3 * SROW3 * 4);   // [2 warps][PADX] complex
-    static constexpr size_t OFF_TW = OFF_X + 2 * (size_t)PADX * 8;
+    static constexpr size_t OFF_X = al(OFF_S + 3 * SROW3 * 4);   // [2 NF warps][PADX] complex
+    static constexpr size_t OFF_TW = OFF_X + 2 * NF * (size_t)PADX * 8;
     static constexpr size_t OFF_RED = al(OFF_TW + (size_t)N * 8);
     static constexpr size_t OFF_BAR = OFF_RED + 8 * NP1 * 8;
-    // barriers: stage[4] g_full[4] g_empty[4] l_full[4] ln_full[2] ln_empty[2]
-    static constexpr int B_STAGE = 0, B_GF = 4, B_GE = 8, B_LF = 12, B_LNF = 16, B_LNE = 18, NBAR = 20;
+    // barriers: stage[4] g_full[4] g_empty[4] l_full[4] ln_full[NLN] ln_empty[NLN]
+    static constexpr int B_STAGE = 0, B_GF = 4, B_GE = 8, B_LF = 12, B_LNF = 16, B_LNE = 16 + NLN,
+                         NBAR = 16 + 2 * NLN;
     static constexpr size_t SMEM = OFF_BAR + NBAR * 8;
     static constexpr int NTJ = N / TJ, NTK = N / KC;
+    static_assert(NL % NF == 0 && NLN % NF == 0 && NG % NF == 0, "rings are split by plane parity");
     static constexpr int NTILES = NTJ * NTK;       // cluster tiles (j block, k block)
 };
 
@@ -119,23 +128,56 @@ __device__ __forceinline__ void st_async_v2(uint32_t raddr, float2 v, uint32_t r
                  "f"(v.x), "f"(v.y), "r"(rbar)
                  : "memory");
 }
-// release arrival on a (possibly remote) barrier of the cluster
+// relaxed arrival on a (possibly remote) barrier of the cluster. The arrivals
+// only say "this slot's data has been consumed" (its shared-memory reads have
+// returned and fed arithmetic before the arrive issues); a release here would
+// be a cluster-scope fence that waits for the thread's outstanding HBM stores
+// (ncu: `membar` stalls dominated the first version of this kernel).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t rbar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
 }
 #ifndef CM_K1F_SPIN_TRAP
-#define CM_K1F_SPIN_TRAP (1u << 26)  // a wait this long is a bug: trap instead of hanging the GPU
+#define CM_K1F_SPIN_TRAP (1u << 30)  // a wait this long is a bug: trap instead of hanging the GPU
+#endif
+// Waits on barriers completed from OTHER CTAs of the cluster (st.async tx,
+// remote arrivals). A blocking try_wait may suspend the warp for up to a
+// system-dependent time and is not promptly woken by remote completions, so
+// these waits poll: test_wait (CM_K1F_WAIT 2, default) or try_wait with a
+// short suspend-time hint (1) or the default try_wait (0).
+#ifndef CM_K1F_WAIT
+#define CM_K1F_WAIT 2
+#endif
+#ifndef CM_K1F_HINT
+#define CM_K1F_HINT 32
 #endif
 __device__ __forceinline__ void mbar_wait_cl(uint32_t bar, uint32_t parity) {
     uint32_t ok = 0, spins = 0;
     do {
+#if CM_K1F_WAIT == 2
         asm volatile(
             "{\n.reg .pred P1;\n"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
             "selp.u32 %0, 1, 0, P1;\n}\n"
             : "=r"(ok)
             : "r"(bar), "r"(parity)
             : "memory");
+#elif CM_K1F_WAIT == 1
+        asm volatile(
+            "{\n.reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+            "selp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity), "r"(CM_K1F_HINT)
+            : "memory");
+#else
+        asm volatile(
+            "{\n.reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+#endif
         if (!ok && ++spins > CM_K1F_SPIN_TRAP) __trap();
     } while (!ok);
 }
@@ -149,8 +191,22 @@ __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+#ifdef CM_K1F_TRACE
+__device__ unsigned long long* g_k1f_trace;
+#define K1T(ev, uu)                                                                            \
+    do {                                                                                       \
+        if (lane == 0 && blockIdx.x < (unsigned)NCL && (uu) < 64) {                            \
+            unsigned long long t_;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+            g_k1f_trace[((size_t)blockIdx.x * 10 + (ev)) * 64 + (uu)] = t_;                    \
+        }                                                                                      \
+    } while (0)
+#else
+#define K1T(ev, uu) do {} while (0)
+#endif
+
 template <int N, int F>
-__global__ void __launch_bounds__(K1Geo<N>::NT, 3)
+__global__ void __launch_bounds__(K1Geo<N>::NT, CM_K1F_MINB)
 k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restrict__ twN, float invL,
            const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmp,
            const __grid_constant__ CUtensorMap tma) {
@@ -202,10 +258,11 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
         k0 = (tile / G::NTJ) * KC;
     };
 
-    if (w == G::WC2R) {
+    if (w >= G::WC2R && w < G::WC2R + G::NF) {
+        const int f = w - G::WC2R;  // this warp's planes: u = f (mod NF)
         // ============================ C2R warp ============================
         const uint32_t lbase = smem_s + (uint32_t)G::OFF_L;
-        C* xb = reinterpret_cast<C*>(smem_raw + G::OFF_X);
+        C* xb = reinterpret_cast<C*>(smem_raw + G::OFF_X) + f * G::PADX;
         const PadAddr pad{};
         const WarpSync wsync{};
         auto issue_line = [&](int u) {  // spectrum rows of plane u -> line slot u % NL
@@ -220,12 +277,13 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
             bulk_load_s(lbase + (uint32_t)sl * G::LSLOT, src, G::LSLOT, B(G::B_LF + sl));
         };
         if (lane == 0)
-            for (int u = 0; u < G::NL; ++u) issue_line(u);
-        for (int u = 0;; ++u) {
+            for (int u = f; u < G::NL; u += G::NF) issue_line(u);
+        for (int u = f;; u += G::NF) {
             const int ord = u / KC, tile = tile_of(ord);
             if (tile >= ntiles_c) break;
             const int sl = u % G::NL;
             mbar_wait_cl(B(G::B_LF + sl), (uint32_t)(u / G::NL) & 1u);
+            K1T(4, u);
             const C* lsrc = reinterpret_cast<const C*>(smem_raw + G::OFF_L + (size_t)sl * G::LSLOT);
             C v[LPC][E];
 #pragma unroll
@@ -262,7 +320,9 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                 __syncwarp();
             }
             // g chunks to every CTA of the cluster once its G slot is free
+            K1T(5, u);
             mbar_wait_cl(B(G::B_GE + gs), ((uint32_t)(u / G::NG) & 1u) ^ 1u);
+            K1T(6, u);
 #pragma unroll
             for (int l = 0; l < LPC; ++l) {
                 const int row = (int)crank * LPC + l;
@@ -278,12 +338,13 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                 }
             }
         }
-    } else if (w == G::WR2C) {
+    } else if (w >= G::WR2C) {
+        const int f = w - G::WR2C;
         // ============================ R2C warp ============================
-        C* xb = reinterpret_cast<C*>(smem_raw + G::OFF_X) + G::PADX;
+        C* xb = reinterpret_cast<C*>(smem_raw + G::OFF_X) + (G::NF + f) * G::PADX;
         const PadAddr pad{};
         const WarpSync wsync{};
-        for (int u = 0;; ++u) {
+        for (int u = f;; u += G::NF) {
             const int ord = u / KC, tile = tile_of(ord);
             if (tile >= ntiles_c) break;
             int j0, k0;
@@ -291,6 +352,7 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
             const int k = k0 + u % KC;
             const int sl = u % G::NLN;
             mbar_wait_cl(B(G::B_LNF + sl), (uint32_t)(u / G::NLN) & 1u);
+            K1T(7, u);
             const float* lsrc = reinterpret_cast<const float*>(smem_raw + G::OFF_LN + (size_t)sl * G::LNSLOT);
             C v[LPC][E];
 #pragma unroll
@@ -299,15 +361,16 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                 for (int m = 0; m < E; ++m)
                     v[l][m] = *reinterpret_cast<const C*>(lsrc + l * N + 2 * (lane + 32 * m));
             __syncwarp();
-            if (lane == 0) {
-                // re-arm the slot for plane u + NLN, then release it to every writer
-                mbar_expect_tx_s(B(G::B_LNF + sl), G::LNSLOT);
-                for (int c = 0; c < NCL; ++c) mbar_arrive_cluster(mapa_s(B(G::B_LNE + sl), (uint32_t)c));
-            }
 #pragma unroll
             for (int l = 0; l < LPC; ++l) {
                 fft_regs<Nh, E, N, true>(v[l], lane, xb, pad, xline_tw<float, true>(tw, nullptr), wsync);
                 __syncwarp();
+                if (l == LPC - 1 && lane == 0) {
+                    // every read of the slot has fed the transforms: re-arm it for
+                    // plane u + NLN, then release it to every writer
+                    mbar_expect_tx_s(B(G::B_LNF + sl), G::LNSLOT);
+                    for (int c = 0; c < NCL; ++c) mbar_arrive_cluster(mapa_s(B(G::B_LNE + sl), (uint32_t)c));
+                }
 #pragma unroll
                 for (int m = 0; m < E; ++m) xb[pad(lane + 32 * m)] = v[l][m];
                 __syncwarp();
@@ -329,6 +392,7 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                 }
                 __syncwarp();
             }
+            K1T(8, u);
         }
     } else {
         // ========================= stencil warps =========================
@@ -460,6 +524,7 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
             auto step = [&](int k, float (&x_cur)[4], float (&s_cur)[4], float (&gn_cur)[4],
                             float (&ds_cur)[4], float (&x_nx)[4], float (&s_nx)[4], float (&gn_nx)[4],
                             float (&ds_nx)[4]) {
+                if (w == 0) K1T(0, u);
                 if (tid == 0) issue(k + 2);
                 wait(k + 1);
                 s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx);
@@ -470,11 +535,13 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                     if (halo && lane <= TJ) Sn[lane * SW + CI] = s_col(k + 1);
                 }
                 named_bar(1, G::NST);
+                if (w == 0) K1T(1, u);
                 // the previous plane's G slot is consumed by every stencil warp
                 if (tid == 0 && k > k0) release_g(u - 1);
                 if (!halo && row_in) {
                     const int gs = u % G::NG;
                     mbar_wait_cl(B(G::B_GF + gs), (uint32_t)(u / G::NG) & 1u);
+                    if (w == 0) K1T(2, u);
                     const float* Sc = Sc_ring;
                     const size_t gidx = ((size_t)k * N + gj) * N + gi0;
                     const unsigned char* stk = stage(k);
@@ -557,6 +624,7 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                     {
                         const int ls = u % G::NLN;
                         mbar_wait_cl(B(G::B_LNE + ls), ((uint32_t)(u / G::NLN) & 1u) ^ 1u);
+                        if (w == 0) K1T(3, u);
                         const uint32_t owner = (uint32_t)(w / LPC);
                         const uint32_t off = (uint32_t)(G::OFF_LN + ls * G::LNSLOT) +
                                              4u * (uint32_t)((w % LPC) * N + i0 + ii);
@@ -712,15 +780,46 @@ inline cudaError_t k1f_launch(StencilParams<float> p, float2* S, const float2* t
     const float invL = float(1.0 / ((double)N * N * N));
     cudaLaunchAttribute at[1];
     cudaLaunchConfig_t cfg = k1f_config<N>(grid, s, at);
+#ifdef CM_K1F_TRACE
+    static unsigned long long* tbuf = nullptr;
+    static int launches = 0;
+    const size_t tn = (size_t)K1Geo<N>::NCL * 10 * 64;
+    if (!tbuf) {
+        cudaMalloc(&tbuf, tn * 8);
+        cudaMemcpyToSymbol(g_k1f_trace, &tbuf, sizeof(tbuf));
+    }
+    cudaMemsetAsync(tbuf, 0, tn * 8, s);
+#endif
+    cudaError_t rc = cudaErrorInvalidValue;
     switch (s2_flags(p)) {
 #define CM_K1F_CASE(FL) \
     case FL:            \
-        return cudaLaunchKernelEx(&cfg, k1f_kernel<N, FL>, p, S, twN, invL, tmx, tmp, tma);
+        rc = cudaLaunchKernelEx(&cfg, k1f_kernel<N, FL>, p, S, twN, invL, tmx, tmp, tma); \
+        break;
         CM_S2_MODES(CM_K1F_CASE)
 #undef CM_K1F_CASE
         default:
-            return cudaErrorInvalidValue;
+            break;
     }
+#ifdef CM_K1F_TRACE
+    if (++launches == 2) {
+        std::vector<unsigned long long> h(tn);
+        cudaMemcpyAsync(h.data(), tbuf, tn * 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        unsigned long long t0 = ~0ull;
+        for (auto v : h) if (v && v < t0) t0 = v;
+        for (int b = 0; b < K1Geo<N>::NCL; ++b)
+            for (int ev = 0; ev < 9; ++ev) {
+                std::fprintf(stderr, "cta%d ev%d:", b, ev);
+                for (int u = 0; u < 40; ++u) {
+                    const unsigned long long v = h[((size_t)b * 10 + ev) * 64 + u];
+                    std::fprintf(stderr, " %lld", v ? (long long)(v - t0) : -1ll);
+                }
+                std::fprintf(stderr, "\n");
+            }
+    }
+#endif
+    return rc;
 }
 
 } // namespace cm
