@@ -241,6 +241,10 @@ int cm_penalized_objective(cm_ctx* ctx, const double* x, const cm_reg_config* cf
                            double* out7);
 /* fft3 (fourier.hpp:11): unnormalised forward transform, full complex grid */
 int cm_fft3(cm_ctx* ctx, const double* x, double* out_interleaved);
+/* fft3_centered (fourier.hpp:24, fourier.cpp:109): fft3 of the half-shifted
+ * volume, computed as the (-1)^(a+b+c)-signed fft3; full complex
+ * grid. The resident solve result (cm_get_spectrum) is left intact. */
+int cm_fft3_centered(cm_ctx* ctx, const double* x, double* out_interleaved);
 
 /* Transform-free components for ANY side n >= 1 (the reference accepts odd and
  * tiny volumes here, test_regularizer.cpp:141-161, 245); fp64 on the current

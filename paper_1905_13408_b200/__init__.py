@@ -9,7 +9,8 @@ from .regularizer import (  # noqa: F401
     AccumulatorPair, Context, DataScales, DeviceError, Error, GridMismatch, InvalidArgument,
     MStepTraceRow, Multipliers, NonHermitianAccumulator, NonHermitianInput, NonPositiveScale,
     ObjectiveValue, RegConfig, Refresh, SolveStats, StepDiverged, StepRule, WeightFields,
-    compute_weights, context, data_gradient, derive_config, em_m_step, fft3, m_step, penalized_objective,
+    compute_weights, context, data_gradient, derive_config, em_m_step, fft3, fft3_centered, m_step,
+    penalized_objective,
     prox_l1, scale_data, smoothed_tv_gradient, smoothed_tv_value, validate_reg_config,
 )
 

@@ -91,6 +91,7 @@ def load() -> C.CDLL:
         "cm_prox_l1": [P, P, P, P],
         "cm_penalized_objective": [P, P, C.POINTER(cm_reg_config), P, P, P],
         "cm_fft3": [P, P, P],
+        "cm_fft3_centered": [P, P, P],
         "cm_compute_weights_n": [C.c_int, P, C.c_double, C.c_double, C.c_int, P, P],
         "cm_smoothed_tv_value_n": [C.c_int, P, C.c_double, P, _dp],
         "cm_smoothed_tv_gradient_n": [C.c_int, P, C.c_double, P, P],

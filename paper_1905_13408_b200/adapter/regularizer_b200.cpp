@@ -8,64 +8,25 @@
 // regularizer.cpp, plus libcm.so; nothing else in the reference changes.
 //
 // Status codes are rethrown as the reference's exception types
-// (errors.hpp:7-30). Contexts are cached per thread and side length, so
-// em_refine's repeated m_step calls (refine.cpp:181, 249) reuse device memory.
-// Precision: CM_PRECISION=64 (default here: the reference's fp64 tests pass
-// unchanged) or 32 (product mode, 1e-5 objective parity).
-#include <cstdlib>
-#include <map>
-#include <memory>
+// (errors.hpp:7-30). Contexts are cached per thread and side length
+// (cm_adapter.hpp), so em_refine's repeated m_step calls (refine.cpp:181, 249)
+// reuse device memory, the accumulator scale_data made resident is not
+// uploaded twice, and fft3_centered of the returned volume reads the resident
+// result (params_b200.cpp, fourier_b200.cpp). Precision: CM_PRECISION=64
+// (default here: the reference's fp64 tests pass unchanged) or 32 (product
+// mode, 1e-5 objective parity). Devices: CM_DEVICES (default "0").
 #include <string>
-#include <utility>
 #include <vector>
 
-#include "cm_api.h"
+#include "cm_adapter.hpp"
 #include "cryomap/regularizer.hpp"
 
 namespace cryomap {
 
 namespace {
 
-[[noreturn]] void rethrow(int rc) {
-    const std::string msg = cm_last_error();
-    switch (rc) {
-        case CM_ERR_INVALID_ARGUMENT:
-        case CM_ERR_UNSUPPORTED: throw InvalidArgument(msg);
-        case CM_ERR_GRID_MISMATCH: throw GridMismatch(msg);
-        case CM_ERR_NON_HERMITIAN: throw NonHermitianAccumulator(msg);
-        case CM_ERR_STEP_DIVERGED: throw StepDiverged(msg);
-        case CM_ERR_NON_POSITIVE_SCALE: throw NonPositiveScale(msg);
-        case CM_ERR_NON_HERMITIAN_INPUT: throw NonHermitianInput(msg);
-        default: throw Error("cm (B200 solver): " + msg);
-    }
-}
-
-void check(int rc) {
-    if (rc != CM_OK) rethrow(rc);
-}
-
-int precision() {
-    const char* p = std::getenv("CM_PRECISION");
-    return (p && std::atoi(p) == 32) ? 32 : 64;
-}
-
-struct CtxDel {
-    void operator()(cm_ctx* c) const { cm_ctx_destroy(c); }
-};
-
-cm_ctx* context(int n) {
-    thread_local std::map<std::pair<int, int>, std::unique_ptr<cm_ctx, CtxDel>> cache;
-    const auto key = std::make_pair(n, precision());
-    auto it = cache.find(key);
-    if (it == cache.end()) {
-        require_even_side(n);  // volume.hpp:94-97
-        cm_ctx* c = nullptr;
-        const int dev = 0;
-        check(cm_ctx_create(n, &dev, 1, key.second, &c));
-        it = cache.emplace(key, std::unique_ptr<cm_ctx, CtxDel>(c)).first;
-    }
-    return it->second.get();
-}
+using cm_adapter::check;
+using cm_adapter::context;
 
 cm_reg_config to_c(const RegConfig& c) {
     cm_reg_config r{};
@@ -95,10 +56,8 @@ ObjectiveValue to_obj(const double* v) {
     return o;
 }
 
-void upload(cm_ctx* ctx, const AccumulatorPair& acc) {
-    check(cm_set_accumulator(ctx, acc.weight.data(),
-                             reinterpret_cast<const double*>(acc.numerator.data()),
-                             acc.finalized ? 1 : 0));
+void upload(const AccumulatorPair& acc) {
+    cm_adapter::upload_acc(cm_adapter::slot(acc.side_n), acc);
 }
 
 } // namespace
@@ -143,7 +102,7 @@ Volume3D smoothed_tv_gradient(const Volume3D& v, double mu, const std::vector<do
 Volume3D data_gradient(const Volume3D& x, const AccumulatorPair& acc) {
     if (x.side_n != acc.side_n) throw GridMismatch("data_gradient: side_n differs");
     cm_ctx* ctx = context(acc.side_n);
-    upload(ctx, acc);
+    upload(acc);
     Volume3D g(x.side_n, x.voxel_size);
     check(cm_data_gradient(ctx, x.data.data(), g.data.data()));
     return g;
@@ -162,7 +121,7 @@ ObjectiveValue penalized_objective(const Volume3D& x, const AccumulatorPair& acc
                                    const Volume3D& x_weights_source) {
     validate_reg_config(config);
     cm_ctx* ctx = context(acc.side_n);
-    upload(ctx, acc);
+    upload(acc);
     const cm_reg_config c = to_c(config);
     double o[7];
     check(cm_penalized_objective(ctx, x.data.data(), &c, x_anchor.data.data(),
@@ -175,22 +134,25 @@ Volume3D m_step(const AccumulatorPair& acc, const Volume3D& x_init, const Volume
     validate_reg_config(config);
     if (x_init.side_n != acc.side_n || x_anchor.side_n != acc.side_n)
         throw GridMismatch("m_step: side_n differs");
-    cm_ctx* ctx = context(acc.side_n);
+    cm_adapter::Slot& s = cm_adapter::slot(acc.side_n);
+    cm_ctx* ctx = s.ctx.get();
     const cm_reg_config c = to_c(config);
     std::vector<cm_trace_row> rows(trace ? (size_t)config.inner_iters : 0);
     Volume3D out(x_init.side_n, x_init.voxel_size);
     cm_solve_stats st{};
-    // x_init and x_anchor may be one object (refine.cpp:181): pass one pointer
+    // the accumulator scale_data(acc) made resident is not uploaded again
+    // (em_refine: refine.cpp:175-181); x_init and x_anchor may be one object
+    // (refine.cpp:181): pass one pointer
+    cm_adapter::upload_acc(s, acc);
     const double* xa = (&x_init == &x_anchor) ? x_init.data.data() : x_anchor.data.data();
-    const int rc = cm_m_step(ctx, acc.weight.data(),
-                             reinterpret_cast<const double*>(acc.numerator.data()),
-                             acc.finalized ? 1 : 0, x_init.data.data(), xa, &c,
-                             out.data.data(), trace ? rows.data() : nullptr,
-                             trace ? config.inner_iters : 0, &st);
+    check(cm_set_volumes(ctx, x_init.data.data(), xa));
+    const int rc = cm_solve(ctx, &c, trace ? rows.data() : nullptr, trace ? config.inner_iters : 0, &st);
     if (trace)
         for (int r = 0; r < st.trace_rows; ++r)
             trace->push_back({to_obj(rows[r].before), to_obj(rows[r].after), rows[r].step});
     check(rc);
+    check(cm_get_volume(ctx, out.data.data()));
+    cm_adapter::note_result(s, out);  // fft3_centered(out) reads the resident result
     return out;
 }
 

@@ -21,8 +21,9 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
-#define CM_SIDES(X) X(4) X(6) X(8) X(12) X(16) X(24) X(32) X(48) X(64) X(96) X(128) X(192) \
-    X(256) X(384) X(512) X(768) X(1024)
+#define CM_SIDES(X) X(4) X(6) X(8) X(10) X(12) X(14) X(16) X(20) X(24) X(28) X(32) X(40) X(48) \
+    X(56) X(64) X(80) X(96) X(100) X(112) X(128) X(160) X(192) X(200) X(224) X(240) X(256) X(320) \
+    X(360) X(384) X(400) X(448) X(480) X(512) X(640) X(720) X(768) X(800) X(960) X(1024)
 #define CM_DECL(NN) ImplBase* make_impl_##NN(int precision);
 CM_SIDES(CM_DECL)
 
@@ -74,6 +75,25 @@ extern "C" {
 int cm_version(void) { return CM_API_VERSION; }
 const char* cm_last_error(void) { return g_err.c_str(); }
 
+// why a side has no solver context (the reference accepts any even side through
+// FFTW, volume.hpp:94-97)
+static std::string unsupported_side_reason(int n) {
+    const std::string sn = std::to_string(n);
+    if (n < 4 || n % 2) return "side " + sn + " is not an even side >= 4 (require_even_side, volume.hpp:94-97)";
+    int m = n;
+    for (int p : {2, 3, 5, 7})
+        while (m % p == 0) m /= p;
+    if (m != 1) {
+        int q = 11;
+        while (m % q) q += 2;
+        return "side " + sn + " has the prime factor " + std::to_string(q) +
+               ": the FFT engine plans radices 2, 3, 5 and 7 only (no Bluestein stage)";
+    }
+    if (n > 1024) return "side " + sn + " exceeds 1024: one GPU's fp32 working set; use the z-slab solver";
+    return "side " + sn + " (2^a 3^b 5^c 7^d) is not among the sides compiled into this build "
+           "(paper_1905_13408_b200/build.py SIDES, csrc/cm_api.cu CM_SIDES)";
+}
+
 int cm_supported_side(int n) {
     switch (n) {
 #define CM_ONE(NN) case NN:
@@ -90,8 +110,7 @@ int cm_ctx_create(int n, const int* devices, int ndev, int precision, cm_ctx** o
     *out = nullptr;
     if (n < 4 || n % 2 != 0)
         return fail(CM_ERR_INVALID_ARGUMENT, "side_n must be even and >= 4, got " + std::to_string(n));
-    if (!cm_supported_side(n))
-        return fail(CM_ERR_UNSUPPORTED, "no compiled radix plan for side " + std::to_string(n));
+    if (!cm_supported_side(n)) return fail(CM_ERR_UNSUPPORTED, unsupported_side_reason(n));
     if (precision != 32 && precision != 64)
         return fail(CM_ERR_INVALID_ARGUMENT, "precision must be 32 or 64");
     if (ndev > 1) return fail(CM_ERR_INVALID_ARGUMENT, "one device per context (one process per GPU)");
@@ -364,6 +383,12 @@ int cm_penalized_objective(cm_ctx* ctx, const double* x, const cm_reg_config* cf
 int cm_fft3(cm_ctx* ctx, const double* x, double* out_interleaved) {
     CTX_GUARD(ctx);
     return ctx->impl->fft3(x, out_interleaved);
+}
+
+int cm_fft3_centered(cm_ctx* ctx, const double* x, double* out_interleaved) {
+    CTX_GUARD(ctx);
+    if (!x || !out_interleaved) return fail(CM_ERR_INVALID_ARGUMENT, "null argument");
+    return ctx->impl->fft3(x, out_interleaved, 1);
 }
 
 // ---- z-slab distributed solver ------------------------------------------------------

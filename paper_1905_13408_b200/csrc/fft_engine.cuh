@@ -11,7 +11,7 @@
 // Twiddles come from a shared-memory table tw[x] = exp(-2 pi i x / TWN)
 // (TWN = table length, a multiple of LEN); the inverse uses conj.
 // Radices: 16, 8, 4, 2 (compile-time split-in-half DIT with constant
-// twiddles) and 3.
+// twiddles), 3, 5 and 7 (symmetric-pair odd DFTs).
 #pragma once
 
 #include <type_traits>
@@ -26,6 +26,8 @@ __host__ __device__ constexpr int pick_radix(int rem, int E) {
            : (rem % 4 == 0 && E % 4 == 0)   ? 4
            : (rem % 2 == 0 && E % 2 == 0)   ? 2
            : (rem % 3 == 0 && E % 3 == 0)   ? 3
+           : (rem % 5 == 0 && E % 5 == 0)   ? 5
+           : (rem % 7 == 0 && E % 7 == 0)   ? 7
                                             : 0;
 }
 
@@ -121,6 +123,66 @@ template <bool FWD, typename C> struct Dft<3, FWD, C> {
         u[1] = cadd(m, r);
         u[2] = csub(m, r);
     }
+};
+
+// odd prime radix P in {5, 7}: y_k = x0 + sum_j cos(2 pi jk/P) (x_j + x_{P-j})
+//                                  -+ i sum_j sin(2 pi jk/P) (x_j - x_{P-j})
+// (pairs j, P-j share the cosine and flip the sine; (P-1)^2/2 real FMAs per
+// component instead of (P-1)^2)
+__host__ __device__ constexpr double odd_cos(int P, int m) {
+    return P == 5 ? (m == 1 ? 0.30901699437494742410 : -0.80901699437494742410)
+                  : (m == 1 ? 0.62348980185873353053 : m == 2 ? -0.22252093395631440429
+                                                              : -0.90096886790241912624);
+}
+__host__ __device__ constexpr double odd_sin(int P, int m) {
+    return P == 5 ? (m == 1 ? 0.95105651629515357212 : 0.58778525229247312917)
+                  : (m == 1 ? 0.78183148246802980871 : m == 2 ? 0.97492791218182360702
+                                                              : 0.43388373911755812048);
+}
+template <int P, bool FWD, typename C> struct DftOdd {
+    static __device__ __forceinline__ void run(C (&u)[P]) {
+        using Rt = decltype(C::x);
+        constexpr int H = (P - 1) / 2;
+        C a[H + 1], b[H + 1];
+#pragma unroll
+        for (int j = 1; j <= H; ++j) {
+            a[j] = cadd(u[j], u[P - j]);
+            b[j] = csub(u[j], u[P - j]);
+        }
+        C y0 = u[0];
+#pragma unroll
+        for (int j = 1; j <= H; ++j) y0 = cadd(y0, a[j]);
+        C out[P];
+        out[0] = y0;
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+            Rt tx = u[0].x, ty = u[0].y, vx = Rt(0), vy = Rt(0);
+#pragma unroll
+            for (int j = 1; j <= H; ++j) {
+                const int m = (j * k) % P;  // cos / sin of 2 pi m / P, m folded into 1..H
+                const bool flip = m > H;
+                const int mm = flip ? P - m : m;
+                const Rt cc = Rt(odd_cos(P, mm));
+                const Rt ss = flip ? Rt(-odd_sin(P, mm)) : Rt(odd_sin(P, mm));
+                tx += cc * a[j].x;
+                ty += cc * a[j].y;
+                vx += ss * b[j].x;
+                vy += ss * b[j].y;
+            }
+            // forward: y_k = t - i v, y_{P-k} = t + i v (inverse: signs swapped)
+            const C iv = cx<C>(-vy, vx);  // i v
+            out[k] = FWD ? cx<C>(tx - iv.x, ty - iv.y) : cx<C>(tx + iv.x, ty + iv.y);
+            out[P - k] = FWD ? cx<C>(tx + iv.x, ty + iv.y) : cx<C>(tx - iv.x, ty - iv.y);
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) u[k] = out[k];
+    }
+};
+template <bool FWD, typename C> struct Dft<5, FWD, C> {
+    static __device__ __forceinline__ void run(C (&u)[5]) { DftOdd<5, FWD, C>::run(u); }
+};
+template <bool FWD, typename C> struct Dft<7, FWD, C> {
+    static __device__ __forceinline__ void run(C (&u)[7]) { DftOdd<7, FWD, C>::run(u); }
 };
 
 // power-of-two radix: decimation in time split into even / odd halves
@@ -220,9 +282,19 @@ __device__ __forceinline__ void fft_regs(C (&v)[E], int t, C* buf, const Addr& a
     }
 }
 
+// Elements per thread for lengths with a factor 5 or 7: every distinct odd
+// prime of LEN once (a radix-R stage needs R | E) times the largest power of
+// two dividing LEN that keeps E <= 32
+__host__ __device__ constexpr int elems_57(int LEN) {
+    const int f = (LEN % 3 == 0 ? 3 : 1) * (LEN % 5 == 0 ? 5 : 1) * (LEN % 7 == 0 ? 7 : 1);
+    int p2 = 1;
+    while (LEN % (2 * p2) == 0 && f * 2 * p2 <= 32) p2 *= 2;
+    return f * p2;
+}
 // Elements per thread for a transform of length LEN.
 __host__ __device__ constexpr int elems_for(int LEN) {
     return LEN <= 24 ? LEN
+           : (LEN % 5 == 0 || LEN % 7 == 0) ? elems_57(LEN)
            : (LEN % 3 == 0) ? (LEN >= 192 ? 24 : 12)
            : (LEN >= 512 ? 16 : 8);
 }

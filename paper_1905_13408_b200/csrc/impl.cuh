@@ -335,7 +335,7 @@ struct ImplBase {
     virtual int prox(const double* x, const double* t, double* out) = 0;
     virtual int objective(const double* x, const cm_reg_config* c, const double* anchor,
                           const double* wsrc, double* out7) = 0;
-    virtual int fft3(const double* x, double* out) = 0;
+    virtual int fft3(const double* x, double* out, int centered = 0) = 0;
     // fft3_centered of the resident solve result (em_refine, refine.cpp:182)
     virtual int result_spectrum(double* out, int centered) = 0;
     // FSC of this context's and another's resident results (refine.cpp:194)
@@ -1078,7 +1078,7 @@ struct Impl final : ImplBase {
             return CM_OK;
         };
 
-        const int per_iter = use_fused ? 6 : 8;  // kernels per iteration
+        const int per_iter = (use_fused || (K1F && use_k1f)) ? 6 : 8;  // kernels per iteration
         const bool use_graph = std::getenv("CM_NO_GRAPH") == nullptr && !profiling;
         const int chunk = 6;
         const int nchunks = (K + chunk - 1) / chunk;
@@ -1403,10 +1403,13 @@ struct Impl final : ImplBase {
         return CM_OK;
     }
 
-    int fft3(const double* x, double* out) override {
-        result_valid = false;
-        CKS(upload_real(x, X[0]));
-        return spectrum_to_host(X[0], out, 0);
+    // fft3 / fft3_centered (fourier.cpp:59-66, 109) of a host volume; the upload
+    // goes to an iterate buffer that does not hold the resident solve result
+    int fft3(const double* x, double* out, int centered) override {
+        R* buf = X[0];
+        if (result_valid && !last_fista && X[last_iter % 3] == buf) buf = X[1];
+        CKS(upload_real(x, buf));
+        return spectrum_to_host(buf, out, centered);
     }
 
     int result_to_spectrum() override {

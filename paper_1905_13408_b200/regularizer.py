@@ -512,3 +512,12 @@ def fft3(v, precision: int | None = None) -> np.ndarray:
     out = np.empty(xa.shape, np.complex128)
     _check(ctx.lib.cm_fft3(ctx.ptr, xa.ctypes.data, out.ctypes.data))
     return out
+
+
+def fft3_centered(v, precision: int | None = None) -> np.ndarray:
+    """fourier.hpp:24 (fourier.cpp:109) — fft3 of halfshift3(v), full complex grid."""
+    ctx = context(_side(v), precision)
+    xa = ctx._vol(v)
+    out = np.empty(xa.shape, np.complex128)
+    _check(ctx.lib.cm_fft3_centered(ctx.ptr, xa.ctypes.data, out.ctypes.data))
+    return out

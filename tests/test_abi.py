@@ -23,10 +23,25 @@ def test_library_exports_every_header_symbol():
 
 def test_supported_sides():
     lib = _lib.load()
-    for n in [4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024]:
+    from paper_1905_13408_b200.build import SIDES
+    for n in SIDES:   # radix 2 / 3 / 5 / 7 plans, incl. common cryo-EM boxes 160..400
         assert lib.cm_supported_side(n) == 1
-    for n in [2, 5, 10, 20, 100, 2048]:
+    for n in [2, 5, 22, 26, 34, 2048]:
         assert lib.cm_supported_side(n) == 0
+
+
+@pytest.mark.parametrize("n,why", [(22, "prime factor 11"), (26, "prime factor 13"),
+                                   (7, "must be even"), (2048, "exceeds 1024"),
+                                   (36, "not among the sides compiled")])
+def test_unsupported_side_states_the_reason(n, why):
+    """Every even side the reference accepts (volume.hpp:94-97) either has a
+    solver context or is rejected with the reason (no CPU fallback)."""
+    import ctypes as C
+    lib = _lib.load()
+    ptr = C.c_void_p()
+    rc = lib.cm_ctx_create(n, None, 0, 32, C.byref(ptr))
+    assert rc != 0
+    assert why in lib.cm_last_error().decode()
 
 
 def test_struct_layout_matches_header(tmp_path):

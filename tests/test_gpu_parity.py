@@ -48,7 +48,8 @@ def check_trace(rows, ref, tol):
 
 
 @pytest.mark.parametrize("prec", [32, 64])
-@pytest.mark.parametrize("n", [4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 128])
+@pytest.mark.parametrize("n", [4, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 100,
+                               112, 128, 160, 200, 224])
 def test_fft3_matches_reference_convention(n, prec):
     """fourier.hpp:6-9: unnormalised forward transform (test_grid_fourier KATs)."""
     x = np.random.default_rng(n).standard_normal((n, n, n))
@@ -211,7 +212,7 @@ SWEEP_MODES = {
 
 
 @pytest.mark.parametrize("prec", [32, 64])
-@pytest.mark.parametrize("n", [12, 48, 96, 128])
+@pytest.mark.parametrize("n", [12, 20, 28, 48, 80, 96, 112, 128, 160])
 def test_sweep_tiles_and_modes_vs_oracle(O, n, prec):
     """Tile geometries of the fused sweep (TJ x TK line tiles, i-chunks, idle
     FFT groups) in every RegConfig mode, anchor != x_init, against the oracle."""
@@ -233,6 +234,34 @@ def test_sweep_tiles_and_modes_vs_oracle(O, n, prec):
         assert rc == 0
         check_trace(trace, tro, TOL[prec]["obj"])
         assert rel_l2(x, xo) <= TOL[prec]["vol"], name
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("n", [20, 28, 40, 56])
+def test_radix5_radix7_sides_vs_unmodified_reference(n, prec):
+    """Sides with factors 5 and 7 (radix-5 / radix-7 stages of the FFT engine)
+    against the UNMODIFIED reference m_step (oracle/_ref, FFTW-API shim):
+    reference default semantics, 12 iterations, traces and volume."""
+    from oracle_lib import Reference, have_reference
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    R = Reference()
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    rc, sy, sn = R.scale_data(p.weight, p.numerator)
+    assert rc == 0
+    s = cm.scale_data(acc, precision=prec)
+    np.testing.assert_allclose([s.s_y, s.s_n], [sy, sn], rtol=1e-12)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 12
+    trace = []
+    x = cm.m_step(acc, p.x0, p.x0, cfg, trace, precision=prec)
+    c = make_cfg(alpha=cfg.alpha, beta=cfg.beta, gamma=cfg.gamma, eps=cfg.eps,
+                 eps_prime=cfg.eps_prime, mu=cfg.mu, inner_iters=12)
+    rc, xr, trr = R.m_step(p.weight, p.numerator, p.x0, p.x0, c)
+    assert rc == 0, R.last_error()
+    check_trace(trace, trr, TOL[prec]["obj"])
+    assert rel_l2(x, xr) <= TOL[prec]["vol"]
 
 
 @pytest.mark.parametrize("prec", [32, 64])
@@ -330,6 +359,38 @@ def test_fused_plane_pairs_match_separate_passes(n, monkeypatch):
     assert rel_l2(x_fus, x_sep) <= 1e-6
     np.testing.assert_allclose([r.after.surrogate() for r in t_fus],
                                [r.after.surrogate() for r in t_sep], rtol=1e-6)
+
+
+@pytest.mark.parametrize("n", [256, 512])
+@pytest.mark.parametrize("mode", ["per_inner", "per_m_step", "fista"])
+def test_fused_k1_cluster_kernel_matches_separate_passes(n, mode, monkeypatch):
+    """The opt-in fused K1 (CM_K1F=1, k1f.cuh: x C2R + stencil + x R2C in one
+    thread-block-cluster kernel over distributed shared memory) gives the same
+    iterates and audit trace as the separate x-transform kernels."""
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=32)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 8
+    if mode == "per_m_step":
+        cfg.refresh = cm.Refresh.per_m_step
+    if mode == "fista":
+        cfg.refresh = cm.Refresh.per_m_step
+        cfg.momentum = 1
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CM_K1F", flag)
+        ctx = cm.Context(n, 32)   # the flag is read when a context is created
+        ctx.set_accumulator(acc)
+        ctx.set_volumes(p.x0, p.x0)
+        tr = []
+        st = ctx.solve(cfg, tr)
+        out[flag] = (ctx.get_volume(), tr, st)
+        ctx.close()
+    assert out["1"][2].kernel_launches < out["0"][2].kernel_launches  # two launches fewer
+    assert rel_l2(out["1"][0], out["0"][0]) <= 1e-6
+    np.testing.assert_allclose([r.after.surrogate() for r in out["1"][1]],
+                               [r.after.surrogate() for r in out["0"][1]], rtol=1e-6)
 
 
 @pytest.mark.parametrize("prec", [32, 64])
