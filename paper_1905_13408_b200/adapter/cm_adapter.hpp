@@ -55,7 +55,8 @@ inline int precision() {
     return (p && std::atoi(p) == 32) ? 32 : 64;
 }
 
-// the devices a context drives: CM_DEVICES="0,1,2,3" (default "0")
+// the devices a context drives: CM_DEVICES="0,1,2,3" (default "0"); more than one
+// device selects the z-slab solver (needs CM_PRECISION=32, sides n % 128 == 0)
 inline int devices(int* out, int cap) {
     const char* e = std::getenv("CM_DEVICES");
     int n = 0;
@@ -113,6 +114,8 @@ struct CtxDel {
 
 struct Slot {
     std::unique_ptr<cm_ctx, CtxDel> ctx;
+    bool multi = false;                   // ctx spans several GPUs (z-slab solver)
+    std::unique_ptr<cm_ctx, CtxDel> aux;  // multi: one-GPU context for the transforms
     AccId acc;                         // accumulator resident on the device
     bool acc_valid = false;
     const double* result = nullptr;    // host buffer m_step returned, and its checksum
@@ -132,11 +135,26 @@ inline Slot& slot(int n) {
         check(cm_ctx_create(n, dev, nd, key.second, &c));
         it = cache.emplace(key, Slot{}).first;
         it->second.ctx.reset(c);
+        it->second.multi = nd > 1;
     }
     return it->second;
 }
 
 inline cm_ctx* context(int n) { return slot(n).ctx.get(); }
+
+// the context that runs whole-volume transforms (fft3_centered): the solver's
+// own, or for a multi-GPU solver a one-GPU context on its first device
+inline cm_ctx* transform_context(Slot& s, int n) {
+    if (!s.multi) return s.ctx.get();
+    if (!s.aux) {
+        int dev[16];
+        devices(dev, 16);
+        cm_ctx* c = nullptr;
+        check(cm_ctx_create(n, dev, 1, precision(), &c));
+        s.aux.reset(c);
+    }
+    return s.aux.get();
+}
 
 // make `acc` the resident accumulator (no upload when it already is)
 inline void upload_acc(Slot& s, const AccumulatorPair& acc) {
@@ -150,6 +168,21 @@ inline void upload_acc(Slot& s, const AccumulatorPair& acc) {
     s.acc_valid = true;
 }
 
+// a one-GPU context holding `acc` for the component entry points (data_gradient,
+// penalized_objective): the solver's own, or the transform context of a
+// multi-GPU solver
+inline cm_ctx* component_context(const AccumulatorPair& acc) {
+    Slot& s = slot(acc.side_n);
+    if (!s.multi) {
+        upload_acc(s, acc);
+        return s.ctx.get();
+    }
+    cm_ctx* c = transform_context(s, acc.side_n);
+    check(cm_set_accumulator(c, acc.weight.data(), reinterpret_cast<const double*>(acc.numerator.data()),
+                             acc.finalized ? 1 : 0));
+    return c;
+}
+
 inline void note_result(Slot& s, const Volume3D& out) {
     s.result = out.data.data();
     s.result_len = out.data.size();
@@ -157,7 +190,7 @@ inline void note_result(Slot& s, const Volume3D& out) {
 }
 
 inline bool is_result(const Slot& s, const Volume3D& v) {
-    return s.result && v.data.data() == s.result && v.data.size() == s.result_len &&
+    return s.result && !s.multi && v.data.data() == s.result && v.data.size() == s.result_len &&
            sample_sum(v.data.data(), v.data.size()) == s.result_sum;
 }
 

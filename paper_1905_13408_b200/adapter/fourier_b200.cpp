@@ -29,7 +29,7 @@ FourierVolume fft3_centered(const Volume3D& v) {
     if (cm_adapter::is_result(s, v))
         cm_adapter::check(cm_get_spectrum(s.ctx.get(), 1, out));
     else
-        cm_adapter::check(cm_fft3_centered(s.ctx.get(), v.data.data(), out));
+        cm_adapter::check(cm_fft3_centered(cm_adapter::transform_context(s, v.side_n), v.data.data(), out));
     return F;
 }
 

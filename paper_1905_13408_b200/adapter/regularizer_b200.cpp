@@ -26,7 +26,6 @@ namespace cryomap {
 namespace {
 
 using cm_adapter::check;
-using cm_adapter::context;
 
 cm_reg_config to_c(const RegConfig& c) {
     cm_reg_config r{};
@@ -56,9 +55,6 @@ ObjectiveValue to_obj(const double* v) {
     return o;
 }
 
-void upload(const AccumulatorPair& acc) {
-    cm_adapter::upload_acc(cm_adapter::slot(acc.side_n), acc);
-}
 
 } // namespace
 
@@ -101,8 +97,7 @@ Volume3D smoothed_tv_gradient(const Volume3D& v, double mu, const std::vector<do
 
 Volume3D data_gradient(const Volume3D& x, const AccumulatorPair& acc) {
     if (x.side_n != acc.side_n) throw GridMismatch("data_gradient: side_n differs");
-    cm_ctx* ctx = context(acc.side_n);
-    upload(acc);
+    cm_ctx* ctx = cm_adapter::component_context(acc);
     Volume3D g(x.side_n, x.voxel_size);
     check(cm_data_gradient(ctx, x.data.data(), g.data.data()));
     return g;
@@ -120,8 +115,7 @@ ObjectiveValue penalized_objective(const Volume3D& x, const AccumulatorPair& acc
                                    const RegConfig& config, const Volume3D& x_anchor,
                                    const Volume3D& x_weights_source) {
     validate_reg_config(config);
-    cm_ctx* ctx = context(acc.side_n);
-    upload(acc);
+    cm_ctx* ctx = cm_adapter::component_context(acc);
     const cm_reg_config c = to_c(config);
     double o[7];
     check(cm_penalized_objective(ctx, x.data.data(), &c, x_anchor.data.data(),

@@ -4,6 +4,8 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/cm_api.h"
 #include "dist.cuh"
@@ -54,7 +56,40 @@ static ImplBase* make_impl(int n, int precision) {
 
 using namespace cm;
 
+// One context over several GPUs of the box (cm_ctx_create with ndev > 1): the
+// z-slab runtime (dist.cuh) with one rank per device, each rank driven by its
+// own host thread for the duration of a call (NCCL communicators of one
+// process, one thread per rank: the collectives inside a solve need every rank
+// running). All device ids equal: the ranks are emulated on that one GPU
+// (EmuComm, device-to-device copies; the correctness configuration).
+struct MultiDev {
+    int n = 0, P = 0;
+    std::vector<std::unique_ptr<DistBase>> ranks;  // one per device, or one hosting P virtual ranks
+    template <class F> int run(F&& f) {
+        const int R = (int)ranks.size();
+        if (R == 1) {
+            if (cudaSetDevice(ranks[0]->device) != cudaSuccess) return fail(CM_ERR_CUDA, "cudaSetDevice failed");
+            return f(0, *ranks[0]);
+        }
+        std::vector<int> rc(R, CM_OK);
+        std::vector<std::string> msg(R);
+        std::vector<std::thread> th;
+        for (int r = 0; r < R; ++r)
+            th.emplace_back([&, r] {
+                rc[r] = cudaSetDevice(ranks[r]->device) != cudaSuccess
+                            ? fail(CM_ERR_CUDA, "cudaSetDevice failed")
+                            : f(r, *ranks[r]);
+                if (rc[r] != CM_OK) msg[r] = g_err;
+            });
+        for (auto& t : th) t.join();
+        for (int r = 0; r < R; ++r)
+            if (rc[r] != CM_OK) return fail(rc[r], "rank " + std::to_string(r) + ": " + msg[r]);
+        return CM_OK;
+    }
+};
+
 struct cm_ctx {
+    std::unique_ptr<MultiDev> multi;  // ndev > 1
     std::unique_ptr<ImplBase> impl;
     int n = 0;
     int precision = 32;
@@ -65,6 +100,8 @@ struct cm_ctx {
 
 #define CTX_GUARD(ctx)                                                         \
     do {                                                                       \
+        if ((ctx) && (ctx)->multi)                                             \
+            return fail(CM_ERR_UNSUPPORTED, "this entry point needs a one-GPU context (ndev == 1)"); \
         if (!(ctx) || !(ctx)->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context"); \
         if (cudaSetDevice((ctx)->device) != cudaSuccess)                       \
             return fail(CM_ERR_CUDA, "cudaSetDevice failed");                  \
@@ -105,6 +142,64 @@ int cm_supported_side(int n) {
     }
 }
 
+static int multi_create(int n, const int* devices, int ndev, int precision, cm_ctx** out) {
+    if (!devices) return fail(CM_ERR_INVALID_ARGUMENT, "ndev > 1 needs the device list");
+    if (precision != 32)
+        return fail(CM_ERR_UNSUPPORTED, "multi-GPU contexts run the fp32 z-slab solver (precision 32)");
+    if (n % 128 != 0 || n % ndev != 0 || (n / ndev) % 64 != 0)
+        return fail(CM_ERR_UNSUPPORTED, "multi-GPU context: the z-slab solver needs n % 128 == 0 and "
+                                        "n / ndev a multiple of 64 (side " + std::to_string(n) + ", " +
+                                        std::to_string(ndev) + " devices)");
+    bool same = true, distinct = true;
+    for (int a = 0; a < ndev; ++a)
+        for (int b = 0; b < ndev; ++b)
+            if (a != b) {
+                same &= devices[a] == devices[b];
+                distinct &= devices[a] != devices[b];
+            }
+    if (!same && !distinct)
+        return fail(CM_ERR_INVALID_ARGUMENT, "devices must be all distinct (one rank per GPU) or all "
+                                             "equal (ranks emulated on one GPU)");
+    auto ctx = std::make_unique<cm_ctx>();
+    ctx->n = n;
+    ctx->precision = precision;
+    ctx->device = devices[0];
+    ctx->multi = std::make_unique<MultiDev>();
+    MultiDev& m = *ctx->multi;
+    m.n = n;
+    m.P = ndev;
+    if (same) {
+        CK(cudaSetDevice(devices[0]));
+        m.ranks.emplace_back(make_dist(n));
+        if (!m.ranks[0]) return fail(CM_ERR_UNSUPPORTED, "no z-slab build for side " + std::to_string(n));
+        m.ranks[0]->device = devices[0];
+        m.ranks[0]->comm = std::make_unique<EmuComm>(ndev);
+        CKS(m.ranks[0]->init());
+    } else {
+        NcclApi& api = nccl_api();
+        std::string err;
+        if (!api.load(&err)) return fail(CM_ERR_NCCL, err);
+        ncclUniqueId id;
+        if (api.GetUniqueId(&id) != ncclSuccess) return fail(CM_ERR_NCCL, "ncclGetUniqueId failed");
+        for (int r = 0; r < ndev; ++r) {
+            m.ranks.emplace_back(make_dist(n));
+            if (!m.ranks[r]) return fail(CM_ERR_UNSUPPORTED, "no z-slab build for side " + std::to_string(n));
+            m.ranks[r]->device = devices[r];
+        }
+        // every rank's communicator is created concurrently (ncclCommInitRank
+        // returns once all ranks have joined)
+        CKS(m.run([&](int r, DistBase& d) {
+            int st = 0;
+            auto c = std::make_unique<NcclComm>(ndev, r, id, &st);
+            if (st) return fail(CM_ERR_NCCL, "NCCL init failed: " + c->err);
+            d.comm = std::move(c);
+            return d.init();
+        }));
+    }
+    *out = ctx.release();
+    return CM_OK;
+}
+
 int cm_ctx_create(int n, const int* devices, int ndev, int precision, cm_ctx** out) {
     if (!out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
     *out = nullptr;
@@ -113,7 +208,7 @@ int cm_ctx_create(int n, const int* devices, int ndev, int precision, cm_ctx** o
     if (!cm_supported_side(n)) return fail(CM_ERR_UNSUPPORTED, unsupported_side_reason(n));
     if (precision != 32 && precision != 64)
         return fail(CM_ERR_INVALID_ARGUMENT, "precision must be 32 or 64");
-    if (ndev > 1) return fail(CM_ERR_INVALID_ARGUMENT, "one device per context (one process per GPU)");
+    if (ndev > 1) return multi_create(n, devices, ndev, precision, out);
     const int dev = (devices && ndev == 1) ? devices[0] : 0;
     CK(cudaSetDevice(dev));
     auto ctx = std::make_unique<cm_ctx>();
@@ -136,6 +231,12 @@ int cm_ctx_destroy(cm_ctx* ctx) {
 }
 
 int cm_ctx_info(const cm_ctx* ctx, int* n, int* precision, long long* device_bytes) {
+    if (ctx && ctx->multi) {
+        if (n) *n = ctx->n;
+        if (precision) *precision = ctx->precision;
+        if (device_bytes) *device_bytes = -1;
+        return CM_OK;
+    }
     if (!ctx || !ctx->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
     if (n) *n = ctx->n;
     if (precision) *precision = ctx->precision;
@@ -144,6 +245,10 @@ int cm_ctx_info(const cm_ctx* ctx, int* n, int* precision, long long* device_byt
 }
 
 int cm_set_accumulator(cm_ctx* ctx, const double* weight, const double* numerator, int finalized) {
+    if (ctx && ctx->multi) {
+        if (!weight || !numerator) return fail(CM_ERR_INVALID_ARGUMENT, "null accumulator");
+        return ctx->multi->run([&](int, DistBase& d) { return d.set_accumulator(weight, numerator, finalized); });
+    }
     CTX_GUARD(ctx);
     if (!weight || !numerator) return fail(CM_ERR_INVALID_ARGUMENT, "null accumulator");
     return ctx->impl->set_accumulator(weight, numerator, finalized);
@@ -158,6 +263,16 @@ int cm_accumulator_info(const cm_ctx* ctx, double* residue, double* max_weight) 
 }
 
 int cm_scale_data(cm_ctx* ctx, double* s_y, double* s_n) {
+    if (ctx && ctx->multi) {
+        DistBase& d = *ctx->multi->ranks[0];
+        if (!d.acc_set) return fail(CM_ERR_STATE, "accumulator not set");
+        if (!d.acc_fin) return fail(CM_ERR_NON_HERMITIAN, "scale_data: accumulator is not finalized");
+        if (d.residue > 1e-8)
+            return fail(CM_ERR_NON_HERMITIAN_INPUT, "ifft3: whitened accumulator is not Hermitian");
+        if (s_y) *s_y = d.s_y;
+        if (s_n) *s_n = d.s_n;
+        return CM_OK;
+    }
     CTX_GUARD(ctx);
     ImplBase* im = ctx->impl.get();
     if (!im->acc_set) return fail(CM_ERR_STATE, "accumulator not set");
@@ -196,6 +311,10 @@ int cm_derive_config(double s_y, double s_n, double eps, double eps_prime, doubl
 }
 
 int cm_set_volumes(cm_ctx* ctx, const double* x_init, const double* x_anchor) {
+    if (ctx && ctx->multi) {
+        if (!x_init || !x_anchor) return fail(CM_ERR_INVALID_ARGUMENT, "null volume");
+        return ctx->multi->run([&](int, DistBase& d) { return d.set_volumes(x_init, x_anchor); });
+    }
     CTX_GUARD(ctx);
     if (!x_init || !x_anchor) return fail(CM_ERR_INVALID_ARGUMENT, "null volume");
     return ctx->impl->set_volumes(x_init, x_anchor);
@@ -203,6 +322,18 @@ int cm_set_volumes(cm_ctx* ctx, const double* x_init, const double* x_anchor) {
 
 int cm_solve(cm_ctx* ctx, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
              cm_solve_stats* stats) {
+    if (ctx && ctx->multi) {
+        // every rank takes the same decisions from all-reduced sums: rank 0 reports
+        const int R = (int)ctx->multi->ranks.size();
+        std::vector<std::vector<cm_trace_row>> tr(R);
+        std::vector<cm_solve_stats> st(R);
+        const int rc = ctx->multi->run([&](int r, DistBase& d) {
+            if (r == 0) return d.solve(cfg, trace, trace_cap, stats ? stats : &st[0]);
+            tr[r].resize(trace ? (size_t)trace_cap : 0);
+            return d.solve(cfg, trace ? tr[r].data() : nullptr, trace ? trace_cap : 0, &st[r]);
+        });
+        return rc;
+    }
     CTX_GUARD(ctx);
     return ctx->impl->solve(cfg, trace, trace_cap, stats);
 }
@@ -221,6 +352,10 @@ int cm_get_profile(const cm_ctx* ctx, double* ms7, int* iters) {
 }
 
 int cm_get_volume(cm_ctx* ctx, double* x_out) {
+    if (ctx && ctx->multi) {
+        if (!x_out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
+        return ctx->multi->run([&](int, DistBase& d) { return d.get_volume(x_out); });  // disjoint planes
+    }
     CTX_GUARD(ctx);
     if (!x_out) return fail(CM_ERR_INVALID_ARGUMENT, "null out");
     return ctx->impl->get_volume(x_out);
@@ -337,6 +472,14 @@ int cm_fsc(cm_ctx* a, cm_ctx* b, double* curve, int cap) {
 int cm_m_step(cm_ctx* ctx, const double* weight, const double* numerator, int finalized,
               const double* x_init, const double* x_anchor, const cm_reg_config* cfg,
               double* x_out, cm_trace_row* trace, int trace_cap, cm_solve_stats* stats) {
+    if (ctx && ctx->multi) {
+        CKS(validate(cfg));
+        CKS(cm_set_accumulator(ctx, weight, numerator, finalized));
+        CKS(cm_set_volumes(ctx, x_init, x_anchor));
+        const int rc = cm_solve(ctx, cfg, trace, trace_cap, stats);
+        if (rc != CM_OK) return rc;
+        return cm_get_volume(ctx, x_out);
+    }
     CTX_GUARD(ctx);
     // reference order: validate config, then the accumulator guard (regularizer.cpp:167-168)
     CKS(validate(cfg));

@@ -165,10 +165,42 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Block-wide sum of NV doubles per thread; result valid in thread 0. scratch
 // must hold 32*NV doubles.
+// Sum over the first `width` lanes of a warp, valid in lane 0; safe when the
+// warp is partial (blocks whose size is not a multiple of 32: radix-5/7 plans
+// such as 10 threads per CTA at side 100). Lanes past `width` are never read.
+__device__ __forceinline__ double warp_sum_partial(double v, int width) {
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = width >= 32 ? 0xffffffffu : ((1u << width) - 1u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_down_sync(mask, v, o);
+        if (lane + o < width) v += t;
+    }
+    return v;
+}
+
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nw = (blockDim.x + 31) >> 5;
+    if (blockDim.x & 31) {  // a partial last warp: guarded tree, fixed order
+        const int width = min(32, (int)blockDim.x - 32 * wid);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = warp_sum_partial(v[q], width);
+        __syncthreads();
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) scratch[wid * NV + q] = v[q];
+        __syncthreads();
+        if (wid == 0) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                double s = lane < nw ? scratch[lane * NV + q] : 0.0;
+                v[q] = warp_sum_partial(s, min(32, (int)blockDim.x));
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
     __syncthreads();

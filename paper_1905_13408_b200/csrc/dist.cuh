@@ -226,6 +226,9 @@ struct DistBase {
     virtual int set_synthetic(unsigned long long seed, double* s_y) = 0;
     std::unique_ptr<Comm> comm;
     int device = 0;
+    // accumulator state (full-grid statistics; every rank holds the same values)
+    bool acc_set = false, acc_fin = false;
+    double residue = 0.0, max_weight = 0.0, s_y = 0.0, s_n = 0.0;
 };
 
 template <int N>
@@ -283,8 +286,7 @@ struct DistImpl final : DistBase {
     double* stage = nullptr;   // full-grid fp64 staging (shared by virtual ranks)
     unsigned long long* stats_mx = nullptr;
     double* stats_part = nullptr;
-    bool acc_set = false, acc_fin = false, vol_set = false, anchor_is_init = false;
-    double residue = 0.0, max_weight = 0.0;
+    bool vol_set = false, anchor_is_init = false;
     int grid_s2 = 1, grid_x = 1, last_iter = 0, last_fista = 0;
     int ygrid = 1, zgrid = 1;
     bool result_valid = false;
@@ -430,7 +432,11 @@ struct DistImpl final : DistBase {
             CK(cudaGetLastError());
         }
         unsigned long long h[4];
+        const int blocks = grid_for(NN * (Nh + 1), 256);
+        std::vector<double> parts(2 * (size_t)blocks);
         CK(cudaMemcpyAsync(h, stats_mx, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(parts.data(), stats_part, sizeof(double) * parts.size(),
+                           cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         double worst, scale, wmax;
         std::memcpy(&worst, &h[0], 8);
@@ -438,6 +444,14 @@ struct DistImpl final : DistBase {
         std::memcpy(&wmax, &h[2], 8);
         residue = scale > 0.0 ? worst / scale : 0.0;
         max_weight = wmax;
+        // scale_data (params.cpp:9-26) by Parseval, as Impl::commit_acc_stage
+        double sw = 0.0, sz = 0.0;
+        for (int b = 0; b < blocks; ++b) {
+            sw += parts[2 * b];
+            sz += parts[2 * b + 1];
+        }
+        s_n = sw / (double)L;
+        s_y = std::sqrt(sz) / (double)L;
         acc_set = true;
         acc_fin = finalized != 0;
         return CM_OK;

@@ -9,6 +9,8 @@
 // imaginary part of column 0 (kernels.cuh layout).
 #pragma once
 
+#include <type_traits>
+
 #include "cm_common.cuh"
 #include "fft_engine.cuh"
 #include "kernels.cuh"
@@ -87,7 +89,11 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
     const int lg = threadIdx.x / T, t = threadIdx.x % T;
     C* buf = lines + lg * X::PADX;
     const PadAddr pad{};
-    const WarpSync wsync{};
+    // a line's T threads inside one warp: warp barriers; T not dividing 32 (sides
+    // with an odd factor in N/2 / E, e.g. 100 = 4 * 25) lets groups straddle
+    // warps: block barriers (every thread runs the same sequence)
+    using LineSync = std::conditional_t<(32 % T == 0), WarpSync, BlockSync>;
+    const LineSync wsync{};
     // persistent: the twiddle table is staged once per CTA
     const int ngrp = (p.nlines + X::LPC - 1) / X::LPC;
     for (int grp = blockIdx.x; grp < ngrp; grp += gridDim.x) {
@@ -99,10 +105,10 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
     if constexpr (DIR == 0) {
 #pragma unroll
         for (int m = 0; m < E; ++m) v[m] = valid ? Srow[t + T * m] : cx<C>(R(0), R(0));
-        __syncwarp();
+        wsync();
 #pragma unroll
         for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
-        __syncwarp();
+        wsync();
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int hh = t + T * m;
@@ -117,7 +123,7 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
                 v[m] = cx<C>(a.x - bb.y, a.y + bb.x);        // A + i B
             }
         }
-        __syncwarp();
+        wsync();
         fft_regs<Nh, E, N, false>(v, t, buf, pad, xline_tw<R, false>(tw, tw4), wsync);
         const R sc = R(p.scale);
         if (valid)
@@ -132,12 +138,12 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
             const int pp = t + T * m;
             v[m] = valid ? *reinterpret_cast<const C*>(xrow + 2 * pp) : cx<C>(R(0), R(0));
         }
-        __syncwarp();
+        wsync();
         fft_regs<Nh, E, N, true>(v, t, buf, pad, xline_tw<R, true>(tw, tw4), wsync);
-        __syncwarp();
+        wsync();
 #pragma unroll
         for (int m = 0; m < E; ++m) buf[pad(t + T * m)] = v[m];
-        __syncwarp();
+        wsync();
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int hh = t + T * m;
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(XGeo<R, N>::NT, XGeo<R, N>::MINB) xfft_kernel(
             if (valid) Srow[hh] = out;
         }
     }
-    __syncwarp();
+    wsync();
     }
 }
 

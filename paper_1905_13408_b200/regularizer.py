@@ -215,16 +215,20 @@ def default_precision() -> int:
 
 
 class Context:
-    """One cm_ctx: a side length, a precision, one GPU; resident data in HBM."""
+    """One cm_ctx: a side length, a precision, one GPU (or, with `devices`, the
+    z-slab solver over several GPUs of the box; all ids equal: ranks emulated
+    on that GPU); resident data in HBM."""
 
-    def __init__(self, n: int, precision: int | None = None, device: int = 0):
+    def __init__(self, n: int, precision: int | None = None, device: int = 0,
+                 devices: list[int] | None = None):
         lib = _lib.load()
         self.lib = lib
         self.n = int(n)
         self.precision = int(precision or default_precision())
         ptr = C.c_void_p()
-        dev = (C.c_int * 1)(device)
-        _check(lib.cm_ctx_create(self.n, dev, 1, self.precision, C.byref(ptr)))
+        ids = list(devices) if devices else [device]
+        dev = (C.c_int * len(ids))(*ids)
+        _check(lib.cm_ctx_create(self.n, dev, len(ids), self.precision, C.byref(ptr)))
         self.ptr = ptr
         self._acc_key = None
 

@@ -340,3 +340,52 @@ def test_slab_synthetic_problem_is_decomposition_independent():
     assert abs(out[0][0] - out[1][0]) <= 1e-12 * out[0][0]
     assert np.isfinite(out[0][1]).all()
     assert _rel(out[1][1], out[0][1]) <= 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ndev", [2, 4])
+def test_multi_device_context_matches_one_gpu(ndev):
+    """cm_ctx_create with ndev > 1 (the drop-in's multi-GPU path, CM_DEVICES in
+    the C++ adapter): the z-slab runtime behind the ordinary cm_m_step /
+    cm_scale_data entry points. With every device id equal the ranks are
+    emulated on one GPU (the configuration a one-GPU box can run); the result
+    and trace equal the one-GPU solver's."""
+    import paper_1905_13408_b200 as cm
+    from paper_1905_13408_b200 import synth
+    n = 256
+    p = synth.synthetic_problem(n)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    one = cm.Context(n, 32)
+    one.set_accumulator(acc)
+    s1 = one.scale_data()
+    cfg = cm.derive_config(s1.s_y, s1.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 6
+    out1 = np.empty((n, n, n))
+    t1 = []
+    one.set_volumes(p.x0, p.x0)
+    one.solve(cfg, t1)
+    out1 = one.get_volume()
+    one.close()
+    multi = cm.Context(n, 32, devices=[0] * ndev)
+    multi.set_accumulator(acc)
+    s2 = multi.scale_data()
+    np.testing.assert_allclose([s2.s_y, s2.s_n], [s1.s_y, s1.s_n], rtol=1e-12)
+    outm = np.empty((n, n, n))
+    st = multi.m_step_host(acc, p.x0, p.x0, cfg, outm)
+    multi.close()
+    assert st.iterations == 6
+    assert np.linalg.norm(outm - out1) / np.linalg.norm(out1) <= 1e-6
+
+
+def test_multi_device_context_rejects_bad_layouts():
+    """Host-side checks of cm_ctx_create(ndev > 1) (no device touched)."""
+    import ctypes as C
+    from paper_1905_13408_b200 import _lib
+    lib = _lib.load()
+    ptr = C.c_void_p()
+    for n, devs, prec, why in [(256, [0, 1, 1], 32, "n / ndev"), (100, [0, 1], 32, "n % 128"),
+                               (256, [0, 0], 64, "precision 32"),
+                               (512, [0, 1, 1, 2], 32, "all distinct")]:
+        arr = (C.c_int * len(devs))(*devs)
+        assert lib.cm_ctx_create(n, arr, len(devs), prec, C.byref(ptr)) != 0
+        assert why in lib.cm_last_error().decode(), (n, devs, lib.cm_last_error())
