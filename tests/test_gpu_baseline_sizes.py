@@ -132,3 +132,38 @@ def test_config3_512cubed_first_iterations_vs_reference():
     check_trace(trace, G["c3_per_inner_trace"], TOL[32]["obj"])
     assert rel(x.reshape(-1)[sample_index(512)], G["c3_per_inner_xsample"]) <= TOL[32]["vol"]
     assert abs(np.linalg.norm(x) / G["c3_per_inner_norm"][0] - 1) <= 1e-5
+
+
+def test_radix5_side_320_vs_unmodified_reference(monkeypatch):
+    """A common cryo-EM box with a factor 5 (320 = 2^6 * 5: radix-5 stages in
+    every transform) through the C ABI the drop-in adapter calls, against the
+    UNMODIFIED reference m_step run live (oracle/_ref): reference default
+    semantics, 2 iterations, fp32 bar."""
+    from oracle_lib import Reference, have_reference, make_cfg
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    monkeypatch.setenv("CM_REF_FFT_THREADS", "8")  # the reference's FFT backend threads only
+    n = 320
+    p = synth.synthetic_problem(n)
+    R = Reference()
+    rc, sy, sn = R.scale_data(p.weight, p.numerator)
+    assert rc == 0
+    rc, base = R.derive_config(sy, sn, p.eps, p.eps_prime)
+    c = make_cfg(alpha=base.alpha, beta=base.beta, gamma=base.gamma, eps=base.eps,
+                 eps_prime=base.eps_prime, mu=base.mu, inner_iters=2)
+    rc, xr, trr = R.m_step(p.weight, p.numerator, p.x0, p.x0, c)
+    assert rc == 0, R.last_error()
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    ctx = cm.Context(n, 32)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    np.testing.assert_allclose([s.s_y, s.s_n], [sy, sn], rtol=1e-12)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 2
+    trace = []
+    ctx.set_volumes(p.x0, p.x0)
+    ctx.solve(cfg, trace)
+    x = ctx.get_volume()
+    ctx.close()
+    check_trace(trace, trr, TOL[32]["obj"])
+    assert rel(x, xr) <= TOL[32]["vol"]
