@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     }
     // two accumulator pairs (even / odd m): half-length dependency chains
     R quad = R(0), cross = R(0), quad1 = R(0), cross1 = R(0);
+    const size_t lplane = opaque(plane);
     if (h == 0) {
 #pragma unroll
         for (int m = 0; m < E; ++m) p.Z0[(size_t)b * N + t + T * m] = v[m];
@@ -175,7 +176,10 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
             if constexpr (!PREFETCH) {
 #pragma unroll
                 for (int m = g0; m < g0 + G; ++m) {
-                    const size_t gi = wy_index(t + T * m);
+                    // b-slab layout through the opaque plane stride (the addresses
+                    // are recomputed, not held live: spills at 128 registers)
+                    const size_t gi = NR != 0 ? wy_index(t + T * m)
+                                              : (size_t)(t + T * m) * lplane + (size_t)b * hl + hloc;
                     w[m] = __ldg(p.W + gi);
                     y[m] = p.Yh[gi];
                 }
@@ -183,7 +187,8 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
 #pragma unroll
             for (int m = g0; m < g0 + G; ++m) {
                 const C f = v[m];
-                if (m & 1) {
+                // E = 32 (one warp per column at 1024) has no registers to spare
+                if ((m & 1) && E <= 16 && NR != 0) {
                     quad1 += w[m] * (f.x * f.x + f.y * f.y);
                     cross1 += y[m].x * f.x + y[m].y * f.y;
                 } else {
