@@ -363,8 +363,16 @@ xline_kernel(XParams<R> p) {
                     acc[0] += (double)wl1 * ax;
                     acc[1] += (double)wtv * hb;
                     acc[2] += (double)wtv * (double)gn;
-                    acc[3] += (double)log(fabs(xc) + eps);
-                    acc[4] += (double)log(gn + epsp);
+                    // log-norms: the fp32 product mode evaluates the logs in fp32 (MUFU,
+                    // ~1 ulp; fp64 log on every voxel made this epilogue 13% of HBM peak),
+                    // the fp64 parity mode in fp64
+                    if constexpr (sizeof(R) == 4) {
+                        acc[3] += (double)__logf(fabsf(xc) + eps);
+                        acc[4] += (double)__logf(gn + epsp);
+                    } else {
+                        acc[3] += (double)log(fabs(xc) + eps);
+                        acc[4] += (double)log(gn + epsp);
+                    }
                     const double dd = (double)xc - (double)av;
                     acc[5] += dd * dd;
                     if (p.xprev) {
@@ -372,11 +380,11 @@ xline_kernel(XParams<R> p) {
                         const R pc = P.at(i, j, k);
                         R e1, e2, e3;
                         grad3(P, i, j, k, pc, e1, e2, e3);
-                        const double pl1 = 1.0 / (fabs((double)pc) + p.eps);
-                        const double ptv = 1.0 / ((double)rnorm3(e1, e2, e3) + p.eps_prime);
-                        acc[6] += pl1 * ax;
-                        acc[7] += ptv * hb;
-                        acc[8] += ptv * (double)gn;
+                        const R pl1 = R(1) / (fabs(pc) + eps);
+                        const R ptv = R(1) / (rnorm3(e1, e2, e3) + epsp);
+                        acc[6] += (double)pl1 * ax;
+                        acc[7] += (double)ptv * hb;
+                        acc[8] += (double)ptv * (double)gn;
                     }
                 }
             }

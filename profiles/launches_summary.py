@@ -20,7 +20,8 @@ for r in rows:
     acc[name][d["Metric Name"]].append(float(d["Metric Value"].replace(",", "")))
 
 MAP = [(r"zmain_kernel<\w+, \d+, 0[,>]", "z_pass"), (r"zcol0_kernel<\w+, \d+, 0[,>]", "z_pass"),
-       (r"ypass_kernel<\w+, \d+, 0[,>]", "y_inverse"), (r"xfft_kernel<\w+, \d+, 0[,>]", "x_c2r"),
+       (r"ypass_kernel<\w+, \d+, 0[,>]", "y_inverse"), (r"ytma_kernel<\d+, (false|0)>", "y_inverse"),
+       (r"ytma_kernel<\d+, (true|1)>", "y_forward"), (r"xfft_kernel<\w+, \d+, 0[,>]", "x_c2r"),
        (r"stencil2?_kernel", "stencil"), (r"^finalize_kernel", "finalize"),
        (r"xfft_kernel<\w+, \d+, 1[,>]", "x_r2c"), (r"ypass_kernel<\w+, \d+, 1[,>]", "y_forward")]
 per = collections.defaultdict(lambda: {"time_us": 0.0, "dram_bytes": 0.0, "launches": 0})
