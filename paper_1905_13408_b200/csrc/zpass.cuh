@@ -55,6 +55,9 @@ template <typename R> struct ZMParams {
 #ifndef CM_Z_TW
 #define CM_Z_TW 0  // columns per CTA (0: 16, capped at 1024 threads)
 #endif
+#ifndef CM_Z_WBULK
+#define CM_Z_WBULK 0  // measured slower at 512^3 (0.49 vs 0.43 ms): opt-in build flag
+#endif
 
 template <typename R, int N> struct ZGeo {
     // 8 elements per thread for power-of-two sides >= 256 so that W and Yh of
@@ -76,8 +79,14 @@ template <typename R, int N> struct ZGeo {
     static constexpr int TW = E8 ? (TWMAX < 1024 / T ? TWMAX : 1024 / T) : Geo<R, N>::TWY;
     static constexpr int NT = TW * T;
     static constexpr int NBM = (N / 2 / TW) * N;  // main blocks
-    static constexpr size_t SMEM_MAIN =
+    static constexpr size_t SMEM_MAIN0 =
         sizeof(Cx<R>) * (N + (size_t)N * TW) + sizeof(double) * 64 + packed_tw_bytes<R>(N, 2);
+    // one GPU, 16-element plan: the CTA's W tile (contiguous in the z-tiled
+    // layout) arrives by one cp.async.bulk issued at CTA start, into shared
+    // memory next to the exchange buffer; two CTAs per SM still fit
+    static constexpr bool WBULK = CM_Z_WBULK && E16 && !E32 && sizeof(R) == 4;
+    static constexpr size_t OFF_WB = (SMEM_MAIN0 + 127) / 128 * 128;
+    static constexpr size_t SMEM_MAIN = WBULK ? OFF_WB + (size_t)N * TW * 4 + 8 : SMEM_MAIN0;
     static constexpr int MINB = (NT >= 1024 || E32) ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
     // column-0 kernel: 8 elements per thread on power-of-two sides >= 256 (more
     // warps per pair block: the kernel is latency bound with 257 blocks)
@@ -128,6 +137,22 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
     const int b = tile / NTX;  // local row
     const size_t plane = (size_t)nrows * hl;
     C* base = p.S + (size_t)b * hl + hloc;
+    constexpr bool WB = ZGeo<R, N>::WBULK && NR != 0 && MODE != ZM_FWD;
+    const float* wsm = reinterpret_cast<const float*>(smem_raw + ZGeo<R, N>::OFF_WB);
+    const uint32_t wbar = smem_u32(smem_raw + ZGeo<R, N>::OFF_WB + (size_t)N * TW * 4);
+    if constexpr (WB) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wbar));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx_s(wbar, (uint32_t)(N * TW * 4));
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(smem_raw + ZGeo<R, N>::OFF_WB)),
+                "l"(reinterpret_cast<uint64_t>(p.W + (size_t)tile * N * TW)), "r"((uint32_t)(N * TW * 4)),
+                "r"(wbar)
+                : "memory");
+        }
+    }
     C v[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = base[(size_t)(t + T * m) * plane];
@@ -175,12 +200,13 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         for (int g0 = 0; g0 < E; g0 += G) {
             if constexpr (!PREFETCH) {
 #pragma unroll
+                if (WB && g0 == 0) mbar_wait_s(wbar, 0);  // the W tile landed during the forward FFT
                 for (int m = g0; m < g0 + G; ++m) {
                     // b-slab layout through the opaque plane stride (the addresses
                     // are recomputed, not held live: spills at 128 registers)
                     const size_t gi = NR != 0 ? wy_index(t + T * m)
                                               : (size_t)(t + T * m) * lplane + (size_t)b * hl + hloc;
-                    w[m] = __ldg(p.W + gi);
+                    w[m] = WB ? wsm[(t + T * m) * TW + col] : __ldg(p.W + gi);
                     y[m] = p.Yh[gi];
                 }
             }
