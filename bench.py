@@ -649,18 +649,23 @@ def run_ours(args):
     # a 3e-7 frozen-weight surrogate decrease to get to 0.99%.
     ttt = None
     if args.ttt:
-        ttt = {"definition": "rel. error <= 1e-2 vs converged solution (profiles/r1_convergence_512.json)"}
-        for name, extra in (("fista", dict(momentum=1, tol_kind=2, tol=0.03)),
-                            ("ista", dict(momentum=0, tol_kind=1, tol=3e-7))):
-            tc = cm.RegConfig(**{**cfg.__dict__, "inner_iters": args.ttt_max_iters,
-                                 "refresh": cm.Refresh.per_m_step, **extra})
+        ttt = {"definition": "rel. L2 error <= 1e-2 vs the converged solution of the same "
+                             "subproblem (BASELINE.md section 4; calibration profiles/r2_ttt.json)"}
+        for name, extra in (("fista", dict(momentum=1, tol_kind=2, tol=0.03,
+                                           refresh=cm.Refresh.per_m_step)),
+                            ("ista", dict(momentum=0, tol_kind=1, tol=3e-7,
+                                          refresh=cm.Refresh.per_m_step)),
+                            ("ista_per_inner", dict(momentum=0, tol_kind=1, tol=1e-7,
+                                                    refresh=cm.Refresh.per_inner))):
+            tc = cm.RegConfig(**{**cfg.__dict__, "inner_iters": args.ttt_max_iters, **extra})
             torch.cuda.synchronize()
             st = ctx.solve(tc)
             ttt[name] = {"iterations": st.iterations, "seconds": st.solve_ms / 1e3,
                          "stop_reason": st.stop_reason, "last_rel": st.last_rel,
                          "criterion": ("step norm < 3% of the largest step" if name == "fista"
-                                       else "frozen-weight surrogate relative decrease < 3e-7"),
-                         "refresh": "per_m_step"}
+                                       else f"surrogate relative decrease < {extra['tol']:g}"),
+                         "refresh": ("per_inner (the reference's semantics)"
+                                     if name == "ista_per_inner" else "per_m_step")}
             if e2e is not None and name == "fista":
                 # the same solve through cm_m_step on pinned host buffers: fp64 full-grid
                 # accumulator + volume H2D, result D2H ("including H2D")
