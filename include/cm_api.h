@@ -61,7 +61,10 @@ typedef struct {
     int refresh;                 /* 0 per_inner, 1 per_m_step */
     int convex_mode;
     /* ---- extensions ---- */
-    int momentum;                /* 0 ISTA (reference), 1 FISTA (no monotone audit) */
+    int momentum;                /* 0 ISTA (reference), 1 FISTA (no monotone audit),
+                                    2 FISTA with gradient-based adaptive restart
+                                    (O'Donoghue & Candes: the momentum restarts when
+                                    (y_k - x_{k+1}) . (x_{k+1} - x_k) > 0) */
     int tol_kind;                /* 0 none, 1 frozen-weight surrogate relative decrease,
                                     2 step norm ||x+ - x|| relative to the largest step
                                       so far (works with FISTA) */

@@ -116,6 +116,9 @@ struct DevState {
     double before[7];   // before_i of the iteration being audited (saved by finalize)
     double last_rel;    // last tolerance measure
     double step_max;    // largest ||x_{k+1} - x_k|| seen (tol_kind 2 normaliser)
+    int restart;        // FISTA with gradient-based adaptive restart (momentum 2)
+    int mom_base;       // iteration of the last restart: theta index = iter - mom_base
+    int restarts;       // restarts taken
 };
 
 // a value the compiler cannot see through (forces recomputation of addresses

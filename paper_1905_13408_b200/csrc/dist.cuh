@@ -684,7 +684,7 @@ struct DistImpl final : DistBase {
             return fail(CM_ERR_NON_HERMITIAN, "accumulator is not Friedel-finalized");
         if (!vol_set) return fail(CM_ERR_STATE, "volumes not set");
         const int K = c->inner_iters;
-        const bool lipschitz = c->step_rule == 0, fista = c->momentum == 1;
+        const bool lipschitz = c->step_rule == 0, fista = c->momentum >= 1;
         const bool convex = c->convex_mode != 0;
         const bool want_trace = trace && cap > 0;
         const bool audit = !fista && (lipschitz || want_trace || c->tol_kind == 1);
@@ -698,7 +698,7 @@ struct DistImpl final : DistBase {
                                     : c->fixed_step;
         const double slack = c->audit_slack > 0.0 ? c->audit_slack : 1e-6;
         const int tol_kind = (fista && c->tol_kind == 1) ? 2 : c->tol_kind;
-        const bool need_part1 = audit || tol_kind == 2;
+        const bool need_part1 = audit || tol_kind == 2 || c->momentum == 2;
         const int nb3 = (Nh / ZG::TW) * NB + NB;
         result_valid = false;
 
@@ -749,6 +749,7 @@ struct DistImpl final : DistBase {
             hs.check_diverge = audit && lipschitz;
             hs.tol_kind = tol_kind;
             hs.fista = fista;
+            hs.restart = c->momentum == 2;
             hs.refresh_inner = refresh_inner;
             hs.tol = c->tol;
             hs.audit_slack = slack;

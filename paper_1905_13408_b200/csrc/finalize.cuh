@@ -131,6 +131,12 @@ static __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinParams 
         if (p.epilogue) return;
         for (int q = 0; q < 7; ++q) S.before[q] = cur[q];
         S.iter = i + 1;
+        if (S.fista && S.restart && s[11] > 0.0) {
+            // gradient restart: the momentum sequence starts over at the next
+            // iteration (theta index iter - mom_base = 0: no momentum)
+            S.mom_base = S.iter;
+            ++S.restarts;
+        }
         if (S.tol_kind == 2) {
             // scale-free step rule: ||x_{k+1} - x_k|| relative to the largest step so
             // far (the first steps are tiny under the Lipschitz step of the TV term)

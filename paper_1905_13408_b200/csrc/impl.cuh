@@ -312,7 +312,7 @@ inline int validate(const cm_reg_config* c) {
         return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown step rule");
     if (c->refresh != 0 && c->refresh != 1)
         return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown refresh mode");
-    if (c->momentum != 0 && c->momentum != 1)
+    if (c->momentum < 0 || c->momentum > 2)
         return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown momentum mode");
     if (c->tol_kind < 0 || c->tol_kind > 2)
         return fail(CM_ERR_INVALID_ARGUMENT, "regularizer: unknown tolerance kind");
@@ -856,7 +856,7 @@ struct Impl final : ImplBase {
         if (!vol_set) return fail(CM_ERR_STATE, "volumes not set");
         const int K = c->inner_iters;
         const bool lipschitz = c->step_rule == 0;
-        const bool fista = c->momentum == 1;
+        const bool fista = c->momentum >= 1;
         const bool convex = c->convex_mode != 0;
         const bool want_trace = trace != nullptr && cap > 0;
         const bool audit = !fista && (lipschitz || want_trace || c->tol_kind == 1);
@@ -937,13 +937,16 @@ struct Impl final : ImplBase {
         hs.tol_kind = c->tol_kind;
         if (fista && hs.tol_kind == 1) hs.tol_kind = 2; // no surrogate audit under momentum
         hs.fista = fista;
+        hs.restart = c->momentum == 2;
+        hs.mom_base = 0;
+        hs.restarts = 0;
         hs.refresh_inner = refresh_inner;
         hs.tol = c->tol;
         hs.audit_slack = slack;
         hs.step = lr;
         CK(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, stream));
 
-        const bool need_part1 = audit || hs.tol_kind == 2;
+        const bool need_part1 = audit || hs.tol_kind == 2 || hs.restart;
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));

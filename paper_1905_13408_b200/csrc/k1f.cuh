@@ -403,7 +403,7 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
         const bool has_beta = p.beta > 0.0, has_alpha = p.alpha > 0.0;
         constexpr bool with_prev = PREV;
         const bool convex = p.convex != 0;
-        const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter]) : 0.f;
+        const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter - p.st->mom_base]) : 0.f;
         float fa[NP1], fb[NP1];
 #pragma unroll
         for (int q = 0; q < NP1; ++q) fa[q] = fb[q] = 0.f;
@@ -637,6 +637,10 @@ k1f_kernel(StencilParams<float> p, float2* __restrict__ S, const float2* __restr
                             fa[9] += dx * dx;
                             fa[10] += nx[c] * nx[c];
                         }
+                    }
+                    if (FISTA) {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) fa[11] += (x_cur[c] - nx[c]) * (nx[c] - base[c]);
                     }
                     if (AUDIT) {
                         float pl1[4] = {0.f, 0.f, 0.f, 0.f}, ptv[4] = {0.f, 0.f, 0.f, 0.f};

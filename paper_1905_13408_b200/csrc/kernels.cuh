@@ -27,7 +27,7 @@ namespace cm {
 enum XMode { XM_OBJ = 2, XM_TVGRAD = 4, XM_WEIGHTS = 5 };
 enum ZMode { ZM_FULL = 0, ZM_FIT = 1, ZM_FWD = 2 };
 
-constexpr int NP1 = 11; // xline partial slots
+constexpr int NP1 = 12; // xline partial slots (11: FISTA restart test)
 constexpr int NP3 = 2;  // zpass partial slots
 
 // ---- compile-time geometry ----------------------------------------------------

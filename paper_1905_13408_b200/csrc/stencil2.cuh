@@ -73,7 +73,7 @@ __host__ __device__ constexpr unsigned s2_used(int F) {
     return ((F & S2_AUDIT) ? (1u | 2u | 32u | ((F & S2_PREV) ? 64u | 128u : 0u) |
                               ((F & S2_TRACE) ? 4u | 8u | 16u | ((F & S2_PREV) ? 256u : 0u) : 0u))
                            : 0u) |
-           ((F & S2_STEP) ? 512u | 1024u : 0u);
+           ((F & S2_STEP) ? 512u | 1024u : 0u) | ((F & S2_FISTA) ? 2048u : 0u);
 }
 
 template <int N, int F>
@@ -105,7 +105,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     constexpr bool with_prev = PREV;
     const bool convex = p.convex != 0;
     // s = 1/((g cg + ce) max(mu, g)): (cg, ce) = (1, eps') reweighted, (0, 1) convex
-    const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter]) : 0.f;
+    const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter - p.st->mom_base]) : 0.f;
 
     if (tid == 0) {
         for (int q = 0; q < G::NSTAGE; ++q) mbar_init(&bar[q], 1);
@@ -342,6 +342,11 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
 #pragma unroll
                     for (int c = 0; c < 4; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
                     *reinterpret_cast<float4*>(p.ynext + gidx) = make_float4(y[0], y[1], y[2], y[3]);
+                }
+                if (FISTA) {
+                    // restart test (O'Donoghue & Candes): (y_k - x_{k+1}) . (x_{k+1} - x_k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fa[11] += (x_cur[c] - nx[c]) * (nx[c] - base[c]);
                 }
                 if (STEP) {
 #pragma unroll

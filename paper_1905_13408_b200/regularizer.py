@@ -97,7 +97,7 @@ class RegConfig:
     refresh: Refresh = Refresh.per_inner
     convex_mode: bool = False
     # extensions (defaults reproduce the reference)
-    momentum: int = 0        # 1 = FISTA
+    momentum: int = 0        # 1 = FISTA, 2 = FISTA with gradient adaptive restart
     tol_kind: int = 0        # 1 surrogate relative decrease, 2 step norm / max step
     tol: float = 0.0
     audit_slack: float = 0.0  # <= 0: 1e-9 (fp64) / 1e-6 (fp32)

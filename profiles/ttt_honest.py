@@ -63,7 +63,8 @@ p, ctx, base = problem(n)
 for label, refresh, momentum, kind, taus in (
         ("ista_per_inner", cm.Refresh.per_inner, 0, 1, [1e-5, 3e-6, 1e-6, 3e-7, 1e-7]),
         ("ista_per_m_step", cm.Refresh.per_m_step, 0, 1, [1e-6, 3e-7, 1e-7]),
-        ("fista_per_m_step", cm.Refresh.per_m_step, 1, 2, [1e-1, 3e-2, 1e-2])):
+        ("fista_per_m_step", cm.Refresh.per_m_step, 1, 2, [1e-1, 3e-2, 1e-2]),
+        ("fista_restart_per_m_step", cm.Refresh.per_m_step, 2, 2, [1e-1, 3e-2, 1e-2])):
     xs, st = solve(ctx, base, inner_iters=ref_iters, refresh=refresh, momentum=momentum)
     rows = []
     for tau in taus:

@@ -287,6 +287,36 @@ def test_fista_reaches_the_ista_fixed_point(prec):
     assert rel_l2(xf, xi) < 2e-4
 
 
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("n", [16, 128])
+def test_fista_restart_reaches_the_ista_fixed_point_faster(n, prec):
+    """FISTA with gradient-based adaptive restart (momentum = 2) converges to
+    the same fixed point as long ISTA, and reaches the step-norm rule in no
+    more iterations than plain FISTA."""
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=prec)
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    base.beta *= 0.01
+    ista = cm.RegConfig(**{**base.__dict__, "inner_iters": 20000, "refresh": cm.Refresh.per_m_step,
+                           "step_rule": cm.StepRule.fixed})
+    lr = 1.0 / (2.0 * p.weight.max() + 2.0 * base.gamma + 12.0 * base.beta / base.eps_prime / base.mu)
+    ista.fixed_step = lr
+    xi = cm.m_step(acc, p.x0, p.x0, ista, precision=prec)
+    fr = cm.RegConfig(**{**ista.__dict__, "inner_iters": 3000, "momentum": 2})
+    xr = cm.m_step(acc, p.x0, p.x0, fr, precision=prec)
+    assert rel_l2(xr, xi) < 2e-4
+    stops = {}
+    for mom in (1, 2):
+        c = cm.RegConfig(**{**ista.__dict__, "inner_iters": 20000, "momentum": mom, "tol_kind": 2,
+                            "tol": 1e-3})
+        st = {}
+        cm.m_step(acc, p.x0, p.x0, c, precision=prec, stats=st)
+        assert st["stop_reason"] == 2
+        stops[mom] = st["iterations"]
+    assert stops[2] <= stops[1], stops
+
+
 def test_tolerance_stop_matches_oracle_trace(O):
     """tol_kind=1 stops at the first iteration whose frozen-weight surrogate
     decrease falls below tol; the returned volume is that iterate."""
