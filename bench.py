@@ -653,6 +653,8 @@ def run_ours(args):
                              "subproblem (BASELINE.md section 4; calibration profiles/r2_ttt.json)"}
         for name, extra in (("fista", dict(momentum=1, tol_kind=2, tol=0.03,
                                            refresh=cm.Refresh.per_m_step)),
+                            ("fista_restart", dict(momentum=2, tol_kind=2, tol=0.03,
+                                                   refresh=cm.Refresh.per_m_step)),
                             ("ista", dict(momentum=0, tol_kind=1, tol=3e-7,
                                           refresh=cm.Refresh.per_m_step)),
                             ("ista_per_inner", dict(momentum=0, tol_kind=1, tol=1e-7,
@@ -662,7 +664,7 @@ def run_ours(args):
             st = ctx.solve(tc)
             ttt[name] = {"iterations": st.iterations, "seconds": st.solve_ms / 1e3,
                          "stop_reason": st.stop_reason, "last_rel": st.last_rel,
-                         "criterion": ("step norm < 3% of the largest step" if name == "fista"
+                         "criterion": ("step norm < 3% of the largest step" if name.startswith("fista")
                                        else f"surrogate relative decrease < {extra['tol']:g}"),
                          "refresh": ("per_inner (the reference's semantics)"
                                      if name == "ista_per_inner" else "per_m_step")}
