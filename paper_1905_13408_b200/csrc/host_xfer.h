@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -31,7 +32,11 @@ struct HostXfer {
     static constexpr int kBufs = 3;
     unsigned char* buf[kBufs] = {};
     cudaEvent_t done[kBufs] = {};
-    int threads = std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+    // host copy threads: CM_XFER_THREADS, default half the hardware threads (<= 16)
+    int threads = []() {
+        if (const char* e = std::getenv("CM_XFER_THREADS")) return std::max(1, std::atoi(e));
+        return (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency() / 2));
+    }();
 
     ~HostXfer() {
         for (int q = 0; q < kBufs; ++q) {
