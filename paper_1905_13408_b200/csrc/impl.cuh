@@ -46,6 +46,7 @@ int fail(int code, const std::string& msg);
 } // namespace cm
 #include "ypass_tma.cuh"
 #include "k1f.cuh"
+#include "yzy.cuh"
 namespace cm {
 
 #define CK(call)                                                                         \
@@ -401,6 +402,12 @@ struct Impl final : ImplBase {
     int sweep_grid = 0;        // persistent stencil CTAs
     int xfft_grid = 0;         // persistent x-line transform CTAs
     int ygrid = 1, zgrid = 1;  // persistent y-pass / z-pass CTAs
+    // y forward + z + y inverse pipelined through L2 in one kernel (yzy.cuh); CM_YZY
+    static constexpr bool YZY = std::is_same<R, float>::value && YzyGeo<N>::OK;
+    bool use_yzy = false;
+    int yzy_grid = 0;
+    int4* yzy_items_d = nullptr;
+    int* yzy_ctr = nullptr;
     // fused K1 (k1f.cuh): x C2R + stencil + x R2C in one cluster kernel; opt-in CM_K1F=1
     static constexpr bool K1F = std::is_same<R, float>::value && K1Geo<N>::OK;
     bool use_k1f = false;
@@ -458,7 +465,7 @@ struct Impl final : ImplBase {
         if (gexec) cudaGraphExecDestroy(gexec);
         void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, gbuf, S, W,
                       Wn, Yh, Yn, Z0, twN, twF4, twI4, stage, part1, part3, part_acc, maxes, st, trace_d,
-                      theta_d, Q0, fcnt};
+                      theta_d, Q0, fcnt, yzy_items_d, yzy_ctr};
         for (void* p : ps)
             if (p) cudaFree(p);
         if (flags_h) cudaFreeHost(flags_h);
@@ -620,6 +627,22 @@ struct Impl final : ImplBase {
             s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
         }
         CKS(dalloc(&part3, (size_t)NB3 * NP3));
+        if constexpr (YZY) {
+            const char* e = std::getenv("CM_YZY");
+            use_yzy = e && e[0] == '1';
+            CK(cudaFuncSetAttribute(yzy_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)YzyGeo<N>::SMEM));
+            int occ = 0, dev = 0, sms = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, yzy_kernel<N>, YzyGeo<N>::NT,
+                                                             YzyGeo<N>::SMEM));
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            yzy_grid = sms * std::max(occ, 1);
+            const std::vector<int4> items = yzy_items<N>();
+            CKS(dalloc(&yzy_items_d, items.size()));
+            CK(cudaMemcpy(yzy_items_d, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+            CKS(dalloc(&yzy_ctr, YzyGeo<N>::NCTR));
+        }
         if constexpr (K1F) {
             // opt-in (CM_K1F=1): measured 1.40 ms per 512^3 sweep against 0.96 ms for the
             // three separate kernels (one line per CTA-plane leaves the
@@ -774,6 +797,16 @@ struct Impl final : ImplBase {
         if constexpr (MODE != ZM_FWD)
             CK(launch_pdl(use_pdl, zcol0_kernel<R, N, MODE>, dim3(N / 2 + 1), dim3(ZG::NT0),
                           ZG::SMEM_COL0, stream, p));
+        return CM_OK;
+    }
+    // y forward (of the spectrum in S) + z pass + y inverse, one launch (yzy.cuh)
+    int launch_yzy(double* part, DevState* s) {
+        if constexpr (YZY) {
+            ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
+            CK(cudaMemsetAsync(yzy_ctr, 0, sizeof(int) * YzyGeo<N>::NCTR, stream));
+            yzy_kernel<N><<<yzy_grid, YzyGeo<N>::NT, YzyGeo<N>::SMEM, stream>>>(p, yzy_items_d, yzy_ctr);
+            CK(cudaGetLastError());
+        }
         return CM_OK;
     }
     int upload_real(const double* host, R* dst) {
@@ -953,8 +986,14 @@ struct Impl final : ImplBase {
         CK(cudaEventRecord(e0, stream));
         int launches = 0;
 
-        // spectrum of the starting point: x R2C, y forward
-        if (use_fused) {
+        // spectrum of the starting point: x R2C, y forward (yzy: + z and y inverse
+        // of iteration 0)
+        const bool yzy = YZY && use_yzy && !use_fused && !profiling;
+        if (yzy) {
+            CKS(launch_xfft(1, fista ? YF[0] : X[0], nullptr));
+            CKS(launch_yzy(audit ? part3 : nullptr, st));
+            launches += 2;
+        } else if (use_fused) {
             CKS(launch_fused(1, fista ? YF[0] : X[0], nullptr));
             launches += 1;
         } else {
@@ -1073,6 +1112,11 @@ struct Impl final : ImplBase {
             return CM_OK;
         };
         auto iteration = [&](int g) -> int {
+            if (yzy) {  // z + y inverse ran in the previous yzy launch
+                CKS(sweep_and_finalize(g, nullptr));                // K1 + FIN
+                CKS(launch_yzy(audit ? part3 : nullptr, st));      // K2 + next K3 + K4
+                return CM_OK;
+            }
             CKS(launch_z<ZM_FULL>(audit ? part3 : nullptr, st));  // K3
             if (use_fused) CKS(launch_fused(0, gbuf, &st->done));  // K4 + K1a
             else CKS(launch_y(false, st));                         // K4
@@ -1081,7 +1125,8 @@ struct Impl final : ImplBase {
             return CM_OK;
         };
 
-        const int per_iter = (use_fused || (K1F && use_k1f)) ? 6 : 8;  // kernels per iteration
+        const int per_iter = yzy ? (K1F && use_k1f ? 3 : 5)
+                                 : (use_fused || (K1F && use_k1f)) ? 6 : 8;  // kernels per iteration
         const bool use_graph = std::getenv("CM_NO_GRAPH") == nullptr && !profiling;
         const int chunk = 6;
         const int nchunks = (K + chunk - 1) / chunk;

@@ -423,6 +423,40 @@ def test_fused_k1_cluster_kernel_matches_separate_passes(n, mode, monkeypatch):
                                [r.after.surrogate() for r in out["0"][1]], rtol=1e-6)
 
 
+@pytest.mark.parametrize("n", [256, 512])
+@pytest.mark.parametrize("mode", ["per_inner", "fista_tol"])
+def test_yzy_l2_pipeline_matches_separate_passes(n, mode, monkeypatch):
+    """The opt-in y-forward + z + y-inverse L2 pipeline (CM_YZY=1, yzy.cuh: one
+    persistent kernel, items claimed in order, per-group completion counters)
+    gives the same iterates, audit trace and stop as the separate passes."""
+    p = synth.synthetic_problem(n)
+    acc = acc_of(p.weight, p.numerator)
+    s = cm.scale_data(acc, precision=32)
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 9
+    if mode == "fista_tol":  # early stop through the device flag inside a graph chunk
+        cfg.refresh = cm.Refresh.per_m_step
+        cfg.momentum = 1
+        cfg.tol_kind = 2
+        cfg.tol = 0.5
+        cfg.inner_iters = 60
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CM_YZY", flag)
+        ctx = cm.Context(n, 32)
+        ctx.set_accumulator(acc)
+        ctx.set_volumes(p.x0, p.x0)
+        tr = []
+        st = ctx.solve(cfg, tr)
+        out[flag] = (ctx.get_volume(), tr, st)
+        ctx.close()
+    assert out["1"][2].iterations == out["0"][2].iterations
+    assert out["1"][2].stop_reason == out["0"][2].stop_reason
+    assert rel_l2(out["1"][0], out["0"][0]) <= 1e-6
+    np.testing.assert_allclose([r.after.surrogate() for r in out["1"][1]],
+                               [r.after.surrogate() for r in out["0"][1]], rtol=1e-6)
+
+
 @pytest.mark.parametrize("prec", [32, 64])
 def test_config2_reweighting_loops_vs_oracle(O, prec):
     """BASELINE config 2 structure: bond-like (chain) phantom, three
