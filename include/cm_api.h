@@ -94,9 +94,15 @@ typedef struct {
 int cm_version(void);
 const char* cm_last_error(void);
 
-/* Side lengths with a compiled plan: 4 6 8 12 16 24 32 48 64 96 128 192 256 384
- * 512 768 1024 (radix 2/3). precision: 32 (fp32 product mode) or 64 (fp64
- * parity mode). devices/ndev: ndev must be 1 (one process per GPU). */
+/* Side lengths with a compiled plan (build.py SIDES): the even 2^a 3^b 5^c 7^d
+ * sides 4 .. 1280 listed there (e.g. 64 100 128 160 200 256 320 360 384 400 512
+ * 640 720 768 800 960 1024 1152 1200 1280); cm_last_error() after a 0 names why
+ * a side is missing (odd, prime factor >= 11, above 1280, or not compiled).
+ * precision: 32 (fp32 product mode) or 64 (fp64 parity mode). devices/ndev:
+ * ndev == 1 is one context on one GPU; ndev > 1 shards the volume in z slabs
+ * over the listed devices (cm_ctx_info, cm_set_accumulator, cm_scale_data,
+ * cm_set_volumes, cm_solve, cm_get_volume and cm_m_step; the other entry points
+ * return CM_ERR_UNSUPPORTED on such a context). */
 int cm_supported_side(int n);
 int cm_ctx_create(int n, const int* devices, int ndev, int precision, cm_ctx** out);
 int cm_ctx_destroy(cm_ctx* ctx);

@@ -22,7 +22,8 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libcm.so"
 
 SIDES = [4, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 100, 112, 128, 160, 192,
-         200, 224, 240, 256, 320, 360, 384, 400, 448, 480, 512, 640, 720, 768, 800, 960, 1024]
+         200, 224, 240, 256, 320, 360, 384, 400, 448, 480, 512, 640, 720, 768, 800, 960, 1024,
+         1152, 1200, 1280]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -25,7 +25,8 @@ int fail(int code, const std::string& msg) {
 
 #define CM_SIDES(X) X(4) X(6) X(8) X(10) X(12) X(14) X(16) X(20) X(24) X(28) X(32) X(40) X(48) \
     X(56) X(64) X(80) X(96) X(100) X(112) X(128) X(160) X(192) X(200) X(224) X(240) X(256) X(320) \
-    X(360) X(384) X(400) X(448) X(480) X(512) X(640) X(720) X(768) X(800) X(960) X(1024)
+    X(360) X(384) X(400) X(448) X(480) X(512) X(640) X(720) X(768) X(800) X(960) X(1024) \
+    X(1152) X(1200) X(1280)
 #define CM_DECL(NN) ImplBase* make_impl_##NN(int precision);
 CM_SIDES(CM_DECL)
 
@@ -126,7 +127,9 @@ static std::string unsupported_side_reason(int n) {
         return "side " + sn + " has the prime factor " + std::to_string(q) +
                ": the FFT engine plans radices 2, 3, 5 and 7 only (no Bluestein stage)";
     }
-    if (n > 1024) return "side " + sn + " exceeds 1024: one GPU's fp32 working set; use the z-slab solver";
+    if (n > 1280)
+        return "side " + sn + " exceeds 1280: N^3 >= 2^31 voxels (the kernels keep 32-bit voxel "
+               "offsets) and one GPU's fp32 working set (~48 N^3 bytes) exceeds its HBM";
     return "side " + sn + " (2^a 3^b 5^c 7^d) is not among the sides compiled into this build "
            "(paper_1905_13408_b200/build.py SIDES, csrc/cm_api.cu CM_SIDES)";
 }

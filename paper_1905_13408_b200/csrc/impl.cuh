@@ -518,9 +518,10 @@ struct Impl final : ImplBase {
             const cuuint64_t strides[2] = {(cuuint64_t)N * sizeof(R), (cuuint64_t)N * N * sizeof(R)};
             const cuuint32_t box[3] = {bw, bj, bk};
             const cuuint32_t es[3] = {1, 1, 1};
-            CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CUresult r = enc(out, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                             3, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map (x) encode failed");
             return CM_OK;
         }

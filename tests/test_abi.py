@@ -31,7 +31,7 @@ def test_supported_sides():
 
 
 @pytest.mark.parametrize("n,why", [(22, "prime factor 11"), (26, "prime factor 13"),
-                                   (7, "must be even"), (2048, "exceeds 1024"),
+                                   (7, "must be even"), (2048, "exceeds 1280"),
                                    (36, "not among the sides compiled")])
 def test_unsupported_side_states_the_reason(n, why):
     """Every even side the reference accepts (volume.hpp:94-97) either has a
