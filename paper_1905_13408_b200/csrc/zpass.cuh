@@ -59,6 +59,9 @@ template <typename R> struct ZMParams {
 #define CM_Z_WBULK 0  // measured slower at 512^3 (0.49 vs 0.43 ms): opt-in build flag
 #endif
 
+#ifndef CM_Z_MINB_D
+#define CM_Z_MINB_D 2
+#endif
 template <typename R, int N> struct ZGeo {
     // 8 elements per thread for power-of-two sides >= 256 so that W and Yh of
     // the whole column fit in registers next to it (prefetched before the
@@ -87,7 +90,10 @@ template <typename R, int N> struct ZGeo {
     static constexpr bool WBULK = CM_Z_WBULK && E16 && !E32 && sizeof(R) == 4;
     static constexpr size_t OFF_WB = (SMEM_MAIN0 + 127) / 128 * 128;
     static constexpr size_t SMEM_MAIN = WBULK ? OFF_WB + (size_t)N * TW * 4 + 8 : SMEM_MAIN0;
-    static constexpr int MINB = (NT >= 1024 || E32) ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
+    // fp64: 16 complex doubles per thread at N >= 512 are 64 registers of data
+    // alone; the fp32 bound of 4 CTAs (64 registers) spilled 1.2 KB per thread
+    static constexpr int MINB = sizeof(R) == 8 ? CM_Z_MINB_D
+                                : (NT >= 1024 || E32) ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
     // column-0 kernel: 8 elements per thread on power-of-two sides >= 256 (more
     // warps per pair block: the kernel is latency bound with 257 blocks)
     static constexpr int E0 = (N >= 256 && (N & (N - 1)) == 0) ? 8 : Geo<R, N>::EY;
