@@ -399,7 +399,31 @@ def big_slab(args, world, rank, local):
             "ms_per_iter": ms_iter, "stop_reason": st.stop_reason,
             "hbm_frac_per_gpu": iter_bytes / (ms_iter / 1e3) / 1e9 / hbm,
             "exchange_bytes_per_rank_per_iter": plan.exchange_bytes_per_iteration(),
+            "model_per_p": slab_model(n, ms_iter * world),
             "data": "device-rendered blob lattice + random symmetric weight (timing only)"}
+
+
+def slab_model(n, compute_ms_1, link_gbs=900.0):
+    """Modelled split of one z-slab iteration at P ranks: compute = the measured
+    one-GPU-equivalent iteration time / P; comm = the bytes each rank sends
+    (SlabPlan.exchange_bytes_per_iteration) at the nominal NVLink 5 rate per
+    direction; 'serial' if no exchange overlaps compute, 'overlapped' if all of it
+    does. Also the accumulator upload per rank (rows + mirrors) against the full
+    grid's 24 n^3 bytes."""
+    from paper_1905_13408_b200.slab import SlabPlan
+
+    out = {}
+    for P in (1, 2, 4, 8):
+        pl = SlabPlan(n, P)
+        if not pl.supported():
+            continue
+        comp = compute_ms_1 / P
+        comm = 0.0 if P == 1 else pl.exchange_bytes_per_iteration() / (link_gbs * 1e9) * 1e3
+        out[str(P)] = {"compute_ms": round(comp, 3), "comm_ms": round(comm, 3),
+                       "serial_ms": round(comp + comm, 3), "overlapped_ms": round(max(comp, comm), 3),
+                       "acc_upload_gb_per_rank": round(pl.acc_upload_bytes(0) / 1e9, 3),
+                       "acc_full_grid_gb": round(24 * n ** 3 / 1e9, 3)}
+    return out
 
 
 def run_slab(args, world, rank, local):

@@ -282,8 +282,15 @@ int cm_dctx_create(int n, int world, int rank, int device, const unsigned char* 
 int cm_dctx_destroy(cm_dctx* d);
 /* planes per rank, first plane of this process, ranks hosted by this process */
 int cm_dctx_layout(const cm_dctx* d, int* planes_per_rank, int* first_plane, int* ranks_here);
+/* Each rank uploads only the accumulator rows its b-slab reads (its spectrum
+ * rows b and their mirrors N - b: about 2/P of the 24 N^3 bytes, staged from the
+ * caller's pageable arrays through a pinned ring); the full-grid statistics
+ * (scale_data, residue) are per-row partials all-gathered and summed in row
+ * order, identical on every rank and for every P. */
 int cm_dctx_set_accumulator(cm_dctx* d, const double* weight, const double* numerator,
                             int finalized);
+/* host-to-device bytes of this process's last cm_dctx_set_accumulator */
+int cm_dctx_upload_bytes(const cm_dctx* d, long long* acc_h2d_bytes);
 int cm_dctx_set_volumes(cm_dctx* d, const double* x_init, const double* x_anchor);
 int cm_dctx_solve(cm_dctx* d, const cm_reg_config* cfg, cm_trace_row* trace, int trace_cap,
                   cm_solve_stats* stats);

@@ -101,6 +101,7 @@ def load() -> C.CDLL:
         "cm_dctx_destroy": [P],
         "cm_dctx_layout": [P, _ip, _ip, _ip],
         "cm_dctx_set_accumulator": [P, P, P, C.c_int],
+        "cm_dctx_upload_bytes": [P, C.POINTER(C.c_longlong)],
         "cm_dctx_set_volumes": [P, P, P],
         "cm_dctx_solve": [P, C.POINTER(cm_reg_config), P, C.c_int, C.POINTER(cm_solve_stats)],
         "cm_dctx_get_volume": [P, P],

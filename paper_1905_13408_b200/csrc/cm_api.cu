@@ -607,6 +607,12 @@ int cm_dctx_layout(const cm_dctx* d, int* planes_per_rank, int* first_plane, int
     return CM_OK;
 }
 
+int cm_dctx_upload_bytes(const cm_dctx* d, long long* acc_h2d_bytes) {
+    if (!d || !d->impl) return fail(CM_ERR_INVALID_ARGUMENT, "null context");
+    if (acc_h2d_bytes) *acc_h2d_bytes = (long long)d->impl->acc_h2d_bytes;
+    return CM_OK;
+}
+
 int cm_dctx_set_accumulator(cm_dctx* d, const double* weight, const double* numerator,
                             int finalized) {
     DCTX_GUARD(d);

@@ -94,12 +94,28 @@ __host__ __device__ inline size_t bslab_index(int n, int nrows, int c, int bl, i
     return (size_t)half * ((size_t)n * nrows * hh) + ((size_t)c * nrows + bl) * hh + (a - half * hh);
 }
 
-// Full-grid fp64 accumulator -> this rank's b rows of the packed half spectrum
-// (same projection and sign as convert_acc_kernel); statistics over the full grid
-// are taken once by the owner of the staging copy.
-__global__ static void convert_rows_kernel(int n, int rb0, int nrows, const double* __restrict__ W,
-                                           const double* __restrict__ Y, float* Wm, float* Wn,
-                                           float2* Ym, float2* Yn, float2* Q0) {
+// The accumulator rows a rank needs: its b rows [rb0, rb0 + nrows) and their
+// Friedel mirrors (N - b) mod N — the projection pairs n with -n. Sorted,
+// distinct. 2 nrows rows (fewer when the sets overlap) instead of the N rows
+// of the full grid: the upload is 2/P of the 24 N^3 bytes per rank.
+inline std::vector<int> acc_rows_needed(int n, int rb0, int nrows) {
+    std::vector<char> need(n, 0);
+    for (int b = rb0; b < rb0 + nrows; ++b) {
+        need[b] = 1;
+        need[b ? n - b : 0] = 1;
+    }
+    std::vector<int> rows;
+    for (int b = 0; b < n; ++b)
+        if (need[b]) rows.push_back(b);
+    return rows;
+}
+
+// Sliced fp64 accumulator (W [c][lr][a], Y [c][lr][a] complex over the nrl rows
+// of acc_rows_needed; lrow[b] = local row) -> this rank's b rows of the packed
+// half spectrum (same projection and sign as convert_acc_kernel).
+__global__ static void convert_rows_kernel(int n, int rb0, int nrows, int nrl, const int* __restrict__ lrow,
+                                           const double* __restrict__ W, const double* __restrict__ Y,
+                                           float* Wm, float* Wn, float2* Ym, float2* Yn, float2* Q0) {
     const int nh = n / 2;
     const size_t total = (size_t)n * nrows * (nh + 1);
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < total;
@@ -109,8 +125,8 @@ __global__ static void convert_rows_kernel(int n, int rb0, int nrows, const doub
         const int bl = (int)(bc % nrows), c = (int)(bc / nrows);
         const int b = rb0 + bl;
         const int am = a ? n - a : 0, bm = b ? n - b : 0, cm_ = c ? n - c : 0;
-        const size_t i = ((size_t)c * n + b) * n + a;
-        const size_t m = ((size_t)cm_ * n + bm) * n + am;
+        const size_t i = ((size_t)c * nrl + lrow[b]) * n + a;
+        const size_t m = ((size_t)cm_ * nrl + lrow[bm]) * n + am;
         const double wp = 0.5 * (W[i] + W[m]);
         const double sg = ((a + b + c) & 1) ? -1.0 : 1.0;
         const double pr = sg * 0.5 * (Y[2 * i] + Y[2 * m]), pi = sg * 0.5 * (Y[2 * i + 1] - Y[2 * m + 1]);
@@ -128,6 +144,70 @@ __global__ static void convert_rows_kernel(int n, int rb0, int nrows, const doub
             reinterpret_cast<float*>(q)[a == 0 ? 0 : 1] = float(wp);
             q[a == 0 ? 1 : 2] = make_float2(float(pr), float(pi));
         }
+    }
+}
+
+// Accumulator statistics of one spectrum row b per CTA (the half spectrum's
+// (c, a) plane of that row, convert_acc_kernel's terms): out[s * nrows + bl] for
+// s = sum W, sum |Z_H|^2, max residue, max scale, max W. The decomposition is
+// fixed per row, so the row partials — and their sum in b order on the host —
+// do not depend on how many ranks share the rows.
+__global__ static void __launch_bounds__(256) acc_row_stats_kernel(int n, int rb0, int nrows, int nrl,
+                                                                   const int* __restrict__ lrow,
+                                                                   const double* __restrict__ W,
+                                                                   const double* __restrict__ Y,
+                                                                   double* out) {
+    const int nh = n / 2, bl = blockIdx.x, b = rb0 + bl, bm = b ? n - b : 0;
+    const size_t lb = (size_t)lrow[b], lm = (size_t)lrow[bm];
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // sw, sz, worst, scale, wmax
+    const size_t per = (size_t)n * (nh + 1);
+    for (size_t q = threadIdx.x; q < per; q += blockDim.x) {
+        const int a = (int)(q % (nh + 1)), c = (int)(q / (nh + 1));
+        const int am = a ? n - a : 0, cm_ = c ? n - c : 0;
+        const size_t i = ((size_t)c * nrl + lb) * n + a, m = ((size_t)cm_ * nrl + lm) * n + am;
+        const double w = W[i], wmt = W[m];
+        const double yr = Y[2 * i], yi = Y[2 * i + 1], mr = Y[2 * m], mi = Y[2 * m + 1];
+        v[2] = fmax(v[2], fmax(hypot(yr - mr, yi + mi), fabs(w - wmt)));
+        v[3] = fmax(v[3], fmax(fmax(hypot(yr, yi), w), fmax(hypot(mr, mi), wmt)));
+        v[4] = fmax(v[4], fmax(w, wmt));
+        const bool inner = (a != 0 && a != nh);
+        v[0] += inner ? (w + wmt) : w;
+        double zr = 0.0, zi = 0.0;
+        if (w > 0.0) {
+            const double sc = 1.0 / sqrt(w);
+            zr += yr * sc;
+            zi += yi * sc;
+        }
+        if (wmt > 0.0) {
+            const double sc = 1.0 / sqrt(wmt);
+            zr += mr * sc;
+            zi -= mi * sc;
+        }
+        zr *= 0.5;
+        zi *= 0.5;
+        v[1] += (inner ? 2.0 : 1.0) * (zr * zr + zi * zi);
+    }
+    __shared__ double red[8][5];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        v[1] += __shfl_xor_sync(0xffffffffu, v[1], o);
+#pragma unroll
+        for (int s = 2; s < 5; ++s) v[s] = fmax(v[s], __shfl_xor_sync(0xffffffffu, v[s], o));
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int s = 0; s < 5; ++s) red[wid][s] = v[s];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {  // fixed warp order
+            t[0] += red[w][0];
+            t[1] += red[w][1];
+            for (int s = 2; s < 5; ++s) t[s] = fmax(t[s], red[w][s]);
+        }
+        for (int s = 0; s < 5; ++s) out[(size_t)s * nrows + bl] = t[s];
     }
 }
 
@@ -229,6 +309,7 @@ struct DistBase {
     // accumulator state (full-grid statistics; every rank holds the same values)
     bool acc_set = false, acc_fin = false;
     double residue = 0.0, max_weight = 0.0, s_y = 0.0, s_n = 0.0;
+    size_t acc_h2d_bytes = 0;  // host-to-device bytes of the last set_accumulator
 };
 
 template <int N>
@@ -273,6 +354,8 @@ struct DistImpl final : DistBase {
         DevState* st = nullptr;
         double* trace = nullptr;
         double* theta = nullptr;
+        double* rowstat = nullptr;      // [5][NB] accumulator row statistics
+        double* rowstat_all = nullptr;  // [P][5][NB] all-gathered
         CUtensorMap tmx[5] = {}, tmp[3] = {}, tmg = {}, tma = {};
     };
 
@@ -283,9 +366,10 @@ struct DistImpl final : DistBase {
     std::vector<Rank> ranks;
     cudaStream_t stream = nullptr;
     std::vector<void*> allocs;
-    double* stage = nullptr;   // full-grid fp64 staging (shared by virtual ranks)
-    unsigned long long* stats_mx = nullptr;
-    double* stats_part = nullptr;
+    double* stage = nullptr;   // fp64 staging (shared by virtual ranks, grown on demand)
+    size_t stage_cap = 0;      // doubles
+    int* lrow_d = nullptr;     // accumulator row -> staged row (set_accumulator)
+    HostXfer xfer;             // pageable host buffers through a pinned ring
     bool vol_set = false, anchor_is_init = false;
     int grid_s2 = 1, grid_x = 1, last_iter = 0, last_fista = 0;
     int ygrid = 1, zgrid = 1;
@@ -294,6 +378,7 @@ struct DistImpl final : DistBase {
 
     ~DistImpl() override {
         for (void* p : allocs) cudaFree(p);
+        if (stage) cudaFree(stage);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
         if (cstream) cudaStreamDestroy(cstream);
@@ -411,45 +496,86 @@ struct DistImpl final : DistBase {
     }
 
     // ---- data upload ---------------------------------------------------------------
+    // fp64 staging, grown on demand: the accumulator rows of one rank (3 nrl N^2
+    // doubles) or one rank's ghosted planes of a volume
+    int ensure_stage(size_t doubles) {
+        if (stage_cap >= doubles) return CM_OK;
+        CK(cudaStreamSynchronize(stream));
+        if (stage) cudaFree(stage);
+        stage = nullptr;
+        stage_cap = 0;
+        CK(cudaMalloc((void**)&stage, doubles * sizeof(double)));
+        stage_cap = doubles;
+        return CM_OK;
+    }
+
+    // Each rank uploads only the accumulator rows its b-slab conversion reads
+    // (acc_rows_needed: its rows and their mirrors), from the caller's pageable
+    // arrays through the pinned ring (host_xfer.h); the full-grid statistics
+    // are per-row partials (acc_row_stats_kernel) all-gathered across ranks and
+    // summed on the host in row order, so every rank — and every P — gets the
+    // same numbers.
     int set_accumulator(const double* w, const double* y, int finalized) override {
-        const size_t L = NN * N;
-        if (!stage) CKS(dalloc(&stage, 3 * L));
-        if (!stats_mx) {
-            CKS(dalloc(&stats_mx, 4));
-            CKS(dalloc(&stats_part, 2 * 148 * 32));
-        }
-        CK(cudaMemcpyAsync(stage, w, 8 * L, cudaMemcpyHostToDevice, stream));
-        CK(cudaMemcpyAsync(stage + L, y, 16 * L, cudaMemcpyHostToDevice, stream));
-        // residue and max weight over the full grid (every process holds the whole
-        // accumulator, as the reference's BackProjector does)
-        CK(cudaMemsetAsync(stats_mx, 0, 32, stream));
-        convert_acc_kernel<R><<<grid_for(NN * (Nh + 1), 256), 256, 0, stream>>>(
-            N, stage, stage + L, nullptr, nullptr, nullptr, nullptr, stats_part, stats_mx);
-        CK(cudaGetLastError());
+        if (!lrow_d) CKS(dalloc(&lrow_d, N));
+        acc_h2d_bytes = 0;
+        std::vector<void*> mine, all;
         for (Rank& k : ranks) {
-            convert_rows_kernel<<<grid_for(NN * (Nh + 1) / P, 256), 256, 0, stream>>>(
-                N, k.rb0, NB, stage, stage + L, k.W, k.Wn, k.Yh, k.Yn, k.Q0);
+            if (!k.rowstat) {
+                CKS(dalloc(&k.rowstat, 5 * (size_t)NB));
+                CKS(dalloc(&k.rowstat_all, 5 * (size_t)N));
+            }
+            const std::vector<int> rows = acc_rows_needed(N, k.rb0, NB);
+            const size_t nrl = rows.size();
+            CKS(ensure_stage(3 * nrl * NN));
+            std::vector<int> lrow(N, -1);
+            for (size_t r = 0; r < nrl; ++r) lrow[rows[r]] = (int)r;
+            std::vector<CopySeg> sw, sy;
+            for (int c = 0; c < N; ++c)
+                for (size_t r = 0; r < nrl;) {
+                    size_t e = r + 1;
+                    while (e < nrl && rows[e] == rows[e - 1] + 1) ++e;
+                    const size_t b0 = (size_t)rows[r], nb = e - r;
+                    sw.push_back({w + ((size_t)c * N + b0) * N, nb * N * 8});
+                    sy.push_back({y + 2 * (((size_t)c * N + b0) * N), nb * N * 16});
+                    r = e;
+                }
+            double* W = stage;
+            double* Y = stage + nrl * NN;
+            CKS(xfer.h2d_segments(W, sw, stream));
+            CKS(xfer.h2d_segments(Y, sy, stream));
+            CK(cudaMemcpyAsync(lrow_d, lrow.data(), sizeof(int) * N, cudaMemcpyHostToDevice, stream));
+            acc_h2d_bytes += 24 * nrl * NN;
+            acc_row_stats_kernel<<<NB, 256, 0, stream>>>(N, k.rb0, NB, (int)nrl, lrow_d, W, Y, k.rowstat);
             CK(cudaGetLastError());
+            convert_rows_kernel<<<grid_for(NN * (Nh + 1) / P, 256), 256, 0, stream>>>(
+                N, k.rb0, NB, (int)nrl, lrow_d, W, Y, k.W, k.Wn, k.Yh, k.Yn, k.Q0);
+            CK(cudaGetLastError());
+            // the stage and the row map are reused by the next hosted rank
+            CK(cudaStreamSynchronize(stream));
+            mine.push_back(k.rowstat);
+            all.push_back(k.rowstat_all);
         }
-        unsigned long long h[4];
-        const int blocks = grid_for(NN * (Nh + 1), 256);
-        std::vector<double> parts(2 * (size_t)blocks);
-        CK(cudaMemcpyAsync(h, stats_mx, sizeof(h), cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(parts.data(), stats_part, sizeof(double) * parts.size(),
+        if (comm->all_gather(mine, all, sizeof(double) * 5 * NB, stream))
+            return fail(CM_ERR_NCCL, "all_gather (accumulator statistics) failed");
+        std::vector<double> h(5 * (size_t)N);
+        CK(cudaMemcpyAsync(h.data(), ranks[0].rowstat_all, sizeof(double) * h.size(),
                            cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
-        double worst, scale, wmax;
-        std::memcpy(&worst, &h[0], 8);
-        std::memcpy(&scale, &h[1], 8);
-        std::memcpy(&wmax, &h[2], 8);
+        double sw = 0.0, sz = 0.0, worst = 0.0, scale = 0.0, wmax = 0.0;
+        for (int r = 0; r < P; ++r) {  // rank r holds rows r NB .. r NB + NB - 1: row order
+            const double* q = h.data() + (size_t)r * 5 * NB;
+            for (int bl = 0; bl < NB; ++bl) {
+                sw += q[bl];
+                sz += q[NB + bl];
+                worst = std::fmax(worst, q[2 * NB + bl]);
+                scale = std::fmax(scale, q[3 * NB + bl]);
+                wmax = std::fmax(wmax, q[4 * NB + bl]);
+            }
+        }
         residue = scale > 0.0 ? worst / scale : 0.0;
         max_weight = wmax;
         // scale_data (params.cpp:9-26) by Parseval, as Impl::commit_acc_stage
-        double sw = 0.0, sz = 0.0;
-        for (int b = 0; b < blocks; ++b) {
-            sw += parts[2 * b];
-            sz += parts[2 * b + 1];
-        }
+        const size_t L = NN * N;
         s_n = sw / (double)L;
         s_y = std::sqrt(sz) / (double)L;
         acc_set = true;
@@ -459,12 +585,10 @@ struct DistImpl final : DistBase {
 
     // host full volume -> this rank's ghosted planes (zero outside the grid)
     int upload_slab(const double* host, R* dst, const Rank& k) {
-        const size_t L = NN * N;
-        if (!stage) CKS(dalloc(&stage, 3 * L));
+        CKS(ensure_stage(ghosted()));
         CK(cudaMemsetAsync(dst, 0, ghosted() * 4, stream));
         const int k_lo = std::max(0, k.koff - 1), k_hi = std::min(N, k.koff + NK + 1);
-        CK(cudaMemcpyAsync(stage, host + (size_t)k_lo * NN, 8 * NN * (k_hi - k_lo),
-                           cudaMemcpyHostToDevice, stream));
+        CKS(xfer.h2d(stage, host + (size_t)k_lo * NN, 8 * NN * (k_hi - k_lo), stream));
         const size_t cnt = NN * (k_hi - k_lo);
         to_real_kernel<R><<<grid_for(cnt, 256), 256, 0, stream>>>(
             stage, dst + (size_t)(k_lo - (k.koff - 1)) * NN, cnt);
@@ -982,16 +1106,13 @@ struct DistImpl final : DistBase {
     // this process's planes of the result into the full host volume
     int get_volume(double* out) override {
         if (!result_valid) return fail(CM_ERR_STATE, "no solver result resident");
-        const size_t L = NN * N;
-        if (!stage) CKS(dalloc(&stage, 3 * L));
+        CKS(ensure_stage(ghosted()));
         for (Rank& k : ranks) {
             const R* src = (last_fista ? k.XF[last_iter % 2] : k.X[last_iter % 3]) + NN;
             to_double_kernel<R><<<grid_for((size_t)NK * NN, 256), 256, 0, stream>>>(
                 src, stage, (size_t)NK * NN);
             CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(out + (size_t)k.koff * NN, stage, 8 * (size_t)NK * NN,
-                               cudaMemcpyDeviceToHost, stream));
-            CK(cudaStreamSynchronize(stream));
+            CKS(xfer.d2h(out + (size_t)k.koff * NN, stage, 8 * (size_t)NK * NN, stream));
         }
         return CM_OK;
     }

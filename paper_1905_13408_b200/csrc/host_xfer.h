@@ -31,14 +31,33 @@ namespace cm {
 int fail(int code, const std::string& msg);
 
 // A persistent pool of copy threads (thread creation per 64 MiB chunk cost
-// ~20 us x threads x chunks: a few percent of a 5 GB transfer)
+// ~20 us x threads x chunks: a few percent of a 5 GB transfer). A job is a
+// destination range [0, bytes) filled from a list of source segments (one
+// segment: a plain memcpy); worker t of nt copies [t part, (t+1) part).
+struct CopySeg {
+    const void* src;
+    size_t bytes;
+};
+
+inline void copy_segments(unsigned char* dst, const CopySeg* segs, size_t nseg, size_t lo, size_t hi) {
+    size_t off = 0;
+    for (size_t s = 0; s < nseg && off < hi; ++s) {
+        const size_t end = off + segs[s].bytes;
+        if (end > lo) {
+            const size_t a = std::max(off, lo), b = std::min(end, hi);
+            std::memcpy(dst + a, (const unsigned char*)segs[s].src + (a - off), b - a);
+        }
+        off = end;
+    }
+}
+
 struct CopyPool {
     std::vector<std::thread> th;
     std::mutex m;
     std::condition_variable cv, done_cv;
     unsigned char* dst = nullptr;
-    const unsigned char* src = nullptr;
-    size_t part = 0, bytes = 0;
+    const CopySeg* segs = nullptr;
+    size_t nseg = 0, part = 0, bytes = 0;
     int gen = 0, pending = 0;
     bool quit = false;
     explicit CopyPool(int n) {
@@ -50,12 +69,12 @@ struct CopyPool {
                     cv.wait(lk, [&] { return quit || gen != seen; });
                     if (quit) return;
                     seen = gen;
-                    const size_t off = part * t;
+                    const size_t lo = std::min(part * t, bytes), hi = std::min(lo + part, bytes);
                     unsigned char* d = dst;
-                    const unsigned char* sp = src;
-                    const size_t len = off < bytes ? std::min(part, bytes - off) : 0;
+                    const CopySeg* sg = segs;
+                    const size_t ns = nseg;
                     lk.unlock();
-                    if (len) std::memcpy(d + off, sp + off, len);
+                    if (hi > lo) copy_segments(d, sg, ns, lo, hi);
                     lk.lock();
                     if (--pending == 0) done_cv.notify_one();
                 }
@@ -70,22 +89,27 @@ struct CopyPool {
         for (auto& t : th) t.join();
     }
     int size() const { return (int)th.size() + 1; }
-    void copy(void* d, const void* sp, size_t n) {
+    void copy(void* d, const CopySeg* sg, size_t ns, size_t n) {
         const int nt = size();
         const size_t prt = (n / nt + 4095) & ~size_t(4095);
         {
             std::lock_guard<std::mutex> lk(m);
             dst = (unsigned char*)d;
-            src = (const unsigned char*)sp;
+            segs = sg;
+            nseg = ns;
             part = prt;
             bytes = n;
             pending = nt - 1;
             ++gen;
         }
         cv.notify_all();
-        std::memcpy(d, sp, std::min(prt, n));
+        copy_segments((unsigned char*)d, sg, ns, 0, std::min(prt, n));
         std::unique_lock<std::mutex> lk(m);
         done_cv.wait(lk, [&] { return pending == 0; });
+    }
+    void copy(void* d, const void* sp, size_t n) {
+        const CopySeg one{sp, n};
+        copy(d, &one, 1, n);
     }
 };
 
@@ -136,6 +160,58 @@ struct HostXfer {
             return;
         }
         pool->copy(dst, src, bytes);
+    }
+
+    void pcopy_segs(void* dst, const CopySeg* segs, size_t nseg, size_t bytes) const {
+        if (!pool || bytes < (size_t(8) << 20)) {
+            copy_segments((unsigned char*)dst, segs, nseg, 0, bytes);
+            return;
+        }
+        pool->copy(dst, segs, nseg, bytes);
+    }
+
+    // gather: the segments, concatenated in order, land contiguously at dev
+    // (pageable sources packed into the pinned ring by the copy pool). Same
+    // completion semantics as h2d.
+    int h2d_segments(void* dev, const std::vector<CopySeg>& segs, cudaStream_t st) {
+        if (segs.empty()) return CM_OK;
+        if (pinned(segs[0].src)) {
+            size_t off = 0;
+            for (const CopySeg& g : segs) {
+                if (cudaMemcpyAsync((unsigned char*)dev + off, g.src, g.bytes, cudaMemcpyHostToDevice, st) !=
+                    cudaSuccess)
+                    return fail(CM_ERR_CUDA, "host-to-device copy failed");
+                off += g.bytes;
+            }
+            return CM_OK;
+        }
+        if (int rc = ensure()) return rc;
+        size_t s = 0, soff = 0, doff = 0;  // next source byte: segment s, offset soff
+        std::vector<CopySeg> cur;
+        for (int i = 0; s < segs.size(); ++i) {
+            const int b = i % kBufs;
+            // the chunk's segment list (the first and last may be partial)
+            cur.clear();
+            size_t len = 0;
+            while (s < segs.size() && len < kChunk) {
+                const size_t take = std::min(segs[s].bytes - soff, kChunk - len);
+                cur.push_back({(const unsigned char*)segs[s].src + soff, take});
+                len += take;
+                soff += take;
+                if (soff == segs[s].bytes) {
+                    ++s;
+                    soff = 0;
+                }
+            }
+            if (cudaEventSynchronize(done[b]) != cudaSuccess) return fail(CM_ERR_CUDA, "staging wait failed");
+            pcopy_segs(buf[b], cur.data(), cur.size(), len);
+            if (cudaMemcpyAsync((unsigned char*)dev + doff, buf[b], len, cudaMemcpyHostToDevice, st) !=
+                    cudaSuccess ||
+                cudaEventRecord(done[b], st) != cudaSuccess)
+                return fail(CM_ERR_CUDA, "host-to-device copy failed");
+            doff += len;
+        }
+        return CM_OK;
     }
 
     // stream-ordered on return for pinned sources; for pageable sources the

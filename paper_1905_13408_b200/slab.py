@@ -66,6 +66,20 @@ class SlabPlan:
     def rows(self, rank: int) -> range:
         return range(rank * self.nb, (rank + 1) * self.nb)
 
+    def acc_rows(self, rank: int) -> list[int]:
+        """Accumulator rows b (of the full grid's [c][b][a]) that rank's b-slab
+        conversion reads: its rows and their Friedel mirrors (n - b) mod n, sorted
+        (csrc/dist.cuh acc_rows_needed; the rank uploads only these)."""
+        need = set()
+        for b in self.rows(rank):
+            need.add(b)
+            need.add((self.n - b) % self.n)
+        return sorted(need)
+
+    def acc_upload_bytes(self, rank: int) -> int:
+        """fp64 W (8 B) + numerator (16 B) over the rank's accumulator rows."""
+        return 24 * len(self.acc_rows(rank)) * self.n * self.n
+
     def ghosted_planes(self, rank: int) -> list[int | None]:
         """Global plane behind each local plane of the ghosted layout (None: outside)."""
         out = []
@@ -168,6 +182,13 @@ class SlabContext:
             raise GridMismatch("accumulator arrays do not match side_n")
         _check(self.lib.cm_dctx_set_accumulator(self.ptr, w.ctypes.data, y.ctypes.data,
                                                 int(bool(acc.finalized))))
+
+    @property
+    def acc_upload_bytes(self) -> int:
+        """Host-to-device bytes of this process's last set_accumulator."""
+        v = C.c_longlong()
+        _check(self.lib.cm_dctx_upload_bytes(self.ptr, C.byref(v)))
+        return v.value
 
     def set_volumes(self, x_init, x_anchor=None) -> None:
         xi = self._vol(x_init)

@@ -155,6 +155,93 @@ def test_slab_exchange_pattern_gloo(n):
         assert all(r[1:]), r
 
 
+def _convert_rows(Wsrc, Ysrc, row_of, n, b):
+    """dist.cuh convert_rows_kernel restated for one spectrum row b: the projected,
+    sign-folded (W, Yh) over (c, a), a in [0, n/2], from accumulator rows held at
+    row_of(b) and row_of(-b)."""
+    c = np.arange(n)[:, None]
+    a = np.arange(n // 2 + 1)[None, :]
+    cm_, am, bm = (-c) % n, (-a) % n, (-b) % n
+    w, wm = Wsrc[c, row_of(b), a], Wsrc[cm_, row_of(bm), am]
+    y, ym = Ysrc[c, row_of(b), a], Ysrc[cm_, row_of(bm), am]
+    sg = np.where((a + b + c) & 1, -1.0, 1.0)
+    return 0.5 * (w + wm), sg * 0.5 * (y + ym.conj()), (w, wm, y, ym, a)
+
+
+def _row_stats(parts, n):
+    """acc_row_stats_kernel's five row terms (sum W, sum |Z_H|^2, max residue,
+    max scale, max W)."""
+    w, wm, y, ym, a = parts
+    inner = (a != 0) & (a != n // 2)
+    sw = np.where(inner, w + wm, w).sum()
+    zh = 0.5 * (y / np.sqrt(w) + (ym / np.sqrt(wm)).conj())
+    sz = (np.where(inner, 2.0, 1.0) * np.abs(zh) ** 2).sum()
+    worst = max(np.abs(y - ym.conj()).max(), np.abs(w - wm).max())
+    scale = max(np.abs(y).max(), w.max(), np.abs(ym).max(), wm.max())
+    return np.array([sw, sz, worst, scale, max(w.max(), wm.max())])
+
+
+def _acc_worker(rank: int, world: int, port: int, n: int, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = SlabPlan(n, world)
+        rng = np.random.default_rng(11)
+        W = rng.random((n, n, n)) + 0.5                                   # [c][b][a]
+        Y = rng.standard_normal((n, n, n)) + 1j * rng.standard_normal((n, n, n))
+        rows = plan.acc_rows(rank)
+        local = {b: i for i, b in enumerate(rows)}
+        Ws, Ys = W[:, rows, :], Y[:, rows, :]                              # what the rank uploads
+        ok_conv, mine = True, []
+        for b in plan.rows(rank):
+            wp, yp, parts = _convert_rows(Ws, Ys, lambda r: local[r], n, b)  # KeyError: row missing
+            wf, yf, _ = _convert_rows(W, Y, lambda r: r, n, b)
+            ok_conv &= np.array_equal(wp, wf) and np.array_equal(yp, yf)
+            mine.append(_row_stats(parts, n))
+        mine = torch.from_numpy(np.array(mine).T.copy())                  # [5][nb]
+        got = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(got, mine)
+        allrows = torch.cat(got, dim=1).numpy()                          # [5][n], row order
+        sw, sz = allrows[0].sum(), allrows[1].sum()                      # in row order
+        one = np.array([_row_stats(_convert_rows(W, Y, lambda r: r, n, b)[2], n) for b in range(n)]).T
+        ok_stats = (sw == one[0].sum() and sz == one[1].sum() and
+                    allrows[2:].max(axis=1).tolist() == one[2:].max(axis=1).tolist())
+        ok_bytes = (len(rows) <= min(n, 2 * plan.nb) and
+                    plan.acc_upload_bytes(rank) == 24 * len(rows) * n * n)
+        q.put((rank, bool(ok_conv), bool(ok_stats), bool(ok_bytes)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,world", [(8, 2), (16, 4)])
+def test_sliced_accumulator_upload_gloo(n, world):
+    """Each rank converts its b rows from only the accumulator rows it uploads
+    (SlabPlan.acc_rows: its rows and their mirrors), bit-identical to converting
+    from the full grid; the per-row statistics, all-gathered and summed in row
+    order, equal the single-rank sums exactly."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_acc_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert all(r[1:]), r
+    plan = SlabPlan(64, 8)
+    assert plan.acc_rows(0) == [0] + list(range(1, 8)) + list(range(57, 64))
+    assert plan.acc_rows(4) == list(range(25, 40))
+
+
 # ---------------------------------------------------------------------------------------
 # device solver, P ranks emulated on one GPU
 # ---------------------------------------------------------------------------------------
@@ -210,6 +297,32 @@ def test_slab_matches_single_gpu(n, world):
         _check_traces(_traces(t2), _traces(t1), 1e-6, name)
         assert _rel(x2, x1) <= 1e-6, (name, _rel(x2, x1))
     sc.close()
+
+
+@pytest.mark.gpu
+def test_slab_sliced_upload_is_decomposition_independent():
+    """Each emulated rank uploads only its accumulator rows (the bytes SlabPlan
+    predicts, ~2/P of the full grid's); the volume is bit-identical to one rank's."""
+    from paper_1905_13408_b200.slab import SlabContext
+
+    n = 256
+    p, acc, base = _problem(n)
+    cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 6})
+    out = {}
+    for world in (1, 4):
+        sc = SlabContext(n, world)
+        sc.set_accumulator(acc)
+        plan = sc.plan
+        assert sc.acc_upload_bytes == sum(plan.acc_upload_bytes(r) for r in range(world))
+        sc.set_volumes(p.x0)
+        t = []
+        sc.solve(cfg, t)
+        out[world] = (sc.get_volume(), _traces(t))
+        sc.close()
+    assert SlabPlan(n, 4).acc_upload_bytes(1) < 24 * n ** 3 // 2 + 1
+    assert np.array_equal(out[4][0], out[1][0])
+    # the objective partials are summed per rank, then across ranks: roundoff only
+    np.testing.assert_allclose(out[4][1], out[1][1], rtol=1e-12, atol=0)
 
 
 @pytest.mark.gpu
