@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--big-iters", type=int, default=20)
     ap.add_argument("--em", type=int, default=1, help="time the EM-block extras (V, FSC)")
     ap.add_argument("--prec64", type=int, default=1, help="also time the fp64 parity mode")
+    ap.add_argument("--configs", type=int, default=1,
+                    help="also time BASELINE configs 1, 2 and one config-5 replica (0/1)")
     return ap.parse_args()
 
 
@@ -755,6 +757,13 @@ def run_ours(args):
         c64.close()
         del c64
 
+    oc = None
+    if args.configs and world == 1 and args.precision == 32:
+        try:
+            oc = other_configs(local, with_reference=not args.no_cpu_baseline)
+        except Exception as e:  # reported, never fatal to the headline line
+            oc = {"error": str(e)[:300]}
+
     big = None
     if args.big_n:
         del ctx
@@ -785,13 +794,119 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "e2e_pinned": e2e_pinned,
             "clocks": clocks,
             "gpu_launches": launches, "time_to_tolerance": ttt, "big": big, "em_block": em,
-            "precision64": p64,
+            "precision64": p64, "other_configs": oc,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def other_configs(device: int = 0, with_reference: bool = True) -> dict:
+    """The BASELINE configs other than the headline (one GPU each; the driver's
+    multi-GPU runs cover config 4's scaling):
+      config1: 64^3 blob phantom, 100 iterations, single reweighting pass
+        (per_m_step weights), lipschitz + audit — launch-bound; the solve on the
+        device (graph), end to end through cm_m_step from pageable buffers, and
+        the unmodified reference (oracle/_ref, one core) on the same call;
+      config2: 256^3 bond-like phantom, 3 reweighting loops (per_m_step,
+        x_init <- previous output) each to tolerance (ISTA surrogate 1e-6; FISTA
+        step 3%, opt-in);
+      config5: one 384^3 replica of the 8-volume batch (100 ISTA iterations,
+        reference semantics); `bench.py --gpus N --mode replicas` runs N."""
+    import torch
+
+    import paper_1905_13408_b200 as cm
+    from paper_1905_13408_b200 import synth
+
+    out = {}
+    # ---- config 1
+    n = 64
+    p = synth.synthetic_problem(n)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    ctx = cm.Context(n, 32, device=device)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg = cm.RegConfig(**{**cfg.__dict__, "inner_iters": 100, "refresh": cm.Refresh.per_m_step})
+    ctx.set_volumes(p.x0, p.x0)
+    ctx.solve(cfg)
+    reps = 20
+    dev = sorted(ctx.solve(cfg).solve_ms for _ in range(reps))[reps // 2]
+    o64 = np.empty((n, n, n))
+    ctx.m_step_host(acc, p.x0, p.x0, cfg, o64)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ctx.m_step_host(acc, p.x0, p.x0, cfg, o64)
+    e2e_ms = (time.perf_counter() - t0) / reps * 1e3
+    c1 = {"side": n, "iterations": 100, "refresh": "per_m_step", "solve_ms_device": dev,
+          "value": n ** 3 * 100 / (dev / 1e3), "unit": "voxel-iterations/s",
+          "e2e_ms_pageable": e2e_ms, "e2e_value": n ** 3 * 100 / (e2e_ms / 1e3),
+          "ms_per_iteration": dev / 100,
+          "note": "launch-bound: one CUDA graph of 100 iterations x 7 kernels"}
+    if with_reference:
+        try:
+            sys.path.insert(0, str(ROOT / "tests"))
+            from oracle_lib import REF_DIR, Reference, make_cfg
+
+            if (REF_DIR / "libcryomap_ref.so").exists():
+                os.environ["CM_REF_FFT_THREADS"] = "1"
+                R = Reference()
+                rcfg = make_cfg(alpha=cfg.alpha, beta=cfg.beta, gamma=cfg.gamma, eps=cfg.eps,
+                                eps_prime=cfg.eps_prime, mu=cfg.mu, inner_iters=100, refresh=1)
+                rc, xr, _ = R.m_step(p.weight, p.numerator, p.x0, p.x0, rcfg, trace=False)
+                assert rc == 0
+                c1["reference_seconds_1core"] = R.last_seconds
+                c1["reference_value"] = n ** 3 * 100 / R.last_seconds
+                c1["rel_l2_vs_reference"] = float(np.linalg.norm(o64 - xr) / np.linalg.norm(xr))
+        except Exception as e:  # reported, never fatal
+            c1["reference_error"] = str(e)[:200]
+    out["config1_64"] = c1
+    ctx.close()
+    # ---- config 2
+    n = 256
+    p = synth.synthetic_problem(n, kind="bonds")
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    ctx = cm.Context(n, 32, device=device)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    base = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    c2 = {"side": n, "phantom": "bond-like chains", "loops": 3}
+    for name, extra in (("ista_surrogate_1e-6", dict(tol_kind=1, tol=1e-6)),
+                        ("fista_step_3pct", dict(momentum=1, tol_kind=2, tol=0.03))):
+        cfg = cm.RegConfig(**{**base.__dict__, "inner_iters": 20000,
+                              "refresh": cm.Refresh.per_m_step, **extra})
+        x, its, secs = p.x0, [], 0.0
+        for _ in range(3):
+            ctx.set_volumes(x, p.x0)
+            st = ctx.solve(cfg)
+            x = ctx.get_volume()
+            its.append(st.iterations)
+            secs += st.solve_ms / 1e3
+        c2[name] = {"iterations": its, "seconds": secs,
+                    "rel_err_vs_truth": float(np.linalg.norm(x - p.truth) / np.linalg.norm(p.truth))}
+    out["config2_256"] = c2
+    ctx.close()
+    # ---- config 5 (one replica)
+    n = 384
+    p = synth.synthetic_problem(n)
+    acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
+    ctx = cm.Context(n, 32, device=device)
+    ctx.set_accumulator(acc)
+    s = ctx.scale_data()
+    cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
+    cfg.inner_iters = 100
+    ctx.set_volumes(p.x0, p.x0)
+    ctx.solve(cfg)
+    ms = sorted(ctx.solve(cfg).solve_ms for _ in range(5))[2]
+    out["config5_384_replica"] = {"side": n, "iterations": 100, "solve_ms_device": ms,
+                                  "ms_per_iteration": ms / 100,
+                                  "value": n ** 3 * 100 / (ms / 1e3), "unit": "voxel-iterations/s",
+                                  "note": "per-GPU work of the 8 x 384^3 batch"}
+    ctx.close()
+    return out
 
 
 def em_iteration(device: int = 0, n: int = 128, m: int = 1000, n_poses: int = 200,
