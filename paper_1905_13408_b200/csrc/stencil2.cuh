@@ -33,10 +33,31 @@
 
 namespace cm {
 
+// planes per march: the KC in {64, 32, 16, 8} minimising the plane steps of the
+// busiest CTA slot (148 SMs x CM_S2_MINB), ceil(tiles / slots) x (KC + 2 for the
+// march prologue); ties keep the longer march. 512^3 / 384^3 / 256^3: 64; 128^3:
+// 8 (64-plane marches ran 64 CTAs for the whole sweep: 57 -> 19 us)
+__host__ __device__ constexpr int s2_kc(int n) {
+    if (n < 64) return n;
+    int best = 64;
+    long best_cost = -1;
+    for (int kc = 64; kc >= 8; kc /= 2) {
+        if (n % kc) continue;
+        const long tiles = (long)(n / 128) * (n / CM_S2_TJ) * (n / kc);
+        const long slots = 148L * CM_S2_MINB;
+        const long cost = (tiles + slots - 1) / slots * (kc + 2);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = kc;
+        }
+    }
+    return best;
+}
+
 template <int N> struct S2Geo {
     static constexpr int CI = 128;
     static constexpr int TJ = CM_S2_TJ;
-    static constexpr int KC = N < 64 ? N : 64;   // planes per march
+    static constexpr int KC = s2_kc(N);          // planes per march
     static constexpr int NW = TJ + 1;            // + halo-row warp
     static constexpr int NT = NW * 32;
     static constexpr int XW = 136;               // slab row: global i0-4 .. i0+131
