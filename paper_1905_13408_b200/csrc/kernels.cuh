@@ -43,6 +43,19 @@ __host__ __device__ constexpr int pow2_divisor_le(int v, int cap) {
 #ifndef CM_Y_TWMAX
 #define CM_Y_TWMAX 16  // columns per y tile (128-byte rows in fp32)
 #endif
+// plans with >= 24 elements per thread (radix-3/5/7 sides): at most
+// CM_Y_NT_E24 threads per y / z tile, two CTAs per SM (128 registers). The
+// 512-thread tiles of 768^3 were held to 64 registers and spilled: z pass 2.79
+// -> 1.86 ms, y passes 1.17 -> 0.90-0.95 ms (profiles/r2_ab_e24.txt)
+#ifndef CM_Y_NT_E24
+#define CM_Y_NT_E24 256
+#endif
+#ifndef CM_Y_MINB_E24
+#define CM_Y_MINB_E24 2
+#endif
+#ifndef CM_Z_MINB_E24
+#define CM_Z_MINB_E24 2
+#endif
 
 template <typename R, int N> struct Geo {
     using C = Cx<R>;
@@ -57,7 +70,10 @@ template <typename R, int N> struct Geo {
     static constexpr int TY = N / EY;
     static constexpr int SMEM_CAP = CM_Y_SMEM_CAP_KB * 1024; // per tile buffer budget (bytes)
     static constexpr int TWY_CAP = (SMEM_CAP / (N * (int)sizeof(C))) < 1 ? 1 : (SMEM_CAP / (N * (int)sizeof(C)));
-    static constexpr int TWY_LIM = (CM_Y_TWMAX < (1024 / TY) ? CM_Y_TWMAX : (1024 / TY));
+    static constexpr int TWMAX_ = (EY >= 24 && CM_Y_NT_E24 / TY < CM_Y_TWMAX)
+                                      ? (CM_Y_NT_E24 / TY < 1 ? 1 : CM_Y_NT_E24 / TY)
+                                      : CM_Y_TWMAX;
+    static constexpr int TWY_LIM = (TWMAX_ < (1024 / TY) ? TWMAX_ : (1024 / TY));
     static constexpr int TWY = pow2_divisor_le(Nh, TWY_LIM < TWY_CAP ? TWY_LIM : TWY_CAP);
     static constexpr int TW3_LIM = (512 / TY) < 1 ? 1 : (512 / TY);
     static constexpr int TW3_CAP = TWY_CAP / 2 < 1 ? 1 : TWY_CAP / 2;
@@ -169,7 +185,9 @@ template <int N> __host__ __device__ constexpr bool y_pipe() {
 
 template <typename R, int N, bool FWD, bool DM = false>
 __global__ void __launch_bounds__(Geo<R, N>::TWY * Geo<R, N>::TY,
-                                  (Geo<R, N>::TWY * Geo<R, N>::TY <= 512 && !y_pipe<N>()) ? 2 : 1)
+                                  (Geo<R, N>::TWY * Geo<R, N>::TY <= 512 && !y_pipe<N>())
+                                      ? (Geo<R, N>::EY >= 24 ? CM_Y_MINB_E24 : 2)
+                                      : 1)
 ypass_kernel(YParams<R> p) {
     using G = Geo<R, N>;
     using C = Cx<R>;

@@ -93,7 +93,9 @@ template <typename R, int N> struct ZGeo {
     // fp64: 16 complex doubles per thread at N >= 512 are 64 registers of data
     // alone; the fp32 bound of 4 CTAs (64 registers) spilled 1.2 KB per thread
     static constexpr int MINB = sizeof(R) == 8 ? CM_Z_MINB_D
-                                : (NT >= 1024 || E32) ? 1 : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
+                                : (NT >= 1024 || E32) ? 1
+                                : E >= 24 ? CM_Z_MINB_E24
+                                : (NT <= 256 ? 4 : 2);  // 512 threads: two CTAs per SM
     // column-0 kernel: 8 elements per thread on power-of-two sides >= 256 (more
     // warps per pair block: the kernel is latency bound with 257 blocks)
     static constexpr int E0 = (N >= 256 && (N & (N - 1)) == 0) ? 8 : Geo<R, N>::EY;

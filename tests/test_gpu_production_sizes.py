@@ -101,10 +101,12 @@ def test_slab_8_ranks_at_512(p512):
     assert _rel(x2, x1) <= 1e-6
 
 
-@pytest.mark.parametrize("n", [384, 768])
+@pytest.mark.parametrize("n", [384, 768, 480, 720])
 def test_radix3_sides_fp32_vs_fp64(n):
     """BASELINE config 5 side (384^3; 768^3 likewise): radix-3 plans, 3 x 128
-    stencil tiles; fp32 product kernels against the fp64 parity mode."""
+    stencil tiles; 480^3 / 720^3: radix-3/5 plans and a partial last 128-wide
+    x tile of the vector sweep (the oracle pins that path at 160^3,
+    test_gpu_parity); fp32 product kernels against the fp64 parity mode."""
     p = synth.synthetic_problem(n, n_blobs=2000)
     acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
     s = cm.scale_data(acc, precision=64)
