@@ -395,8 +395,9 @@ struct Impl final : ImplBase {
     CUtensorMap tm_p[3] = {};  // x_prev boxes of X[0..2]
     CUtensorMap tm_gt = {};    // g tiles
     CUtensorMap tm_at = {};    // anchor tiles
-    // z-marching stencil (fp32, N % 128 == 0): per-plane slab maps
-    static constexpr bool S2 = sizeof(R) == 4 && N % 128 == 0;
+    // z-marching stencil (fp32, N >= 128, N % 8 == 0; the last 128-wide x tile
+    // partial when 128 does not divide N): per-plane slab maps
+    static constexpr bool S2 = sizeof(R) == 4 && N >= 128 && N % 8 == 0;
     CUtensorMap tm2_x[5] = {}, tm2_p[3] = {}, tm2_g = {}, tm2_a = {};
     int s2_grid = 0;
     int sweep_grid = 0;        // persistent stencil CTAs

@@ -43,7 +43,7 @@ __host__ __device__ constexpr int s2_kc(int n) {
     long best_cost = -1;
     for (int kc = 64; kc >= 8; kc /= 2) {
         if (n % kc) continue;
-        const long tiles = (long)(n / 128) * (n / CM_S2_TJ) * (n / kc);
+        const long tiles = (long)((n + 127) / 128) * (n / CM_S2_TJ) * (n / kc);
         const long slots = 148L * CM_S2_MINB;
         const long cost = (tiles + slots - 1) / slots * (kc + 2);
         if (best_cost < 0 || cost < best_cost) {
@@ -76,7 +76,7 @@ template <int N> struct S2Geo {
     static constexpr size_t OFF_RED = al(OFF_S + S_BYTES);
     static constexpr size_t OFF_BAR = OFF_RED + 32 * NP1 * 8;
     static constexpr size_t SMEM = OFF_BAR + NSTAGE * 8;
-    static constexpr int NTI = N / CI, NTJ = N / TJ, NTK = N / KC;
+    static constexpr int NTI = (N + CI - 1) / CI, NTJ = N / TJ, NTK = N / KC;  // last x tile partial
     static constexpr int NTILES = NTI * NTJ * NTK;  // single GPU (nk = N)
 };
 
@@ -179,6 +179,10 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         const int ii = 4 * lane;
         const int gi0 = i0 + ii;
         const bool row_in = gj < N;
+        // partial last x tile (N % 128 != 0): the lane's 4 voxels are all in or
+        // all out; out-of-grid lanes keep s = 0 and join the shuffles, but load,
+        // store and accumulate nothing
+        const bool col_in = gi0 < N;
         // replicate boundary (gradient.cpp:7-24): the backward neighbour of the
         // first row / column / plane is the voxel itself, so D = 0 there without
         // a per-voxel test; forward terms vanish because s = 0 outside the grid
@@ -200,7 +204,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             float xl = __shfl_up_sync(0xffffffffu, c4.w, 1);
             if (lane == 0) xl = xlo ? c4.x : xr[-1];
             const float xlv[4] = {xl, c4.x, c4.y, c4.z};
-            const bool qin = koff + q < N && row_in;
+            const bool qin = koff + q < N && row_in && col_in;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float d1 = xq[c] - xlv[c], d2 = xq[c] - yv[c], d3 = xq[c] - zv[c];
@@ -231,7 +235,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         };
         // per_m_step weights come from a frozen field: s uses w_tv from it
         auto apply_wtvf = [&](int q, float (&sv)[4], float (&gn)[4]) {
-            if (!p.wtvf || convex || !(koff + q < N && row_in)) return;
+            if (!p.wtvf || convex || !(koff + q < N && row_in && col_in)) return;
             const float4 wv = __ldg(reinterpret_cast<const float4*>(
                 p.wtvf + ((size_t)(q + zs) * N + gj) * N + gi0));
             const float wt[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -318,13 +322,14 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                         if (p.wl1src == p.anchor) {
 #pragma unroll
                             for (int c = 0; c < 4; ++c) ws[c] = av[c];
-                        } else {
+                        } else if (col_in) {
                             const float4 v = __ldg(reinterpret_cast<const float4*>(p.wl1src + gidx));
                             ws[0] = v.x; ws[1] = v.y; ws[2] = v.z; ws[3] = v.w;
                         }
                     }
                     if (p.wtvf) {
-                        const float4 v = __ldg(reinterpret_cast<const float4*>(p.wtvf + gidx));
+                        const float4 v = col_in ? __ldg(reinterpret_cast<const float4*>(p.wtvf + gidx))
+                                                : make_float4(1.f, 1.f, 1.f, 1.f);
                         wtv[0] = v.x; wtv[1] = v.y; wtv[2] = v.z; wtv[3] = v.w;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) wl1[c] = rcp_(fabsf(ws[c]) + eps);
@@ -339,7 +344,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     }
                 }
                 float base[4] = {x_cur[0], x_cur[1], x_cur[2], x_cur[3]};
-                if (FISTA) {
+                if (FISTA && col_in) {
                     const float4 o4 = __ldg(reinterpret_cast<const float4*>(p.xold + gidx));
                     base[0] = o4.x; base[1] = o4.y; base[2] = o4.z; base[3] = o4.w;
                 }
@@ -356,20 +361,20 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     }
                     nx[c] = v;
                 }
-                if (!p.obj_only)
+                if (!p.obj_only && col_in)
                     *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
-                if (FISTA && !p.obj_only) {
+                if (FISTA && !p.obj_only && col_in) {
                     float y[4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
                     *reinterpret_cast<float4*>(p.ynext + gidx) = make_float4(y[0], y[1], y[2], y[3]);
                 }
-                if (FISTA) {
+                if (FISTA && col_in) {
                     // restart test (O'Donoghue & Candes): (y_k - x_{k+1}) . (x_{k+1} - x_k)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) fa[11] += (x_cur[c] - nx[c]) * (nx[c] - base[c]);
                 }
-                if (STEP) {
+                if (STEP && col_in) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         const float dx = nx[c] - base[c];
@@ -401,6 +406,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                     }
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
+                        if (!col_in) break;
                         const float ax = fabsf(x_cur[c]), g = gn_cur[c];
                         const float hb = g < mu ? g * g * inv2mu : g - hmu;
                         fa[0] += wl1[c] * ax;
