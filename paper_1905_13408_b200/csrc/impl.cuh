@@ -423,6 +423,12 @@ struct Impl final : ImplBase {
     // measured neutral (dependents cannot start work before the predecessor
     // completes) or slower with an early trigger (waiting CTAs hold SM slots)
     bool use_pdl = std::getenv("CM_PDL") != nullptr;
+    // z pass L2 prefetch lookahead (tiles) for S rows and the W / Yh blocks
+    // (profiles/r2_ab_zpf.txt, 512^3: the CTA's own W / Yh block requested at
+    // CTA start, 0.434 -> 0.413 ms; S rows of later tiles or W / Yh of a later
+    // tile are slower; CM_Z_PFW=-1 disables)
+    int z_pf = std::getenv("CM_Z_PF") ? std::atoi(std::getenv("CM_Z_PF")) : 0;
+    int z_pfw = std::getenv("CM_Z_PFW") ? std::atoi(std::getenv("CM_Z_PFW")) : 0;
     cudaGraphExec_t gexec = nullptr;  // instantiated 6-iteration chunk (reused while gkey holds)
     std::vector<uint64_t> gkey;
     // fused y/x plane pairs (xyfused.cuh): fp32 power-of-two sides 256..1024
@@ -794,6 +800,8 @@ struct Impl final : ImplBase {
     int launch_z(double* part, DevState* s) {
         using ZG = ZGeo<R, N>;
         ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
+        p.pf = z_pf;
+        p.pfw = z_pfw;
         dim3 grid(Nh / ZG::TW, N);
         CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
         if constexpr (MODE != ZM_FWD)
@@ -1220,22 +1228,63 @@ struct Impl final : ImplBase {
             // close the last trace row: fit(x_K) and the penalties of x_K under the
             // weights of iteration K-1 (regularizer.cpp:208)
             CKS(launch_z<ZM_FIT>(part3, nullptr));
-            XParams<R> p = xp();
-            p.eps = c->eps;
-            p.eps_prime = c->eps_prime;
-            p.mu = c->mu;
-            p.convex = convex;
-            p.audit = 1;
-            p.anchor = anchor;
-            p.part = part1;
-            p.xcur = X[K % 3];
-            p.xprev = refresh_inner ? X[(K + 2) % 3] : nullptr;
-            p.wsrc = wfixed ? wfixed : p.xcur;
-            CKS(launch_x<XM_OBJ>(p));
+            // the penalties: the z-marching sweep in its objective-only mode (the
+            // same partial slots as a per-iteration audit; 1.9 -> ~0.4 ms at 512^3
+            // against the scalar xline epilogue), else the generic line kernel
+            int nb1 = NB1;
+            bool done_s2 = false;
+            if constexpr (S2) {
+                if (!fista && std::getenv("CM_STENCIL1") == nullptr) {
+                    StencilParams<R> q{};
+                    q.g = gbuf;  // read by the ring, unused without an update
+                    q.st = nullptr;
+                    q.lr = lr;
+                    q.alpha = c->alpha;
+                    q.beta = c->beta;
+                    q.gamma = c->gamma;
+                    q.eps = c->eps;
+                    q.eps_prime = c->eps_prime;
+                    q.mu = c->mu;
+                    q.convex = convex;
+                    q.audit = 1;
+                    q.trace_full = want_trace;
+                    q.anchor = anchor;
+                    q.part = part1;
+                    q.koff = 0;
+                    q.nk = N;
+                    q.zshift = 0;
+                    q.obj_only = 1;
+                    q.xcur = X[K % 3];
+                    q.xnext = X[(K + 1) % 3];
+                    q.xprev = refresh_inner ? X[(K + 2) % 3] : nullptr;
+                    if (wfixed) {
+                        q.wtvf = wtvf;
+                        q.wl1src = wfixed;
+                    }
+                    CK(stencil2_launch<N>(q, s2_grid, stream, tm2_x[K % 3], tm2_p[(K + 2) % 3], tm2_g,
+                                          tm2_a));
+                    nb1 = s2_grid;
+                    done_s2 = true;
+                }
+            }
+            if (!done_s2) {
+                XParams<R> p = xp();
+                p.eps = c->eps;
+                p.eps_prime = c->eps_prime;
+                p.mu = c->mu;
+                p.convex = convex;
+                p.audit = 1;
+                p.anchor = anchor;
+                p.part = part1;
+                p.xcur = X[K % 3];
+                p.xprev = refresh_inner ? X[(K + 2) % 3] : nullptr;
+                p.wsrc = wfixed ? wfixed : p.xcur;
+                CKS(launch_x<XM_OBJ>(p));
+            }
             FinParams f{};
             f.st = st;
             f.part1 = part1;
-            f.nb1 = NB1;
+            f.nb1 = nb1;
             f.part3 = part3;
             f.nb3 = NB3;
             f.trace = want_trace ? trace_d : nullptr;

@@ -38,6 +38,9 @@ template <typename R> struct ZMParams {
     // b-slab ranks with split column halves: stored row length and the first
     // (global) column of this launch; one GPU: N/2 and 0 (compile-time there)
     int hlen, h0;
+    // one GPU: L2 prefetch lookahead in tiles for S (rows of tile + pf) and for
+    // the contiguous W / Yh tiles (tile + pfw; -1: off); 0 / -1 disable
+    int pf = 0, pfw = -1;
 };
 
 #ifndef CM_Z_E8
@@ -117,6 +120,28 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         // the y-forward pass of the stopping iteration has run; stop the next one
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) p.st->done_y = 1;
         return;
+    }
+    if constexpr (NR != 0) {
+        // L2 prefetch of a later tile (no registers or shared memory held): the
+        // pass is latency bound with two CTAs per SM, so the S rows of tile + pf
+        // and the z-tiled W / Yh block of tile + pfw are requested ahead
+        const int tl = blockIdx.y * gridDim.x + blockIdx.x, ntl = (Nh / ZGeo<R, N>::TW) * NR;
+        if (p.pf > 0 && tl + p.pf < ntl) {
+            const int t2 = tl + p.pf;
+            const Cx<R>* rowp = p.S + (size_t)(t2 / (Nh / ZGeo<R, N>::TW)) * Nh +
+                                (t2 % (Nh / ZGeo<R, N>::TW)) * ZGeo<R, N>::TW;
+            for (int c = threadIdx.x; c < N; c += blockDim.x)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + (size_t)c * NR * Nh));
+        }
+        // (bulk prefetch: 16-byte aligned blocks whose size is a multiple of 16)
+        constexpr bool PFW_OK = ((size_t)N * ZGeo<R, N>::TW * sizeof(R)) % 16 == 0;
+        if (PFW_OK && MODE != ZM_FWD && p.pfw >= 0 && tl + p.pfw < ntl && threadIdx.x == 0) {
+            const size_t o = (size_t)(tl + p.pfw) * N * ZGeo<R, N>::TW;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.W + o),
+                         "r"((uint32_t)(N * ZGeo<R, N>::TW * sizeof(R))) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.Yh + o),
+                         "r"((uint32_t)(N * ZGeo<R, N>::TW * sizeof(Cx<R>))) : "memory");
+        }
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* tw = reinterpret_cast<C*>(smem_raw);
