@@ -397,7 +397,8 @@ struct Impl final : ImplBase {
     CUtensorMap tm_at = {};    // anchor tiles
     // z-marching stencil (fp32, N >= 128, N % 8 == 0; the last 128-wide x tile
     // partial when 128 does not divide N): per-plane slab maps
-    static constexpr bool S2 = sizeof(R) == 4 && N >= 128 && N % 8 == 0;
+    // z-marching sweep (stencil2.cuh): fp32, and the fp64 parity mode (2 voxels per lane)
+    static constexpr bool S2 = N >= 128 && N % 8 == 0;
     CUtensorMap tm2_x[5] = {}, tm2_p[3] = {}, tm2_g = {}, tm2_a = {};
     int s2_grid = 0;
     int sweep_grid = 0;        // persistent stencil CTAs
@@ -482,16 +483,15 @@ struct Impl final : ImplBase {
     long long bytes() const override { return alloc_bytes; }
 
     int make_map_box(R* ptr, CUtensorMap* out, cuuint32_t bw, cuuint32_t bj, cuuint32_t bk) {
-        if constexpr (sizeof(R) != 4) {
-            return CM_OK;
-        } else {
+        {
             EncodeTiledFn enc = encode_tiled_fn();
             if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
             const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
             const cuuint64_t strides[2] = {(cuuint64_t)N * sizeof(R), (cuuint64_t)N * N * sizeof(R)};
             const cuuint32_t box[3] = {bw, bj, bk};
             const cuuint32_t es[3] = {1, 1, 1};
-            CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
+            CUresult r = enc(out, sizeof(R) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                             3, ptr, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(CM_ERR_CUDA, "tensor map encode failed");
@@ -502,7 +502,7 @@ struct Impl final : ImplBase {
         if constexpr (!S2) {
             return CM_OK;
         } else {
-            using SG = S2Geo<N>;
+            using SG = S2GeoT<R, N>;
             CKS(make_map_box(ptr, &tm2_x[which], SG::XW, SG::XR, 1));
             if (which < 3) CKS(make_map_box(ptr, &tm2_p[which], SG::XW, SG::PR, 1));
             return CM_OK;
@@ -623,13 +623,13 @@ struct Impl final : ImplBase {
         CKS(make_map_x(gbuf, &tm_gt, 2));
         CKS(make_map_x(anchor, &tm_at, 2));
         if constexpr (S2) {
-            using SG = S2Geo<N>;
+            using SG = S2GeoT<R, N>;
             for (int q = 0; q < 3; ++q) CKS(make_maps2(q, X[q]));
             CKS(make_map_box(gbuf, &tm2_g, SG::CI, SG::TJ, 1));
             CKS(make_map_box(anchor, &tm2_a, SG::CI, SG::TJ, 1));
-            CK(stencil2_prepare<N>());
+            CK((stencil2_prepare<N, R>()));
             int occ2 = 0, dev2 = 0, sms2 = 0;
-            CK(stencil2_occupancy<N>(&occ2));
+            CK((stencil2_occupancy<N, R>(&occ2)));
             CK(cudaGetDevice(&dev2));
             CK(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2));
             s2_grid = std::max(1, std::min(SG::NTILES, sms2 * std::max(occ2, 1)));
@@ -665,6 +665,17 @@ struct Impl final : ImplBase {
                 std::fprintf(stderr, "k1f: N=%d grid=%d CTAs (%d clusters of %d), smem=%zu\n", N, k1f_grid_,
                              k1f_grid_ / K1Geo<N>::NCL, K1Geo<N>::NCL, K1Geo<N>::SMEM);
             if (k1f_grid_ <= 0) use_k1f = false;
+        }
+        {
+            // the persistent sweeps write one partial-sum slot per CTA: part1 must
+            // hold the largest of their grids (the z-marching sweep's grid is known
+            // only now; at 160^3 its 592 CTAs overran the 400 slots allocated above)
+            const int need = std::max(std::max(NB1, sweep_grid), std::max(s2_grid, k1f_grid_));
+            if (need > std::max(NB1, sweep_grid)) {
+                CK(cudaFree(part1));
+                part1 = nullptr;
+                CKS(dalloc(&part1, (size_t)need * NP1));
+            }
         }
         if constexpr (YT) {
             using YG_ = YtGeo<N>;
@@ -1234,7 +1245,7 @@ struct Impl final : ImplBase {
             int nb1 = NB1;
             bool done_s2 = false;
             if constexpr (S2) {
-                if (!fista && std::getenv("CM_STENCIL1") == nullptr) {
+                if (!fista && std::getenv("CM_STENCIL1") == nullptr && std::getenv("CM_EPI_XLINE") == nullptr) {
                     StencilParams<R> q{};
                     q.g = gbuf;  // read by the ring, unused without an update
                     q.st = nullptr;

@@ -1,12 +1,13 @@
-// K1 (fp32, N % 128 == 0) — z-marching register-blocked stencil sweep.
+// K1 (fp32 and fp64, N >= 128, N % 8 == 0) — z-marching register-blocked stencil sweep.
 //
 // Same mathematics as stencil.cuh (regularizer.cpp:44-59, 72-85, 103-110,
 // 125-149, 193-205; gradient.cpp:7-64), reorganised so that every TV dual scale
 //     s(q) = w_tv(q) / max(mu, |Dx(q)|) = 1 / ((|Dx(q)| + eps') max(mu, |Dx(q)|))
 // is computed exactly once and every input sample is read from shared memory
 // once per use:
-//   * a CTA owns a 128 (x) by TJ (y) column of voxels and marches along z over
-//     KC planes; warp w owns row j0 + w, lane l owns x = i0 + 4l .. 4l+3; one
+//   * a CTA owns a CI = 32 VW (x) by TJ (y) column of voxels and marches along z over
+//     KC planes; warp w owns row j0 + w, lane l owns x = i0 + VW l .. VW l + VW-1 (VW = 4
+//     in fp32, 2 in the fp64 parity mode); one
 //     extra warp computes s on the forward halo row j0 + TJ;
 //   * per plane q, TMA brings the x slab (rows j0-1 .. j0+TJ, x halo +-1), the
 //     x_{i-1} slab (rows j0-1 .. j0+TJ-1), and the g and anchor rows into a
@@ -27,6 +28,9 @@
 #ifndef CM_S2_MINB
 #define CM_S2_MINB 4
 #endif
+#ifndef CM_S2_MINB_D
+#define CM_S2_MINB_D 3  // fp64: 136 registers (double accumulators and parameters)
+#endif
 #ifndef CM_S2_TJ
 #define CM_S2_TJ 4  // rows per CTA (+1 halo-row warp); 4 CTAs per SM (8: 2 CTAs, 3.5% slower)
 #endif
@@ -37,14 +41,14 @@ namespace cm {
 // busiest CTA slot (148 SMs x CM_S2_MINB), ceil(tiles / slots) x (KC + 2 for the
 // march prologue); ties keep the longer march. 512^3 / 384^3 / 256^3: 64; 128^3:
 // 8 (64-plane marches ran 64 CTAs for the whole sweep: 57 -> 19 us)
-__host__ __device__ constexpr int s2_kc(int n) {
+__host__ __device__ constexpr int s2_kc(int n, int ci = 128, int minb = CM_S2_MINB) {
     if (n < 64) return n;
     int best = 64;
     long best_cost = -1;
     for (int kc = 64; kc >= 8; kc /= 2) {
         if (n % kc) continue;
-        const long tiles = (long)((n + 127) / 128) * (n / CM_S2_TJ) * (n / kc);
-        const long slots = 148L * CM_S2_MINB;
+        const long tiles = (long)((n + ci - 1) / ci) * (n / CM_S2_TJ) * (n / kc);
+        const long slots = 148L * minb;
         const long cost = (tiles + slots - 1) / slots * (kc + 2);
         if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
@@ -54,36 +58,51 @@ __host__ __device__ constexpr int s2_kc(int n) {
     return best;
 }
 
-template <int N> struct S2Geo {
-    static constexpr int CI = 128;
+// real-type overloads (no implicit float -> double promotion in the fp32 sweep)
+__device__ __forceinline__ float s2abs(float v) { return fabsf(v); }
+__device__ __forceinline__ double s2abs(double v) { return fabs(v); }
+__device__ __forceinline__ float s2min(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double s2min(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float s2max(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double s2max(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float s2fma(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double s2fma(double a, double b, double c) { return fma(a, b, c); }
+
+// R = float: 4 voxels (one float4) per lane, 128-wide x tiles; R = double (the
+// fp64 parity mode): 2 voxels (one double2) per lane, 64-wide x tiles
+template <typename R, int N> struct S2GeoT {
+    static constexpr int VW = 16 / (int)sizeof(R);  // voxels per lane
+    static constexpr int CI = 32 * VW;
+    static constexpr int MINB = sizeof(R) == 4 ? CM_S2_MINB : CM_S2_MINB_D;
     static constexpr int TJ = CM_S2_TJ;
-    static constexpr int KC = s2_kc(N);          // planes per march
+    static constexpr int KC = s2_kc(N, CI, MINB);  // planes per march
     static constexpr int NW = TJ + 1;            // + halo-row warp
     static constexpr int NT = NW * 32;
-    static constexpr int XW = 136;               // slab row: global i0-4 .. i0+131
+    static constexpr int XW = CI + 2 * VW;       // slab row: global i0-VW .. i0+CI+VW-1
     static constexpr int XR = TJ + 2;            // x rows j0-1 .. j0+TJ
     static constexpr int PR = TJ + 1;            // x_prev rows j0-1 .. j0+TJ-1
     static constexpr int GR = TJ;                // g / anchor rows j0 .. j0+TJ-1
-    static constexpr uint32_t XB = XR * XW * 4, PB = PR * XW * 4, GB = GR * CI * 4;
+    static constexpr uint32_t XB = XR * XW * sizeof(R), PB = PR * XW * sizeof(R), GB = GR * CI * sizeof(R);
     static constexpr size_t al(size_t v) { return (v + 127) / 128 * 128; }
     static constexpr size_t OFF_P = al(XB), OFF_G = al(OFF_P + PB), OFF_A = al(OFF_G + GB);
     static constexpr size_t STAGE = al(OFF_A + GB);
     static constexpr int NSTAGE = 4;
-    static constexpr int SW = CI + 4;            // s row (+ halo column at CI)
+    static constexpr int SW = CI + VW;           // s row (+ halo column at CI)
     static constexpr size_t OFF_S = NSTAGE * STAGE;
     static constexpr size_t SROW3 = (size_t)(TJ + 1) * SW;   // floats per s ring slot
-    static constexpr size_t S_BYTES = 3 * SROW3 * 4;
+    static constexpr size_t S_BYTES = 3 * SROW3 * sizeof(R);
     static constexpr size_t OFF_RED = al(OFF_S + S_BYTES);
     static constexpr size_t OFF_BAR = OFF_RED + 32 * NP1 * 8;
     static constexpr size_t SMEM = OFF_BAR + NSTAGE * 8;
     static constexpr int NTI = (N + CI - 1) / CI, NTJ = N / TJ, NTK = N / KC;  // last x tile partial
     static constexpr int NTILES = NTI * NTJ * NTK;  // single GPU (nk = N)
 };
+template <int N> using S2Geo = S2GeoT<float, N>;
 
 #ifdef CM_S2_MAXREG
 #define CM_S2_BOUNDS __maxnreg__(CM_S2_MAXREG)
 #else
-#define CM_S2_BOUNDS __launch_bounds__(S2Geo<N>::NT, CM_S2_MINB)
+#define CM_S2_BOUNDS __launch_bounds__(S2GeoT<R, N>::NT, S2GeoT<R, N>::MINB)
 #endif
 
 // compile-time mode of a sweep: dead terms, branches and accumulators vanish
@@ -97,12 +116,14 @@ __host__ __device__ constexpr unsigned s2_used(int F) {
            ((F & S2_STEP) ? 512u | 1024u : 0u) | ((F & S2_FISTA) ? 2048u : 0u);
 }
 
-template <int N, int F>
+template <typename R, int N, int F>
 __global__ void CM_S2_BOUNDS
-stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
+stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
                 const __grid_constant__ CUtensorMap tmp, const __grid_constant__ CUtensorMap tmg,
                 const __grid_constant__ CUtensorMap tma) {
-    using G = S2Geo<N>;
+    using G = S2GeoT<R, N>;
+    using V = Vec16<R>;
+    constexpr int VW = G::VW;
     constexpr bool AUDIT = F & S2_AUDIT, PREV = AUDIT && (F & S2_PREV);
     constexpr bool TRACE = AUDIT && (F & S2_TRACE), STEP = F & S2_STEP, FISTA = F & S2_FISTA;
     constexpr unsigned USED = s2_used(F);
@@ -111,7 +132,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     pdl_wait();
     if (p.st && ld_done(p.st)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* Sring = reinterpret_cast<float*>(smem_raw + G::OFF_S);   // [3][TJ+1][SW]
+    R* Sring = reinterpret_cast<R*>(smem_raw + G::OFF_S);   // [3][TJ+1][SW]
     double* red = reinterpret_cast<double*>(smem_raw + G::OFF_RED);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + G::OFF_BAR);
     const uint32_t smem_s = smem_u32(smem_raw), bar_s = smem_s + (uint32_t)G::OFF_BAR;
@@ -119,14 +140,14 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;  // w = row within tile, TJ = halo
     const bool halo = (w == TJ);
     // fp32 parameters as references into the (constant-bank) kernel parameters
-    const float &eps = p.f_eps, &epsp = p.f_epsp, &mu = p.f_mu, &lr = p.f_lr, &lra = p.f_lra;
-    const float &beta = p.f_beta, &g2 = p.f_g2, &inv2mu = p.f_inv2mu, &hmu = p.f_hmu;
-    const float &cg = p.f_cg, &ce = p.f_ce;
+    const R &eps = p.f_eps, &epsp = p.f_epsp, &mu = p.f_mu, &lr = p.f_lr, &lra = p.f_lra;
+    const R &beta = p.f_beta, &g2 = p.f_g2, &inv2mu = p.f_inv2mu, &hmu = p.f_hmu;
+    const R &cg = p.f_cg, &ce = p.f_ce;
     const bool has_beta = p.beta > 0.0, has_alpha = p.alpha > 0.0;
     constexpr bool with_prev = PREV;
     const bool convex = p.convex != 0;
     // s = 1/((g cg + ce) max(mu, g)): (cg, ce) = (1, eps') reweighted, (0, 1) convex
-    const float theta = (FISTA && p.st) ? float(p.theta[p.st->iter - p.st->mom_base]) : 0.f;
+    const R theta = (FISTA && p.st) ? R(p.theta[p.st->iter - p.st->mom_base]) : R(0);
 
     if (tid == 0) {
         for (int q = 0; q < G::NSTAGE; ++q) mbar_init(&bar[q], 1);
@@ -136,10 +157,10 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
     for (int q = tid; q < 32 * NP1; q += blockDim.x) red[q] = 0.0;
     __syncthreads();
 
-    // fp32 partials: fa over 8 planes, fb over the tile, then fp64 per warp
-    float fa[NP1], fb[NP1];
+    // partials in R: fa over 8 planes, fb over the tile, then fp64 per warp
+    R fa[NP1], fb[NP1];
 #pragma unroll
-    for (int q = 0; q < NP1; ++q) fa[q] = fb[q] = 0.f;
+    for (int q = 0; q < NP1; ++q) fa[q] = fb[q] = R(0);
 
     uint32_t phase_bits = 0;  // parity of the next wait on each ring slot
     const int koff = p.koff, zs = p.zshift;
@@ -156,8 +177,8 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
             const int sl = slot_of(q);
             const uint32_t bs = bar_s + 8u * sl, ss = smem_s + (uint32_t)((size_t)sl * G::STAGE);
             mbar_expect_tx_s(bs, G::XB + (with_prev ? G::PB : 0u) + 2 * G::GB);
-            tma_load_3d_s(ss, &tmx, i0 - 4, j0 - 1, q + zs, bs);
-            if (with_prev) tma_load_3d_s(ss + (uint32_t)G::OFF_P, &tmp, i0 - 4, j0 - 1, q + zs, bs);
+            tma_load_3d_s(ss, &tmx, i0 - VW, j0 - 1, q + zs, bs);
+            if (with_prev) tma_load_3d_s(ss + (uint32_t)G::OFF_P, &tmp, i0 - VW, j0 - 1, q + zs, bs);
             // g / anchor rows of planes past the march are never read; out of grid -> 0
             tma_load_3d_s(ss + (uint32_t)G::OFF_G, &tmg, i0, j0, q + zs, bs);
             tma_load_3d_s(ss + (uint32_t)G::OFF_A, &tma, i0, j0, q + zs, bs);
@@ -176,10 +197,10 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         wait(k0);
 
         const int gj = j0 + w;                 // this warp's row (halo warp: j0 + TJ)
-        const int ii = 4 * lane;
+        const int ii = VW * lane;
         const int gi0 = i0 + ii;
         const bool row_in = gj < N;
-        // partial last x tile (N % 128 != 0): the lane's 4 voxels are all in or
+        // partial last x tile (N % CI != 0): the lane's VW voxels are all in or
         // all out; out-of-grid lanes keep s = 0 and join the shuffles, but load,
         // store and accumulate nothing
         const bool col_in = gi0 < N;
@@ -189,229 +210,241 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
         const int ry = gj > 0 ? w : w + 1;     // slab row of j-1
         const bool xlo = (i0 == 0);
         // x slab row r (global j0 - 1 + r) of plane q, at this lane's 4 voxels
-        auto xrow = [&](int q, int r) -> const float* {
-            return reinterpret_cast<const float*>(stage(q)) + r * XW + 4 + ii;
+        auto xrow = [&](int q, int r) -> const R* {
+            return reinterpret_cast<const R*>(stage(q)) + r * XW + VW + ii;
         };
         // s on row w of plane q from the slabs of q and q-1 (rows w+1, w in slab coords)
         // returns s[4], plus |Dx|, d-sum for the voxels; halo column (i0+CI) via lane 31
-        auto s_row = [&](int q, float (&xq)[4], float (&sv)[4], float (&gn)[4], float (&ds)[4]) {
-            const float* xr = xrow(q, w + 1);
-            const float* yr = xrow(q, ry);
-            const float* zr = koff + q > 0 ? xrow(q - 1, w + 1) : xr;
-            const float4 c4 = ld4(xr), y4 = ld4(yr), z4 = ld4(zr);
-            xq[0] = c4.x; xq[1] = c4.y; xq[2] = c4.z; xq[3] = c4.w;
-            const float yv[4] = {y4.x, y4.y, y4.z, y4.w}, zv[4] = {z4.x, z4.y, z4.z, z4.w};
-            float xl = __shfl_up_sync(0xffffffffu, c4.w, 1);
-            if (lane == 0) xl = xlo ? c4.x : xr[-1];
-            const float xlv[4] = {xl, c4.x, c4.y, c4.z};
+        auto s_row = [&](int q, R (&xq)[VW], R (&sv)[VW], R (&gn)[VW], R (&ds)[VW]) {
+            const R* xr = xrow(q, w + 1);
+            const R* yr = xrow(q, ry);
+            const R* zr = koff + q > 0 ? xrow(q - 1, w + 1) : xr;
+            R yv[VW], zv[VW];
+            V::ld(xr, xq);
+            V::ld(yr, yv);
+            V::ld(zr, zv);
+            R xl = __shfl_up_sync(0xffffffffu, xq[VW - 1], 1);
+            if (lane == 0) xl = xlo ? xq[0] : xr[-1];
+            R xlv[VW];
+            xlv[0] = xl;
+#pragma unroll
+            for (int c = 1; c < VW; ++c) xlv[c] = xq[c - 1];
             const bool qin = koff + q < N && row_in && col_in;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float d1 = xq[c] - xlv[c], d2 = xq[c] - yv[c], d3 = xq[c] - zv[c];
-                const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
-                const float mx = mu > g ? mu : g;
-                const float s = rcp_(fmaf(g, cg, ce) * mx);  // convex: 1/mx
-                sv[c] = qin ? s : 0.f;
+            for (int c = 0; c < VW; ++c) {
+                const R d1 = xq[c] - xlv[c], d2 = xq[c] - yv[c], d3 = xq[c] - zv[c];
+                const R g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+                const R mx = mu > g ? mu : g;
+                const R s = rcp_(s2fma(g, cg, ce) * mx);  // convex: 1/mx
+                sv[c] = qin ? s : R(0);
                 gn[c] = g;
                 ds[c] = d1 + d2 + d3;
             }
         };
         // s on the column x = i0 + CI of tile row `lane` (0 .. TJ): computed by the
         // halo-row warp, so the row warps carry no divergent halo-column work
-        auto s_col = [&](int q) -> float {
+        auto s_col = [&](int q) -> R {
             const int r = lane, gjr = j0 + lane;
-            if (r > TJ || koff + q >= N || gjr >= N || i0 + CI >= N) return 0.f;
-            const float* xb = reinterpret_cast<const float*>(stage(q)) + 4 + CI;
-            const float* zb = koff + q > 0 ? reinterpret_cast<const float*>(stage(q - 1)) + 4 + CI : xb;
-            const float xc = xb[(r + 1) * XW];
-            const float d1 = xc - xb[(r + 1) * XW - 1];
-            const float d2 = xc - xb[(gjr > 0 ? r : r + 1) * XW];
-            const float d3 = xc - zb[(r + 1) * XW];
-            const float g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
-            const float mx = fmaxf(mu, g);
+            if (r > TJ || koff + q >= N || gjr >= N || i0 + CI >= N) return R(0);
+            const R* xb = reinterpret_cast<const R*>(stage(q)) + VW + CI;
+            const R* zb = koff + q > 0 ? reinterpret_cast<const R*>(stage(q - 1)) + VW + CI : xb;
+            const R xc = xb[(r + 1) * XW];
+            const R d1 = xc - xb[(r + 1) * XW - 1];
+            const R d2 = xc - xb[(gjr > 0 ? r : r + 1) * XW];
+            const R d3 = xc - zb[(r + 1) * XW];
+            const R g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
+            const R mx = mu > g ? mu : g;
             if (p.wtvf && !convex)
                 return __ldg(p.wtvf + ((size_t)(q + zs) * N + gjr) * N + i0 + CI) * rcp_(mx);
-            return rcp_(fmaf(g, cg, ce) * mx);
+            return rcp_(s2fma(g, cg, ce) * mx);
         };
         // per_m_step weights come from a frozen field: s uses w_tv from it
-        auto apply_wtvf = [&](int q, float (&sv)[4], float (&gn)[4]) {
+        auto apply_wtvf = [&](int q, R (&sv)[VW], R (&gn)[VW]) {
             if (!p.wtvf || convex || !(koff + q < N && row_in && col_in)) return;
-            const float4 wv = __ldg(reinterpret_cast<const float4*>(
-                p.wtvf + ((size_t)(q + zs) * N + gj) * N + gi0));
-            const float wt[4] = {wv.x, wv.y, wv.z, wv.w};
+            R wt[VW];
+            V::ldg(p.wtvf + ((size_t)(q + zs) * N + gj) * N + gi0, wt);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float mx = mu > gn[c] ? mu : gn[c];
+            for (int c = 0; c < VW; ++c) {
+                const R mx = mu > gn[c] ? mu : gn[c];
                 sv[c] = wt[c] * rcp_(mx);
             }
         };
 
         // ---- prologue: s(., k0), rolling state of plane k0 and x_prev(k0-1)
-        float x_cur[4], s_cur[4], gn_cur[4], ds_cur[4];
+        R x_cur[VW], s_cur[VW], gn_cur[VW], ds_cur[VW];
         s_row(k0, x_cur, s_cur, gn_cur, ds_cur);
         apply_wtvf(k0, s_cur, gn_cur);
         // s ring: plane k in slot (k - k0) % 3, rotated by pointer
-        float* Sc_ring = Sring;                        // slot of plane k
-        float* Sn_ring = Sring + G::SROW3;             // slot of plane k + 1
-        float* Sx_ring = Sring + 2 * G::SROW3;         // the third slot
-        float* S0 = Sc_ring;
+        R* Sc_ring = Sring;                        // slot of plane k
+        R* Sn_ring = Sring + G::SROW3;             // slot of plane k + 1
+        R* Sx_ring = Sring + 2 * G::SROW3;         // the third slot
+        R* S0 = Sc_ring;
         if (has_beta) {
-            *reinterpret_cast<float4*>(S0 + w * SW + ii) =
-                make_float4(s_cur[0], s_cur[1], s_cur[2], s_cur[3]);
+            V::st(S0 + w * SW + ii, s_cur);
             if (halo && lane <= TJ) S0[lane * SW + CI] = s_col(k0);
         }
-        float xp_prev[4] = {0.f, 0.f, 0.f, 0.f};
+        R xp_prev[VW];
+#pragma unroll
+        for (int c = 0; c < VW; ++c) xp_prev[c] = R(0);
         if (with_prev && !halo) {
             // plane k0-1 of x_prev (the plane itself at the global first plane)
-            const float4 v = ld4(reinterpret_cast<const float*>(stage(koff + k0 > 0 ? k0 - 1 : k0) +
-                                                                G::OFF_P) + (w + 1) * XW + 4 + ii);
-            xp_prev[0] = v.x; xp_prev[1] = v.y; xp_prev[2] = v.z; xp_prev[3] = v.w;
+            V::ld(reinterpret_cast<const R*>(stage(koff + k0 > 0 ? k0 - 1 : k0) + G::OFF_P) +
+                      (w + 1) * XW + VW + ii,
+                  xp_prev);
         }
         __syncthreads();
 
         // one plane of the march; the rolling state alternates between two
         // register sets (the loop is unrolled by two) instead of being copied
-        float x_nb[4], s_nb[4], gn_nb[4], ds_nb[4];
-        auto step = [&](int k, float (&x_cur)[4], float (&s_cur)[4], float (&gn_cur)[4],
-                        float (&ds_cur)[4], float (&x_nx)[4], float (&s_nx)[4],
-                        float (&gn_nx)[4], float (&ds_nx)[4]) {
+        R x_nb[VW], s_nb[VW], gn_nb[VW], ds_nb[VW];
+        auto step = [&](int k, R (&x_cur)[VW], R (&s_cur)[VW], R (&gn_cur)[VW],
+                        R (&ds_cur)[VW], R (&x_nx)[VW], R (&s_nx)[VW],
+                        R (&gn_nx)[VW], R (&ds_nx)[VW]) {
             if (tid == 0) issue(k + 2);  // slot of plane k-2: released by the previous barrier
             wait(k + 1);
             // ---- s of plane k+1 on this warp's row
             s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx);
             apply_wtvf(k + 1, s_nx, gn_nx);
-            float* Sn = Sn_ring;
+            R* Sn = Sn_ring;
             if (has_beta) {
-                *reinterpret_cast<float4*>(Sn + w * SW + ii) =
-                    make_float4(s_nx[0], s_nx[1], s_nx[2], s_nx[3]);
+                V::st(Sn + w * SW + ii, s_nx);
                 if (halo && lane <= TJ) Sn[lane * SW + CI] = s_col(k + 1);
             }
             __syncthreads();
             if (!halo && row_in) {
                 // ---- voxel (j, k): update, prox, partials
-                const float* Sc = Sc_ring;
+                const R* Sc = Sc_ring;
                 const size_t gidx = ((size_t)(k + zs) * N + gj) * N + gi0;
                 const unsigned char* stk = stage(k);
-                const float4 g4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_G) + w * CI + ii);
-                const float4 a4 = ld4(reinterpret_cast<const float*>(stk + G::OFF_A) + w * CI + ii);
-                const float gg[4] = {g4.x, g4.y, g4.z, g4.w}, av[4] = {a4.x, a4.y, a4.z, a4.w};
-                float tvg[4] = {0.f, 0.f, 0.f, 0.f};
+                R gg[VW], av[VW];
+                V::ld(reinterpret_cast<const R*>(stk + G::OFF_G) + w * CI + ii, gg);
+                V::ld(reinterpret_cast<const R*>(stk + G::OFF_A) + w * CI + ii, av);
+                R tvg[VW];
+#pragma unroll
+                for (int c = 0; c < VW; ++c) tvg[c] = R(0);
                 if (has_beta) {
                     // x(j+1, k) and s(j+1, k): next row; x(i+1), s(i+1): next voxel
-                    const float4 yp4 = ld4(xrow(k, w + 2));
-                    const float4 sy4 = ld4(Sc + (w + 1) * SW + ii);
-                    float xr4 = __shfl_down_sync(0xffffffffu, x_cur[0], 1);
-                    float sr4 = __shfl_down_sync(0xffffffffu, s_cur[0], 1);
+                    R yp[VW], sy[VW];
+                    V::ld(xrow(k, w + 2), yp);
+                    V::ld(Sc + (w + 1) * SW + ii, sy);
+                    R xr4 = __shfl_down_sync(0xffffffffu, x_cur[0], 1);
+                    R sr4 = __shfl_down_sync(0xffffffffu, s_cur[0], 1);
                     if (lane == 31) {
-                        xr4 = xrow(k, w + 1)[4];          // x at i0 + CI
+                        xr4 = xrow(k, w + 1)[VW];         // x at i0 + CI
                         sr4 = Sc[w * SW + CI];
                     }
-                    const float xn[4] = {x_cur[1], x_cur[2], x_cur[3], xr4};
-                    const float sxv[4] = {s_cur[1], s_cur[2], s_cur[3], sr4};
-                    const float yp[4] = {yp4.x, yp4.y, yp4.z, yp4.w};
-                    const float sy[4] = {sy4.x, sy4.y, sy4.z, sy4.w};
+                    R xn[VW], sxv[VW];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c + 1 < VW; ++c) {
+                        xn[c] = x_cur[c + 1];
+                        sxv[c] = s_cur[c + 1];
+                    }
+                    xn[VW - 1] = xr4;
+                    sxv[VW - 1] = sr4;
+#pragma unroll
+                    for (int c = 0; c < VW; ++c)
                         tvg[c] = s_cur[c] * ds_cur[c] - sxv[c] * (xn[c] - x_cur[c]) -
                                  sy[c] * (yp[c] - x_cur[c]) - s_nx[c] * (x_nx[c] - x_cur[c]);
                 }
-                float wl1[4] = {1.f, 1.f, 1.f, 1.f}, wtv[4] = {1.f, 1.f, 1.f, 1.f};
+                R wl1[VW], wtv[VW];
+#pragma unroll
+                for (int c = 0; c < VW; ++c) wl1[c] = wtv[c] = R(1);
                 if (!convex) {
-                    float ws[4] = {x_cur[0], x_cur[1], x_cur[2], x_cur[3]};
+                    R ws[VW];
+#pragma unroll
+                    for (int c = 0; c < VW; ++c) ws[c] = x_cur[c];
                     if (p.wl1src) {
                         if (p.wl1src == p.anchor) {
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) ws[c] = av[c];
+                            for (int c = 0; c < VW; ++c) ws[c] = av[c];
                         } else if (col_in) {
-                            const float4 v = __ldg(reinterpret_cast<const float4*>(p.wl1src + gidx));
-                            ws[0] = v.x; ws[1] = v.y; ws[2] = v.z; ws[3] = v.w;
+                            V::ldg(p.wl1src + gidx, ws);
                         }
                     }
                     if (p.wtvf) {
-                        const float4 v = col_in ? __ldg(reinterpret_cast<const float4*>(p.wtvf + gidx))
-                                                : make_float4(1.f, 1.f, 1.f, 1.f);
-                        wtv[0] = v.x; wtv[1] = v.y; wtv[2] = v.z; wtv[3] = v.w;
+                        if (col_in) V::ldg(p.wtvf + gidx, wtv);
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) wl1[c] = rcp_(fabsf(ws[c]) + eps);
+                        for (int c = 0; c < VW; ++c) wl1[c] = rcp_(s2abs(ws[c]) + eps);
                     } else {
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const float a = fabsf(ws[c]) + eps, b = gn_cur[c] + epsp;
-                            const float r = rcp_(a * b);
+                        for (int c = 0; c < VW; ++c) {
+                            const R a = s2abs(ws[c]) + eps, b = gn_cur[c] + epsp;
+                            const R r = rcp_(a * b);
                             wl1[c] = b * r;
                             wtv[c] = a * r;
                         }
                     }
                 }
-                float base[4] = {x_cur[0], x_cur[1], x_cur[2], x_cur[3]};
-                if (FISTA && col_in) {
-                    const float4 o4 = __ldg(reinterpret_cast<const float4*>(p.xold + gidx));
-                    base[0] = o4.x; base[1] = o4.y; base[2] = o4.z; base[3] = o4.w;
-                }
-                float nx[4];
+                R base[VW];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    float gs = 2.f * gg[c] + g2 * (x_cur[c] - av[c]);
+                for (int c = 0; c < VW; ++c) base[c] = x_cur[c];
+                if (FISTA && col_in) V::ldg(p.xold + gidx, base);
+                R nx[VW];
+#pragma unroll
+                for (int c = 0; c < VW; ++c) {
+                    R gs = R(2) * gg[c] + g2 * (x_cur[c] - av[c]);
                     if (has_beta) gs += beta * tvg[c];
-                    float v = x_cur[c] - lr * gs;
+                    R v = x_cur[c] - lr * gs;
                     if (has_alpha) {
-                        const float th = lra * wl1[c];
+                        const R th = lra * wl1[c];
                         // soft threshold, |v| <= th -> 0 (regularizer.cpp:107): v - clamp(v)
-                        v = v - fminf(fmaxf(v, -th), th);
+                        v = v - s2min(s2max(v, -th), th);
                     }
                     nx[c] = v;
                 }
-                if (!p.obj_only && col_in)
-                    *reinterpret_cast<float4*>(p.xnext + gidx) = make_float4(nx[0], nx[1], nx[2], nx[3]);
+                if (!p.obj_only && col_in) V::st(p.xnext + gidx, nx);
                 if (FISTA && !p.obj_only && col_in) {
-                    float y[4];
+                    R y[VW];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
-                    *reinterpret_cast<float4*>(p.ynext + gidx) = make_float4(y[0], y[1], y[2], y[3]);
+                    for (int c = 0; c < VW; ++c) y[c] = nx[c] + theta * (nx[c] - base[c]);
+                    V::st(p.ynext + gidx, y);
                 }
                 if (FISTA && col_in) {
                     // restart test (O'Donoghue & Candes): (y_k - x_{k+1}) . (x_{k+1} - x_k)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) fa[11] += (x_cur[c] - nx[c]) * (nx[c] - base[c]);
+                    for (int c = 0; c < VW; ++c) fa[11] += (x_cur[c] - nx[c]) * (nx[c] - base[c]);
                 }
                 if (STEP && col_in) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float dx = nx[c] - base[c];
+                    for (int c = 0; c < VW; ++c) {
+                        const R dx = nx[c] - base[c];
                         fa[9] += dx * dx;
                         fa[10] += nx[c] * nx[c];
                     }
                 }
                 if (AUDIT) {
-                    float pl1[4] = {0.f, 0.f, 0.f, 0.f}, ptv[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (with_prev) {
-                        const float* P = reinterpret_cast<const float*>(stk + G::OFF_P);
-                        const float4 pc4 = ld4(P + (w + 1) * XW + 4 + ii);
-                        const float4 py4 = ld4(P + ry * XW + 4 + ii);
-                        float pm = __shfl_up_sync(0xffffffffu, pc4.w, 1);
-                        if (lane == 0) pm = xlo ? pc4.x : P[(w + 1) * XW + 3];
-                        const float pc[4] = {pc4.x, pc4.y, pc4.z, pc4.w};
-                        const float pl[4] = {pm, pc4.x, pc4.y, pc4.z};
-                        const float py[4] = {py4.x, py4.y, py4.z, py4.w};
+                    R pl1[VW], ptv[VW];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const float e1 = pc[c] - pl[c], e2 = pc[c] - py[c], e3 = pc[c] - xp_prev[c];
-                            const float a = fabsf(pc[c]) + eps;
-                            const float b = sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp;
-                            const float r = rcp_(a * b);
+                    for (int c = 0; c < VW; ++c) pl1[c] = ptv[c] = R(0);
+                    if (with_prev) {
+                        const R* P = reinterpret_cast<const R*>(stk + G::OFF_P);
+                        R pc[VW], py[VW], pl[VW];
+                        V::ld(P + (w + 1) * XW + VW + ii, pc);
+                        V::ld(P + ry * XW + VW + ii, py);
+                        R pm = __shfl_up_sync(0xffffffffu, pc[VW - 1], 1);
+                        if (lane == 0) pm = xlo ? pc[0] : P[(w + 1) * XW + VW - 1];
+                        pl[0] = pm;
+#pragma unroll
+                        for (int c = 1; c < VW; ++c) pl[c] = pc[c - 1];
+#pragma unroll
+                        for (int c = 0; c < VW; ++c) {
+                            const R e1 = pc[c] - pl[c], e2 = pc[c] - py[c], e3 = pc[c] - xp_prev[c];
+                            const R a = s2abs(pc[c]) + eps;
+                            const R b = sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp;
+                            const R r = rcp_(a * b);
                             pl1[c] = b * r;
                             ptv[c] = a * r;
                             xp_prev[c] = pc[c];
                         }
                     }
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < VW; ++c) {
                         if (!col_in) break;
-                        const float ax = fabsf(x_cur[c]), g = gn_cur[c];
-                        const float hb = g < mu ? g * g * inv2mu : g - hmu;
+                        const R ax = s2abs(x_cur[c]), g = gn_cur[c];
+                        const R hb = g < mu ? g * g * inv2mu : g - hmu;
                         fa[0] += wl1[c] * ax;
                         fa[1] += wtv[c] * hb;
-                        const float dd = x_cur[c] - av[c];
+                        const R dd = x_cur[c] - av[c];
                         fa[5] += dd * dd;
                         if (with_prev) {
                             fa[6] += pl1[c] * ax;
@@ -419,14 +452,14 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                         }
                         if (TRACE) {
                             fa[2] += wtv[c] * g;
-                            fa[3] += __logf(ax + eps);
-                            fa[4] += __logf(g + epsp);
+                            fa[3] += log_(ax + eps);
+                            fa[4] += log_(g + epsp);
                             if (with_prev) fa[8] += ptv[c] * g;
                         }
                     }
                 }
             }
-            float* const sfree = Sc_ring;
+            R* const sfree = Sc_ring;
             Sc_ring = Sn_ring;
             Sn_ring = Sx_ring;
             Sx_ring = sfree;
@@ -439,7 +472,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 for (int q = 0; q < NP1; ++q)
                     if (USED & (1u << q)) {
                         fb[q] += fa[q];
-                        fa[q] = 0.f;
+                        fa[q] = R(0);
                     }
             }
         }
@@ -450,7 +483,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
                 if (USED & (1u << q)) {
                     const double v = warp_sum((double)fb[q]);
                     if (lane == 0) red[w * NP1 + q] += v;
-                    fb[q] = 0.f;
+                    fb[q] = R(0);
                 }
         }
         // every issued plane (k0-1 .. k0+KC) has been waited on
@@ -464,7 +497,7 @@ stencil2_kernel(StencilParams<float> p, const __grid_constant__ CUtensorMap tmx,
 }
 
 // host: mode flags of a sweep and the matching instantiation
-inline int s2_flags(const StencilParams<float>& p) {
+template <typename R> inline int s2_flags(const StencilParams<R>& p) {
     int f = 0;
     if (p.audit) {
         f |= S2_AUDIT;
@@ -478,12 +511,12 @@ inline int s2_flags(const StencilParams<float>& p) {
 
 #define CM_S2_MODES(X) X(0) X(8) X(1) X(9) X(3) X(11) X(5) X(13) X(7) X(15) X(16) X(24)
 
-template <int N> inline cudaError_t stencil2_prepare() {
+template <int N, typename R = float> inline cudaError_t stencil2_prepare() {
     cudaError_t e = cudaSuccess;
 #define CM_S2_ATTR(FL)                                                                         \
     if (e == cudaSuccess)                                                                     \
-        e = cudaFuncSetAttribute(stencil2_kernel<N, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)S2Geo<N>::SMEM);
+        e = cudaFuncSetAttribute(stencil2_kernel<R, N, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)S2GeoT<R, N>::SMEM);
     CM_S2_MODES(CM_S2_ATTR)
 #undef CM_S2_ATTR
     return e;
@@ -506,26 +539,26 @@ inline cudaError_t launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-template <int N>
-inline cudaError_t stencil2_launch(StencilParams<float> p, int grid, cudaStream_t s,
+template <int N, typename R>
+inline cudaError_t stencil2_launch(StencilParams<R> p, int grid, cudaStream_t s,
                                    const CUtensorMap& tmx, const CUtensorMap& tmp,
                                    const CUtensorMap& tmg, const CUtensorMap& tma, bool pdl = false) {
-    p.f_eps = float(p.eps);
-    p.f_epsp = float(p.eps_prime);
-    p.f_mu = float(p.mu);
-    p.f_lr = float(p.lr);
-    p.f_lra = float(p.lr * p.alpha);
-    p.f_beta = float(p.beta);
-    p.f_g2 = float(2.0 * p.gamma);
-    p.f_inv2mu = float(0.5 / p.mu);
-    p.f_hmu = float(0.5 * p.mu);
-    p.f_cg = p.convex ? 0.f : 1.f;
-    p.f_ce = p.convex ? 1.f : float(p.eps_prime);
+    p.f_eps = R(p.eps);
+    p.f_epsp = R(p.eps_prime);
+    p.f_mu = R(p.mu);
+    p.f_lr = R(p.lr);
+    p.f_lra = R(p.lr * p.alpha);
+    p.f_beta = R(p.beta);
+    p.f_g2 = R(2.0 * p.gamma);
+    p.f_inv2mu = R(0.5 / p.mu);
+    p.f_hmu = R(0.5 * p.mu);
+    p.f_cg = p.convex ? R(0) : R(1);
+    p.f_ce = p.convex ? R(1) : R(p.eps_prime);
     switch (s2_flags(p)) {
 #define CM_S2_CASE(FL)                                                                         \
     case FL:                                                                                   \
-        return launch_pdl(pdl, stencil2_kernel<N, FL>, dim3(grid), dim3(S2Geo<N>::NT),          \
-                          S2Geo<N>::SMEM, s, p, tmx, tmp, tmg, tma);
+        return launch_pdl(pdl, stencil2_kernel<R, N, FL>, dim3(grid), dim3(S2GeoT<R, N>::NT),    \
+                          S2GeoT<R, N>::SMEM, s, p, tmx, tmp, tmg, tma);
         CM_S2_MODES(CM_S2_CASE)
 #undef CM_S2_CASE
         default:
@@ -534,9 +567,9 @@ inline cudaError_t stencil2_launch(StencilParams<float> p, int grid, cudaStream_
     return cudaGetLastError();
 }
 
-template <int N> inline cudaError_t stencil2_occupancy(int* occ) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stencil2_kernel<N, S2_AUDIT | S2_PREV>,
-                                                         S2Geo<N>::NT, S2Geo<N>::SMEM);
+template <int N, typename R = float> inline cudaError_t stencil2_occupancy(int* occ) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stencil2_kernel<R, N, S2_AUDIT | S2_PREV>,
+                                                         S2GeoT<R, N>::NT, S2GeoT<R, N>::SMEM);
 }
 
 } // namespace cm

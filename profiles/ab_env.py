@@ -7,7 +7,8 @@ that builds the solver context under that environment, times the per-iteration
 kernels (CUDA events, profiling solve) and the graph-replayed solve, and saves
 the result volume; prints one JSON line per variant plus the relative L2
 difference of each variant's volume against the first (the switches must not
-change results beyond fp32 roundoff)."""
+change results beyond fp32 roundoff). AB_PREC=64 in the environment (or as a
+switch) runs the fp64 parity mode."""
 import itertools
 import json
 import os
@@ -25,7 +26,8 @@ from paper_1905_13408_b200 import synth
 n, iters, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
 p = synth.synthetic_problem(n)
 acc = cm.AccumulatorPair(n, p.numerator, p.weight, True)
-ctx = cm.Context(n, 32)
+import os
+ctx = cm.Context(n, int(os.environ.get("AB_PREC", "32")))
 ctx.set_accumulator(acc)
 s = ctx.scale_data()
 cfg = cm.derive_config(s.s_y, s.s_n, p.eps, p.eps_prime)
@@ -37,7 +39,7 @@ x = ctx.get_volume()
 ctx.set_profiling(True)
 ctx.solve(cfg)
 ms, it = ctx.get_profile()
-np.save(out, x.astype(np.float32))
+np.save(out, x)
 print(json.dumps({"kernels_ms": {k: round(v / it, 4) for k, v in zip(ctx.PROFILE_KERNELS, ms)},
                   "graph_ms_per_iter": round(best, 4)}))
 """
