@@ -35,7 +35,9 @@ for name, m in sorted(acc.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration
     for key, k in MAP:
         if re.search(key, clean):
             per[k]["time_us"] += sum(t) / len(t)
-            per[k]["dram_bytes"] += sum(b) / len(b)
+            # median: the stencil's objective-only epilogue launch (no update
+            # written) is not a per-iteration launch
+            per[k]["dram_bytes"] += sorted(b)[len(b) // 2]
             per[k]["launches"] = len(t)
             break
 traffic_path = Path(__file__).parent / "ncu_traffic.json"
