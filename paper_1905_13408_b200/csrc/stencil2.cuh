@@ -28,6 +28,9 @@
 #ifndef CM_S2_MINB
 #define CM_S2_MINB 4
 #endif
+#ifndef CM_S2_PD
+#define CM_S2_PD 2  // TMA prefetch distance in planes (2 or 3; the ring has 4 slots)
+#endif
 #ifndef CM_S2_MINB_D
 #define CM_S2_MINB_D 3  // fp64: 136 registers (double accumulators and parameters)
 #endif
@@ -62,11 +65,24 @@ __host__ __device__ constexpr int s2_kc(int n, int ci = 128, int minb = CM_S2_MI
 __device__ __forceinline__ float s2abs(float v) { return fabsf(v); }
 __device__ __forceinline__ double s2abs(double v) { return fabs(v); }
 __device__ __forceinline__ float s2min(float a, float b) { return fminf(a, b); }
-__device__ __forceinline__ double s2min(double a, double b) { return fmin(a, b); }
+// fp64: compare-and-select (fmin / fmax carry NaN handling; operands here are finite)
+__device__ __forceinline__ double s2min(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ float s2max(float a, float b) { return fmaxf(a, b); }
-__device__ __forceinline__ double s2max(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ double s2max(double a, double b) { return a > b ? a : b; }
 __device__ __forceinline__ float s2fma(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double s2fma(double a, double b, double c) { return fma(a, b, c); }
+// reciprocal of an operand known positive and normal here ((|x| + eps)(|Dx| + eps'),
+// (|Dx| cg + ce) max(mu, |Dx|), max(mu, |Dx|): eps, eps', mu > 0 are validated):
+// fp64 skips rcp_'s 1/0 guard
+__device__ __forceinline__ float s2rcp(float v) { return rcp_(v); }
+__device__ __forceinline__ double s2rcp(double v) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+    double e = fma(-v, y, 1.0);
+    double z = fma(y, fma(e, e, e), y);
+    e = fma(-v, z, 1.0);
+    return fma(z, e, z);
+}
 
 // R = float: 4 voxels (one float4) per lane, 128-wide x tiles; R = double (the
 // fp64 parity mode): 2 voxels (one double2) per lane, 64-wide x tiles
@@ -192,6 +208,7 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
             issue(k0 - 1);
             issue(k0);
             issue(k0 + 1);
+            if (CM_S2_PD == 3) issue(k0 + 2);
         }
         wait(k0 - 1);
         wait(k0);
@@ -235,7 +252,7 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
                 const R d1 = xq[c] - xlv[c], d2 = xq[c] - yv[c], d3 = xq[c] - zv[c];
                 const R g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
                 const R mx = mu > g ? mu : g;
-                const R s = rcp_(s2fma(g, cg, ce) * mx);  // convex: 1/mx
+                const R s = s2rcp(s2fma(g, cg, ce) * mx);  // convex: 1/mx
                 sv[c] = qin ? s : R(0);
                 gn[c] = g;
                 ds[c] = d1 + d2 + d3;
@@ -255,8 +272,8 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
             const R g = sqrt_(d1 * d1 + d2 * d2 + d3 * d3);
             const R mx = mu > g ? mu : g;
             if (p.wtvf && !convex)
-                return __ldg(p.wtvf + ((size_t)(q + zs) * N + gjr) * N + i0 + CI) * rcp_(mx);
-            return rcp_(s2fma(g, cg, ce) * mx);
+                return __ldg(p.wtvf + ((size_t)(q + zs) * N + gjr) * N + i0 + CI) * s2rcp(mx);
+            return s2rcp(s2fma(g, cg, ce) * mx);
         };
         // per_m_step weights come from a frozen field: s uses w_tv from it
         auto apply_wtvf = [&](int q, R (&sv)[VW], R (&gn)[VW]) {
@@ -266,7 +283,7 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
 #pragma unroll
             for (int c = 0; c < VW; ++c) {
                 const R mx = mu > gn[c] ? mu : gn[c];
-                sv[c] = wt[c] * rcp_(mx);
+                sv[c] = wt[c] * s2rcp(mx);
             }
         };
 
@@ -300,7 +317,10 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
         auto step = [&](int k, R (&x_cur)[VW], R (&s_cur)[VW], R (&gn_cur)[VW],
                         R (&ds_cur)[VW], R (&x_nx)[VW], R (&s_nx)[VW],
                         R (&gn_nx)[VW], R (&ds_nx)[VW]) {
-            if (tid == 0) issue(k + 2);  // slot of plane k-2: released by the previous barrier
+            // prefetch distance 2: the slot of plane k-2 was released by the previous
+            // barrier; distance 3 (CM_S2_PD=3): plane k+3 goes to the slot of k-1
+            // after this step's barrier (all four slots in use, no more shared memory)
+            if (CM_S2_PD == 2 && tid == 0) issue(k + 2);
             wait(k + 1);
             // ---- s of plane k+1 on this warp's row
             s_row(k + 1, x_nx, s_nx, gn_nx, ds_nx);
@@ -311,6 +331,7 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
                 if (halo && lane <= TJ) Sn[lane * SW + CI] = s_col(k + 1);
             }
             __syncthreads();
+            if (CM_S2_PD == 3 && tid == 0) issue(k + 3);
             if (!halo && row_in) {
                 // ---- voxel (j, k): update, prox, partials
                 const R* Sc = Sc_ring;
@@ -364,12 +385,12 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
                     if (p.wtvf) {
                         if (col_in) V::ldg(p.wtvf + gidx, wtv);
 #pragma unroll
-                        for (int c = 0; c < VW; ++c) wl1[c] = rcp_(s2abs(ws[c]) + eps);
+                        for (int c = 0; c < VW; ++c) wl1[c] = s2rcp(s2abs(ws[c]) + eps);
                     } else {
 #pragma unroll
                         for (int c = 0; c < VW; ++c) {
                             const R a = s2abs(ws[c]) + eps, b = gn_cur[c] + epsp;
-                            const R r = rcp_(a * b);
+                            const R r = s2rcp(a * b);
                             wl1[c] = b * r;
                             wtv[c] = a * r;
                         }
@@ -431,7 +452,7 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
                             const R e1 = pc[c] - pl[c], e2 = pc[c] - py[c], e3 = pc[c] - xp_prev[c];
                             const R a = s2abs(pc[c]) + eps;
                             const R b = sqrt_(e1 * e1 + e2 * e2 + e3 * e3) + epsp;
-                            const R r = rcp_(a * b);
+                            const R r = s2rcp(a * b);
                             pl1[c] = b * r;
                             ptv[c] = a * r;
                             xp_prev[c] = pc[c];
