@@ -429,6 +429,7 @@ struct Impl final : ImplBase {
     // CTA start, 0.434 -> 0.413 ms; S rows of later tiles or W / Yh of a later
     // tile are slower; CM_Z_PFW=-1 disables)
     int z_pf = std::getenv("CM_Z_PF") ? std::atoi(std::getenv("CM_Z_PF")) : 0;
+    CUtensorMap* tmz_S_d = nullptr;  // S z-box map in device memory (CM_Z_PF with CM_Z_PFT=1)
     int z_pfw = std::getenv("CM_Z_PFW") ? std::atoi(std::getenv("CM_Z_PFW")) : 0;
     cudaGraphExec_t gexec = nullptr;  // instantiated 6-iteration chunk (reused while gkey holds)
     std::vector<uint64_t> gkey;
@@ -473,7 +474,7 @@ struct Impl final : ImplBase {
         if (gexec) cudaGraphExecDestroy(gexec);
         void* ps[] = {X[0], X[1], X[2], XF[0], XF[1], YF[0], YF[1], x0keep, anchor, winit, wtvf, gbuf, S, W,
                       Wn, Yh, Yn, Z0, twN, twF4, twI4, stage, part1, part3, part_acc, maxes, st, trace_d,
-                      theta_d, Q0, fcnt, yzy_items_d, yzy_ctr};
+                      theta_d, Q0, fcnt, yzy_items_d, yzy_ctr, tmz_S_d};
         for (void* p : ps)
             if (p) cudaFree(p);
         if (flags_h) cudaFreeHost(flags_h);
@@ -689,6 +690,12 @@ struct Impl final : ImplBase {
             CK(cudaDeviceGetAttribute(&smst, cudaDevAttrMultiProcessorCount, devt));
             yt_grid = std::max(1, std::min(YG_::NTILES, smst * std::max(occt, 1)));
             CKS(yt_make_map(S, N, YG_::TW, YG_::BOXB, &tmy_S));
+            if (z_pf > 0 && std::getenv("CM_Z_PFT")) {
+                CUtensorMap m{};
+                CKS(yt_make_map(S, N, ZGeo<R, N>::TW, 1, &m, N < 256 ? N : 256));
+                CKS(dalloc(reinterpret_cast<char**>(&tmz_S_d), sizeof(CUtensorMap)));
+                CK(cudaMemcpy(tmz_S_d, &m, sizeof(m), cudaMemcpyHostToDevice));
+            }
         }
         CKS(dalloc(&part_acc, 2 * 148 * 32));
         CKS(dalloc(&maxes, 4));
@@ -813,6 +820,7 @@ struct Impl final : ImplBase {
         ZMParams<R> p{S, Z0, W, Wn, Yh, Yn, twN, twF4, twI4, part, s, N, Q0, Nh, 0};
         p.pf = z_pf;
         p.pfw = z_pfw;
+        p.tmS = tmz_S_d;
         dim3 grid(Nh / ZG::TW, N);
         CK(launch_pdl(use_pdl, zmain_kernel<R, N, MODE>, grid, dim3(ZG::NT), ZG::SMEM_MAIN, stream, p));
         if constexpr (MODE != ZM_FWD)

@@ -115,13 +115,13 @@ template <int N> inline cudaError_t yt_prepare() {
 }
 
 // packed spectrum S[k][b][h] (float2, Nh per row) as a 3D float map {2 Nh, N, N}
-inline int yt_make_map(void* ptr, int N, int tw, int boxb, CUtensorMap* out) {
+inline int yt_make_map(void* ptr, int N, int tw, int boxb, CUtensorMap* out, int boxc = 1) {
     EncodeTiledFn enc = encode_tiled_fn();
     if (!enc) return fail(CM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int Nh = N / 2;
     const cuuint64_t dims[3] = {(cuuint64_t)2 * Nh, (cuuint64_t)N, (cuuint64_t)N};
     const cuuint64_t strides[2] = {(cuuint64_t)2 * Nh * 4, (cuuint64_t)N * 2 * Nh * 4};
-    const cuuint32_t box[3] = {(cuuint32_t)(2 * tw), (cuuint32_t)boxb, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * tw), (cuuint32_t)boxb, (cuuint32_t)boxc};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

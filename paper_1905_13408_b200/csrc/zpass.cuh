@@ -41,6 +41,10 @@ template <typename R> struct ZMParams {
     // one GPU: L2 prefetch lookahead in tiles for S (rows of tile + pf) and for
     // the contiguous W / Yh tiles (tile + pfw; -1: off); 0 / -1 disable
     int pf = 0, pfw = -1;
+    // one GPU, fp32: S as a 3D tensor map (float pairs) with z boxes {2 TW, 1, <= 256}
+    // in global memory; the S prefetch of tile + pf is then one TMA
+    // cp.async.bulk.prefetch.tensor per 256 rows instead of one LSU prefetch per row
+    const CUtensorMap* tmS = nullptr;
 };
 
 #ifndef CM_Z_E8
@@ -126,7 +130,17 @@ __global__ void __launch_bounds__(ZGeo<R, N>::NT, ZGeo<R, N>::MINB) zmain_kernel
         // pass is latency bound with two CTAs per SM, so the S rows of tile + pf
         // and the z-tiled W / Yh block of tile + pfw are requested ahead
         const int tl = blockIdx.y * gridDim.x + blockIdx.x, ntl = (Nh / ZGeo<R, N>::TW) * NR;
-        if (p.pf > 0 && tl + p.pf < ntl) {
+        if (p.pf > 0 && tl + p.pf < ntl && p.tmS) {
+            if (threadIdx.x == 0) {
+                const int t2 = tl + p.pf, ntx = Nh / ZGeo<R, N>::TW;
+                const int hf = 2 * (t2 % ntx) * ZGeo<R, N>::TW, b2 = t2 / ntx;
+                for (int c0 = 0; c0 < N; c0 += 256)
+                    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                                     reinterpret_cast<uint64_t>(p.tmS)),
+                                 "r"(hf), "r"(b2), "r"(c0)
+                                 : "memory");
+            }
+        } else if (p.pf > 0 && tl + p.pf < ntl) {
             const int t2 = tl + p.pf;
             const Cx<R>* rowp = p.S + (size_t)(t2 / (Nh / ZGeo<R, N>::TW)) * Nh +
                                 (t2 % (Nh / ZGeo<R, N>::TW)) * ZGeo<R, N>::TW;
