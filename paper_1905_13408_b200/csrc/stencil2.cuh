@@ -488,7 +488,9 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
         for (int k = k0; k < k0 + KC; k += 2) {
             step(k, x_cur, s_cur, gn_cur, ds_cur, x_nb, s_nb, gn_nb, ds_nb);
             step(k + 1, x_nb, s_nb, gn_nb, ds_nb, x_cur, s_cur, gn_cur, ds_cur);
-            if (USED && ((k + 1 - k0) & 7) == 7) {
+            // fp32: flush the 8-plane partials into the tile partials (bounded
+            // rounding); fp64 accumulates the tile in fa directly (fewer registers)
+            if (sizeof(R) == 4 && USED && ((k + 1 - k0) & 7) == 7) {
 #pragma unroll
                 for (int q = 0; q < NP1; ++q)
                     if (USED & (1u << q)) {
@@ -502,9 +504,10 @@ stencil2_kernel(StencilParams<R> p, const __grid_constant__ CUtensorMap tmx,
 #pragma unroll
             for (int q = 0; q < NP1; ++q)
                 if (USED & (1u << q)) {
-                    const double v = warp_sum((double)fb[q]);
+                    const double v = warp_sum(sizeof(R) == 4 ? (double)fb[q] : (double)fa[q]);
                     if (lane == 0) red[w * NP1 + q] += v;
                     fb[q] = R(0);
+                    if (sizeof(R) == 8) fa[q] = R(0);
                 }
         }
         // every issued plane (k0-1 .. k0+KC) has been waited on
