@@ -37,6 +37,9 @@
 #ifndef CM_S2_TJ
 #define CM_S2_TJ 4  // rows per CTA (+1 halo-row warp); 4 CTAs per SM (8: 2 CTAs, 3.5% slower)
 #endif
+#ifndef CM_S2_TJ_D
+#define CM_S2_TJ_D 4  // fp64 rows per CTA
+#endif
 
 namespace cm {
 
@@ -44,13 +47,13 @@ namespace cm {
 // busiest CTA slot (148 SMs x CM_S2_MINB), ceil(tiles / slots) x (KC + 2 for the
 // march prologue); ties keep the longer march. 512^3 / 384^3 / 256^3: 64; 128^3:
 // 8 (64-plane marches ran 64 CTAs for the whole sweep: 57 -> 19 us)
-__host__ __device__ constexpr int s2_kc(int n, int ci = 128, int minb = CM_S2_MINB) {
+__host__ __device__ constexpr int s2_kc(int n, int ci = 128, int minb = CM_S2_MINB, int tj = CM_S2_TJ) {
     if (n < 64) return n;
     int best = 64;
     long best_cost = -1;
     for (int kc = 64; kc >= 8; kc /= 2) {
         if (n % kc) continue;
-        const long tiles = (long)((n + ci - 1) / ci) * (n / CM_S2_TJ) * (n / kc);
+        const long tiles = (long)((n + ci - 1) / ci) * (n / tj) * (n / kc);
         const long slots = 148L * minb;
         const long cost = (tiles + slots - 1) / slots * (kc + 2);
         if (best_cost < 0 || cost < best_cost) {
@@ -90,8 +93,8 @@ template <typename R, int N> struct S2GeoT {
     static constexpr int VW = 16 / (int)sizeof(R);  // voxels per lane
     static constexpr int CI = 32 * VW;
     static constexpr int MINB = sizeof(R) == 4 ? CM_S2_MINB : CM_S2_MINB_D;
-    static constexpr int TJ = CM_S2_TJ;
-    static constexpr int KC = s2_kc(N, CI, MINB);  // planes per march
+    static constexpr int TJ = sizeof(R) == 4 ? CM_S2_TJ : CM_S2_TJ_D;
+    static constexpr int KC = s2_kc(N, CI, MINB, TJ);  // planes per march
     static constexpr int NW = TJ + 1;            // + halo-row warp
     static constexpr int NT = NW * 32;
     static constexpr int XW = CI + 2 * VW;       // slab row: global i0-VW .. i0+CI+VW-1
